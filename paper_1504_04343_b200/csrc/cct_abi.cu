@@ -1,0 +1,498 @@
+// cct_abi.cu -- the extern "C" boundary (include/cct.h): argument validation,
+// workspace planning and the per-pass kernel sequences of the lowered
+// convolution (lower -> tcgen05 3xTF32 GEMM -> lift, and the adjoints).
+//
+// Pass / lowering -> GEMM mapping:
+//   FWD  T1: M=b m^2  N=o     K=k^2 d  A=Dhat1 (K-major)  B=W (K-major)   C -> y NCHW (lift fused)
+//   FWD  T2: M=b R m  N=k o   K=k d    A=Dhat2            B=W as (ok x kd) C -> Rhat^T, lift_t2
+//   FWD  T3: M=b R^2  N=k^2 o K=d      A=Dhat3 (=Xp)      B=W as (ok^2 x d) C -> Rhat^T, lift_t3
+//   BWD_DATA: M=cols(Dhat) N=rows K=ncols  A=W (MN-major) B=dRhat^T (MN-major) C -> dDhat, col2im
+//   BWD_WEIGHT: M=cols N=ncols K=rows   A=Dhat (MN-major) B=dRhat^T (K-major) C -> dW (split-K)
+#include <cstdio>
+#include <sstream>
+#include <string>
+
+#include "cct.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "lowering.cuh"
+#include "reduce.cuh"
+
+namespace cct {
+uint64_t launch_count();
+void reset_launch_count();
+}  // namespace cct
+
+using namespace cct;
+
+namespace {
+
+cct_status fail(cct_status s, const std::string& msg) {
+    set_error(msg);
+    return s;
+}
+
+cct_status cuda_status(cudaError_t e, const char* where) {
+    if (e == cudaSuccess) return CCT_OK;
+    return fail(CCT_ERR_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+#define CCT_TRY(expr, where)                                     \
+    do {                                                         \
+        cct_status _s = cuda_status((expr), (where));            \
+        if (_s != CCT_OK) return _s;                             \
+    } while (0)
+
+std::string desc_str(const cct_conv_desc* d) {
+    std::ostringstream os;
+    os << "(n=" << d->n << ", k=" << d->k << ", d=" << d->d << ", o=" << d->o << ", b=" << d->b
+       << ", stride=" << d->stride << ", pad=" << d->pad << ")";
+    return os.str();
+}
+
+cct_status check_desc(const cct_conv_desc* d) {
+    if (!d) return fail(CCT_ERR_CONFIG, "null conv descriptor");
+    if (d->k < 1 || d->d < 1 || d->o < 1 || d->b < 1 || d->stride < 1 || d->pad < 0 ||
+        d->k > d->n + 2 * d->pad)
+        return fail(CCT_ERR_CONFIG, "invalid layer config " + desc_str(d) +
+                                        ": need 1 <= k <= n + 2 pad, d >= 1, o >= 1, b >= 1, stride >= 1, pad >= 0");
+    return CCT_OK;
+}
+
+Geo geo_of(const cct_conv_desc* d) {
+    Geo g;
+    g.b = d->b; g.n = d->n; g.d = d->d; g.k = d->k; g.o = d->o; g.s = d->stride; g.p = d->pad;
+    g.N = g.n + 2 * g.p;
+    g.m = (g.N - g.k) / g.s + 1;
+    g.R = g.s * (g.m - 1) + g.k;
+    return g;
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// bump allocator over the caller's workspace; base == nullptr -> size query.
+// Real workspaces are first aligned up to 256 bytes (hence +256 in the size).
+struct Ws {
+    char* base;
+    size_t off = 0;
+    explicit Ws(void* b)
+        : base(b ? reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(b) + 255) & ~uintptr_t(255))
+                 : nullptr) {}
+    float* take(int64_t floats) {
+        off = (off + 255) & ~size_t(255);
+        float* p = base ? reinterpret_cast<float*>(base + off) : nullptr;
+        off += size_t(floats) * sizeof(float);
+        return p;
+    }
+};
+
+cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
+
+int resolve(const cct_conv_desc* d, cct_lowering l, cct_pass pass) {
+    if (l == CCT_LOWER_T1 || l == CCT_LOWER_T2 || l == CCT_LOWER_T3) return int(l);
+    cct_calibration cal;
+    cct_calibration_default(&cal);
+    cct_lowering out = CCT_LOWER_T1;
+    if (cct_select_lowering(d, &cal, int(pass), &out, nullptr) != CCT_OK) return 1;
+    return int(out);
+}
+
+// Lowered-matrix geometry of one type.
+struct Lowered {
+    int64_t rows, cols, ncols;  // Dhat rows x cols, Khat^T rows (= ncols)
+    int64_t ldc;                // row stride of Dhat / dDhat / W' (floats, multiple of 4)
+    int64_t ldr;                // row stride of Rhat^T / dRhat^T (floats, multiple of 4)
+    RowMap rm;
+};
+
+Lowered lowered_of(const Geo& g, int type) {
+    Lowered L;
+    L.rm = rowmap_internal(g, type);
+    L.rows = g.b * L.rm.rpi;
+    L.cols = lowered_cols(g, type);
+    L.ncols = lowered_ncols(g, type);
+    L.ldc = rup4(L.cols);
+    L.ldr = rup4(L.rows);
+    return L;
+}
+
+// W viewed as (ncols x cols) row-major; zero-copy when the row stride is TMA-legal.
+const float* weights_view(const Lowered& L, const float* w, Ws& ws, cudaStream_t st, int64_t* ld,
+                          cudaError_t* err) {
+    *err = cudaSuccess;
+    if (L.cols % 4 == 0 && aligned16(w)) {
+        *ld = L.cols;
+        return w;
+    }
+    float* wp = ws.take(L.ncols * L.ldc);
+    *ld = L.ldc;
+    if (ws.base) *err = pad_rows(w, L.ncols, L.cols, L.cols, wp, L.ldc, st);
+    return wp;
+}
+
+// Dhat in internal order; T3 with no padding is the input itself.
+const float* dhat_of(const Geo& g, int type, const Lowered& L, const float* x, Ws& ws, cudaStream_t st,
+                     cudaError_t* err) {
+    *err = cudaSuccess;
+    if (type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(x)) return x;
+    float* dh = ws.take(L.rows * L.ldc);
+    if (ws.base) *err = lower(g, type, L.rm, x, dh, L.ldc, st);
+    return dh;
+}
+
+// Run gp writing a flat output span of `span` floats at `out`.  Reductions
+// longer than the accumulation-chain cap (kMaxChainKB k-blocks) are split and
+// reduced in fp32 round-to-nearest (deterministic order).  In planning mode
+// (ws.base == nullptr) only the workspace is reserved.
+cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStream_t st, const char* what) {
+    const int64_t kb = (gp.K + kBK - 1) / kBK;
+    const int splits = int((kb + kMaxChainKB - 1) / kMaxChainKB);
+    float* parts = splits > 1 ? ws.take(int64_t(splits) * span) : nullptr;
+    if (!ws.base) return CCT_OK;
+    gp.C.ptr = splits > 1 ? parts : out;
+    gp.C.s_split = span;
+    gp.splits = splits;
+    CCT_TRY(run_gemm(gp, st), what);
+    if (splits > 1) CCT_TRY(splitk_reduce(parts, span, splits, 1, span, span, out, span, st), "split-K reduce");
+    return CCT_OK;
+}
+
+int wgrad_splits(const Lowered& L) {
+    const int bn = choose_bn(L.ncols);
+    return choose_splits(L.cols, L.ncols, L.rows, num_sms(), bn);
+}
+
+// ---------------------------------------------------------------------------
+// the three passes; ws.base == nullptr plans sizes only
+// ---------------------------------------------------------------------------
+
+cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float* y, Ws& ws,
+                   cudaStream_t st) {
+    const Lowered L = lowered_of(g, type);
+    cudaError_t e;
+    int64_t ldw;
+    const float* wv = weights_view(L, w, ws, st, &ldw, &e);
+    CCT_TRY(e, "pad weights");
+    const float* dh = dhat_of(g, type, L, x, ws, st, &e);
+    CCT_TRY(e, "lower");
+    const int64_t ldd = (dh == x) ? g.d : L.ldc;
+    GemmProblem gp;
+    gp.M = L.rows;
+    gp.N = L.ncols;
+    gp.K = L.cols;
+    gp.A = {dh, ldd, Major::K};
+    gp.B = {wv, ldw, Major::K};
+    float* rht = nullptr;
+    float* out;
+    int64_t span;
+    if (type == 1) {
+        // lift_t1 is a reshape: write NCHW straight from the epilogue
+        out = y;
+        span = g.b * g.o * g.m * g.m;
+        gp.C.mdiv = g.m * g.m;
+        gp.C.s_mq = g.o * g.m * g.m;
+        gp.C.s_mr = 1;
+        gp.C.s_n = g.m * g.m;
+    } else {
+        rht = ws.take(L.ncols * L.ldr);
+        out = rht;
+        span = L.ncols * L.ldr;
+        gp.C.s_mr = 1;
+        gp.C.s_n = L.ldr;
+    }
+    cct_status s = gemm_capped(gp, out, span, ws, st, "gemm (fwd)");
+    if (s != CCT_OK || !ws.base) return s;
+    if (type != 1) CCT_TRY(lift(g, type, L.rm, rht, 1, L.ldr, y, st), "lift");
+    return CCT_OK;
+}
+
+cct_status run_bwd_data(const Geo& g, int type, const float* dy, const float* w, float* dx, Ws& ws,
+                        cudaStream_t st) {
+    const Lowered L = lowered_of(g, type);
+    cudaError_t e;
+    int64_t ldw;
+    const float* wv = weights_view(L, w, ws, st, &ldw, &e);
+    CCT_TRY(e, "pad weights");
+    float* drt = ws.take(L.ncols * L.ldr);
+    const bool direct = (type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(dx));
+    float* dd = direct ? dx : ws.take(L.rows * L.ldc);
+    const int64_t ldd = direct ? g.d : L.ldc;
+    if (ws.base) CCT_TRY(expand(g, type, dy, drt, L.ldr, st), "expand");
+    GemmProblem gp;
+    gp.M = L.cols;
+    gp.N = L.rows;
+    gp.K = L.ncols;
+    gp.A = {wv, ldw, Major::MN};
+    gp.B = {drt, L.ldr, Major::MN};
+    gp.C.s_mr = 1;
+    gp.C.s_n = ldd;
+    cct_status s = gemm_capped(gp, dd, L.rows * ldd, ws, st, "gemm (bwd-data)");
+    if (s != CCT_OK || !ws.base) return s;
+    if (!direct) CCT_TRY(col2im(g, type, dd, ldd, dx, st), "col2im");
+    return CCT_OK;
+}
+
+cct_status run_bwd_weight(const Geo& g, int type, const float* x, const float* dy, float* dw, Ws& ws,
+                          cudaStream_t st) {
+    const Lowered L = lowered_of(g, type);
+    cudaError_t e;
+    const float* dh = dhat_of(g, type, L, x, ws, st, &e);
+    CCT_TRY(e, "lower");
+    const int64_t ldd = (dh == x) ? g.d : L.ldc;
+    float* drt = ws.take(L.ncols * L.ldr);
+    const int splits = wgrad_splits(L);
+    const int64_t wsize = L.ncols * L.cols;
+    float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
+    if (!ws.base) return CCT_OK;
+    CCT_TRY(expand(g, type, dy, drt, L.ldr, st), "expand");
+    GemmProblem gp;
+    gp.M = L.cols;
+    gp.N = L.ncols;
+    gp.K = L.rows;
+    gp.A = {dh, ldd, Major::MN};
+    gp.B = {drt, L.ldr, Major::K};
+    gp.C.ptr = parts;
+    gp.C.s_mr = 1;
+    gp.C.s_n = L.cols;
+    gp.C.s_split = wsize;
+    gp.splits = splits;
+    CCT_TRY(run_gemm(gp, st), "gemm (bwd-weight)");
+    if (splits > 1) CCT_TRY(splitk_reduce(parts, wsize, splits, 1, wsize, wsize, dw, wsize, st), "split-K reduce");
+    return CCT_OK;
+}
+
+cct_status check_ptrs(std::initializer_list<const void*> ps) {
+    for (const void* p : ps)
+        if (!p) return fail(CCT_ERR_CONFIG, "null tensor pointer");
+    return CCT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int cct_abi_version(void) { return CCT_ABI_VERSION; }
+void cct_profile_enable(int on) { cct::profile_enable(on != 0); }
+void cct_profile_read(double* ms, double* flops, double* bytes, uint64_t* launches, int reset) {
+    cct::profile_read(ms, flops, bytes, launches, reset != 0);
+}
+const char* cct_last_error(void) { return cct::last_error(); }
+uint64_t cct_launch_count(void) { return cct::launch_count(); }
+void cct_reset_launch_count(void) { cct::reset_launch_count(); }
+
+cct_status cct_conv_desc_init(cct_conv_desc* desc, int64_t n, int64_t k, int64_t d, int64_t o, int64_t b,
+                              int64_t stride, int64_t pad) {
+    if (!desc) return fail(CCT_ERR_CONFIG, "null conv descriptor");
+    desc->n = n; desc->k = k; desc->d = d; desc->o = o; desc->b = b; desc->stride = stride; desc->pad = pad;
+    desc->m = desc->R = 0;
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    const Geo g = geo_of(desc);
+    desc->m = g.m;
+    desc->R = g.R;
+    return CCT_OK;
+}
+
+cct_status cct_workspace_size(const cct_conv_desc* desc, cct_lowering lowering, cct_pass pass, size_t* bytes) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    if (!bytes) return fail(CCT_ERR_CONFIG, "null size pointer");
+    const Geo g = geo_of(desc);
+    const int type = resolve(desc, lowering, pass);
+    Ws ws(nullptr);
+    // dummy, 16-byte aligned non-null pointers so zero-copy decisions match the real call
+    const float* dummy = reinterpret_cast<const float*>(uintptr_t(256));
+    switch (pass) {
+    case CCT_PASS_FWD: s = run_fwd(g, type, dummy, dummy, nullptr, ws, nullptr); break;
+    case CCT_PASS_BWD_DATA: s = run_bwd_data(g, type, dummy, dummy, reinterpret_cast<float*>(uintptr_t(256)), ws, nullptr); break;
+    case CCT_PASS_BWD_WEIGHT: s = run_bwd_weight(g, type, dummy, dummy, nullptr, ws, nullptr); break;
+    default: return fail(CCT_ERR_CONFIG, "unknown pass");
+    }
+    *bytes = ws.off + 256;
+    return s;
+}
+
+static cct_status run_pass(const cct_conv_desc* desc, cct_lowering lowering, cct_pass pass, const float* a,
+                           const float* b, float* out, void* wsp, size_t ws_bytes, void* stream) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    if ((s = check_ptrs({a, b, out})) != CCT_OK) return s;
+    if (!aligned16(a) || !aligned16(b) || !aligned16(out))
+        return fail(CCT_ERR_CONFIG, "tensor pointers must be 16-byte aligned (cudaMalloc / torch allocations are)");
+    size_t need = 0;
+    if ((s = cct_workspace_size(desc, lowering, pass, &need)) != CCT_OK) return s;
+    if (ws_bytes < need || !wsp) {
+        std::ostringstream os;
+        os << "workspace too small: need " << need << " bytes, got " << ws_bytes << " for " << desc_str(desc);
+        return fail(CCT_ERR_RESOURCE, os.str());
+    }
+    const Geo g = geo_of(desc);
+    const int type = resolve(desc, lowering, pass);
+    Ws ws(wsp);
+    cudaStream_t st = as_stream(stream);
+    switch (pass) {
+    case CCT_PASS_FWD: return run_fwd(g, type, a, b, out, ws, st);
+    case CCT_PASS_BWD_DATA: return run_bwd_data(g, type, a, b, out, ws, st);
+    default: return run_bwd_weight(g, type, a, b, out, ws, st);
+    }
+}
+
+cct_status cct_conv_fwd(const cct_conv_desc* desc, cct_lowering lowering, const float* x, const float* w,
+                        float* y, void* ws, size_t ws_bytes, void* stream) {
+    return run_pass(desc, lowering, CCT_PASS_FWD, x, w, y, ws, ws_bytes, stream);
+}
+
+cct_status cct_conv_bwd_data(const cct_conv_desc* desc, cct_lowering lowering, const float* dy, const float* w,
+                             float* dx, void* ws, size_t ws_bytes, void* stream) {
+    return run_pass(desc, lowering, CCT_PASS_BWD_DATA, dy, w, dx, ws, ws_bytes, stream);
+}
+
+cct_status cct_conv_bwd_weight(const cct_conv_desc* desc, cct_lowering lowering, const float* x,
+                               const float* dy, float* dw, void* ws, size_t ws_bytes, void* stream) {
+    return run_pass(desc, lowering, CCT_PASS_BWD_WEIGHT, x, dy, dw, ws, ws_bytes, stream);
+}
+
+// ---- phase-level API ---------------------------------------------------------
+
+static cct_status phase_geo(const cct_conv_desc* desc, cct_lowering lowering, cct_row_order order, Geo* g,
+                            RowMap* rm) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    if (lowering < CCT_LOWER_T1 || lowering > CCT_LOWER_T3)
+        return fail(CCT_ERR_CONFIG, "phase API needs an explicit lowering type (1, 2 or 3)");
+    *g = geo_of(desc);
+    if (order == CCT_ROWS_SPEC) {
+        if (g->s != 1 || g->p != 0)
+            return fail(CCT_ERR_UNSUPPORTED, "SPEC row order is defined for stride 1, pad 0 only (SPEC.md:85)");
+        *rm = rowmap_spec(*g, int(lowering));
+    } else {
+        *rm = rowmap_internal(*g, int(lowering));
+    }
+    return CCT_OK;
+}
+
+cct_status cct_lowered_shape(const cct_conv_desc* desc, cct_lowering lowering, cct_row_order order,
+                             int64_t* rows, int64_t* cols, int64_t* kcols) {
+    Geo g;
+    RowMap rm;
+    cct_status s = phase_geo(desc, lowering, order, &g, &rm);
+    if (s != CCT_OK) return s;
+    if (rows) *rows = g.b * rm.rpi;
+    if (cols) *cols = lowered_cols(g, int(lowering));
+    if (kcols) *kcols = lowered_ncols(g, int(lowering));
+    return CCT_OK;
+}
+
+cct_status cct_lower(const cct_conv_desc* desc, cct_lowering lowering, cct_row_order order, const float* x,
+                     float* dhat, int64_t ld, void* stream) {
+    Geo g;
+    RowMap rm;
+    cct_status s = phase_geo(desc, lowering, order, &g, &rm);
+    if (s != CCT_OK) return s;
+    if ((s = check_ptrs({x, dhat})) != CCT_OK) return s;
+    if (ld < lowered_cols(g, int(lowering))) return fail(CCT_ERR_CONFIG, "ld smaller than the lowered row length");
+    return cuda_status(lower(g, int(lowering), rm, x, dhat, ld, as_stream(stream)), "lower");
+}
+
+cct_status cct_lower_khat(const cct_conv_desc* desc, cct_lowering lowering, const float* w, float* khat,
+                          void* stream) {
+    Geo g;
+    RowMap rm;
+    cct_status s = phase_geo(desc, lowering, CCT_ROWS_INTERNAL, &g, &rm);
+    if (s != CCT_OK) return s;
+    if ((s = check_ptrs({w, khat})) != CCT_OK) return s;
+    const int64_t cols = lowered_cols(g, int(lowering)), ncols = lowered_ncols(g, int(lowering));
+    // KernelBank storage is Khat^T (ncols x cols); Khat is its transpose
+    return cuda_status(transpose(w, ncols, cols, cols, khat, ncols, as_stream(stream)), "transpose");
+}
+
+cct_status cct_lift(const cct_conv_desc* desc, cct_lowering lowering, cct_row_order order, const float* rhat,
+                    int64_t ld, float* y, void* stream) {
+    Geo g;
+    RowMap rm;
+    cct_status s = phase_geo(desc, lowering, order, &g, &rm);
+    if (s != CCT_OK) return s;
+    if ((s = check_ptrs({rhat, y})) != CCT_OK) return s;
+    if (ld < lowered_ncols(g, int(lowering))) return fail(CCT_ERR_CONFIG, "ld smaller than the Rhat row length");
+    return cuda_status(lift(g, int(lowering), rm, rhat, ld, 1, y, as_stream(stream)), "lift");
+}
+
+// ---- GEMM (multiply replacement) ---------------------------------------------
+
+static cct_status gemm_common(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+                              int64_t ldb, float* C, int64_t ldc, int split_k, void* ws, size_t ws_bytes,
+                              int passes, void* stream) {
+    if (M < 0 || N < 0 || K < 0) return fail(CCT_ERR_CONFIG, "negative GEMM extent");
+    if (M == 0 || N == 0) return CCT_OK;
+    if (!A || !B || !C) return fail(CCT_ERR_CONFIG, "null matrix pointer");
+    if (lda < K || ldb < N || ldc < N) return fail(CCT_ERR_CONFIG, "leading dimension smaller than the row length");
+    if (lda % 4 || ldb % 4 || !aligned16(A) || !aligned16(B))
+        return fail(CCT_ERR_CONFIG, "A/B must be 16-byte aligned with lda, ldb multiples of 4 (TMA)");
+    cudaStream_t st = as_stream(stream);
+    if (K == 0) {
+        return cuda_status(cudaMemset2DAsync(C, size_t(ldc) * 4, 0, size_t(N) * 4, size_t(M), st), "memset");
+    }
+    // Orientation: lanes run over N (columns of C are contiguous):
+    //   C^T (N x M) = B^T (N x K) * A^T:  A' = B stored (K rows x N) -> MN-major,
+    //   B' = A stored (M rows x K) -> K-major, C'(n, m) at C + m*ldc + n.
+    GemmProblem gp;
+    gp.M = N;
+    gp.N = M;
+    gp.K = K;
+    gp.A = {B, ldb, Major::MN};
+    gp.B = {A, lda, Major::K};
+    gp.passes = passes;
+    const int bn = choose_bn(M);
+    int splits = split_k > 0 ? split_k : choose_splits(N, M, K, num_sms(), bn);
+    if (passes != 3) splits = 1;
+    if (splits > 1) {
+        const size_t need = size_t(splits) * size_t(M) * size_t(N) * 4;
+        if (!ws || ws_bytes < need) splits = 1;  // degrade gracefully: no workspace, no split
+    }
+    if (splits > 1) {
+        float* parts = static_cast<float*>(ws);
+        gp.C = {parts, INT64_MAX, 0, 1, N, M * N};
+        gp.splits = splits;
+        CCT_TRY(run_gemm(gp, st), "gemm");
+        return cuda_status(splitk_reduce(parts, M * N, splits, M, N, N, C, ldc, st), "split-K reduce");
+    }
+    gp.C = {C, INT64_MAX, 0, 1, ldc, 0};
+    return cuda_status(run_gemm(gp, st), "gemm");
+}
+
+cct_status cct_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int split_k, size_t* bytes) {
+    if (!bytes) return fail(CCT_ERR_CONFIG, "null size pointer");
+    const int splits = split_k > 0 ? split_k : choose_splits(N, M, K, num_sms(), choose_bn(M));
+    *bytes = splits > 1 ? size_t(splits) * size_t(M) * size_t(N) * 4 : 0;
+    return CCT_OK;
+}
+
+cct_status cct_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B, int64_t ldb,
+                    float* C, int64_t ldc, int split_k, void* ws, size_t ws_bytes, void* stream) {
+    return gemm_common(M, N, K, A, lda, B, ldb, C, ldc, split_k, ws, ws_bytes, 3, stream);
+}
+
+cct_status cct_gemm_passes(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+                           int64_t ldb, float* C, int64_t ldc, int passes, void* stream) {
+    if (passes != 1 && passes != 3) return fail(CCT_ERR_CONFIG, "passes must be 1 or 3");
+    return gemm_common(M, N, K, A, lda, B, ldb, C, ldc, 1, nullptr, 0, passes, stream);
+}
+
+cct_status cct_debug_gemm(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, int a_major,
+                          const float* B, int64_t ldb, int b_major, float* C, int64_t ldc_m, int64_t ldc_n,
+                          int passes, int bn, void* stream) {
+    if (M <= 0 || N <= 0 || K <= 0 || !A || !B || !C) return fail(CCT_ERR_CONFIG, "bad debug gemm arguments");
+    if (lda % 4 || ldb % 4 || !aligned16(A) || !aligned16(B)) return fail(CCT_ERR_CONFIG, "TMA alignment");
+    GemmProblem gp;
+    gp.M = M;
+    gp.N = N;
+    gp.K = K;
+    gp.A = {A, lda, a_major ? Major::MN : Major::K};
+    gp.B = {B, ldb, b_major ? Major::MN : Major::K};
+    gp.C = {C, INT64_MAX, 0, ldc_m, ldc_n, 0};
+    gp.passes = passes;
+    gp.bn = bn;
+    return cuda_status(run_gemm(gp, as_stream(stream)), "gemm");
+}
+
+}  // extern "C"

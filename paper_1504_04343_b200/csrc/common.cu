@@ -1,0 +1,92 @@
+// common.cu -- device property cache, launch counter, thread-local error text.
+#include "common.cuh"
+
+#include <atomic>
+#include <mutex>
+#include <vector>
+
+namespace cct {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+int g_sms[64] = {0};
+}  // namespace
+
+int num_sms() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+    if (!g_sms[dev]) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+            v = 148;
+        g_sms[dev] = v;
+    }
+    return g_sms[dev];
+}
+
+void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+void reset_launch_count() { g_launches.store(0, std::memory_order_relaxed); }
+
+namespace {
+struct Rec {
+    cudaEvent_t a, b;
+    int phase;
+    double flops, bytes;
+};
+std::mutex g_pm;
+std::atomic<bool> g_prof{false};
+std::vector<Rec> g_recs;
+double g_acc_ms[kNumPhases], g_acc_fl[kNumPhases], g_acc_by[kNumPhases];
+uint64_t g_acc_n[kNumPhases];
+}  // namespace
+
+void profile_enable(bool on) { g_prof.store(on); }
+
+PhaseScope::PhaseScope(Phase ph, cudaStream_t s, double flops, double bytes) : slot(-1), st(s) {
+    if (!g_prof.load(std::memory_order_relaxed)) return;
+    Rec r{};
+    if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
+    r.phase = ph;
+    r.flops = flops;
+    r.bytes = bytes;
+    cudaEventRecord(r.a, st);
+    std::lock_guard<std::mutex> lk(g_pm);
+    slot = int(g_recs.size());
+    g_recs.push_back(r);
+}
+
+PhaseScope::~PhaseScope() {
+    if (slot < 0) return;
+    std::lock_guard<std::mutex> lk(g_pm);
+    cudaEventRecord(g_recs[size_t(slot)].b, st);
+}
+
+void profile_read(double* ms, double* flops, double* bytes, uint64_t* launches, bool reset) {
+    std::lock_guard<std::mutex> lk(g_pm);
+    for (Rec& r : g_recs) {
+        cudaEventSynchronize(r.b);
+        float t = 0.f;
+        cudaEventElapsedTime(&t, r.a, r.b);
+        g_acc_ms[r.phase] += t;
+        g_acc_fl[r.phase] += r.flops;
+        g_acc_by[r.phase] += r.bytes;
+        g_acc_n[r.phase] += 1;
+        cudaEventDestroy(r.a);
+        cudaEventDestroy(r.b);
+    }
+    g_recs.clear();
+    for (int i = 0; i < kNumPhases; ++i) {
+        if (ms) ms[i] = g_acc_ms[i];
+        if (flops) flops[i] = g_acc_fl[i];
+        if (bytes) bytes[i] = g_acc_by[i];
+        if (launches) launches[i] = g_acc_n[i];
+        if (reset) g_acc_ms[i] = g_acc_fl[i] = g_acc_by[i] = 0, g_acc_n[i] = 0;
+    }
+}
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+const char* last_error() { return g_last_error.c_str(); }
+
+}  // namespace cct

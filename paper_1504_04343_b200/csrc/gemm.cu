@@ -1,0 +1,426 @@
+// gemm.cu -- warp-specialised, persistent tcgen05 GEMM with 3xTF32 split emulation.
+//
+// Replaces the reference GEMM (convlow::multiply, gemm.cpp:93-122; hot loop
+// gemm_panel gemm.cpp:54-63, fp32 x fp32 -> double accumulate).  fp32 accuracy
+// comes from the split a = a_big + a_small (a_big = a with the low 13 mantissa
+// bits cleared, which is what the tensor core consumes when reading fp32 data
+// as tf32) and three tensor-core products per K slice:
+//     C += A_big*B_big + A_big*B_small + A_small*B_big      (fp32 accumulate in TMEM)
+//
+// CTA = 384 threads, one CTA per SM, persistent over output tiles (m fastest):
+//   warp 0      TMA producer   (one lane): raw A/B tiles -> smem ring
+//   warp 1      MMA issuer     (one lane): 3 x tcgen05.mma.kind::tf32 per 8-wide K step
+//   warp 2      TMEM allocator
+//   warps 4-7   epilogue: tcgen05.ld (TMEM lane quarter = warp%4) -> st.global
+//   warps 8-11  transform: small = x - big for the A and B tiles of each stage
+// Pipelines: smem ring full/tdone/empty (TMA -> transform -> MMA -> TMA) and a
+// double-buffered TMEM accumulator tfull/tempty (MMA <-> epilogue), so the
+// epilogue of tile i overlaps the MMAs of tile i+1.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace cct {
+
+namespace {
+
+struct KParams {
+    int M, N, K;
+    int num_m_tiles, num_n_tiles, splits;
+    int kb_total, kb_per_split;
+    int units;
+    int passes;
+    float* C;
+    int64_t mdiv, s_mq, s_mr, s_n, s_split;
+};
+
+constexpr int kThreads = 384;
+
+__host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
+    return (2 * bn) <= 32 ? 32 : (2 * bn) <= 64 ? 64 : (2 * bn) <= 128 ? 128 : (2 * bn) <= 256 ? 256 : 512;
+}
+
+template <int BN>
+struct Cfg {
+    static constexpr uint32_t A_BYTES = kBM * kBK * 4;
+    static constexpr uint32_t B_BYTES = BN * kBK * 4;
+    static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
+    static constexpr uint32_t STAGE_BYTES = 2 * RAW_BYTES;  // raw | small
+    static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
+    static constexpr uint32_t BAR_BYTES = (3 * STAGES + 4) * 8 + 16;
+    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+    static constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
+};
+
+// a = big + small; big is what the tensor core reads from an fp32 operand in
+// kind::tf32 (low 13 mantissa bits ignored); small is exact.
+__device__ __forceinline__ float4 small_part(float4 v) {
+    float4 r;
+    r.x = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    r.y = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    r.z = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    r.w = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    return r;
+}
+
+// UMMA descriptor of one operand tile for K step kk (8 tf32 wide).
+//   K-major tile: rows of 64 B (16 fp32), SWIZZLE_64B, 8-row atoms of 512 B.
+//   MN-major tile: (rows/32) chunks of [16 K-rows x 128 B] written by TMA with
+//                  SWIZZLE_128B_ATOM_32B; UMMA layout SWIZZLE_128B_BASE32B (the
+//                  only MN-major smem layout for 32-bit operands), 4-K-row
+//                  atoms of 512 B (SBO), chunk stride 2 KB (LBO).
+template <bool MN>
+__device__ __forceinline__ uint64_t tile_desc(uint32_t base, int kk) {
+    if constexpr (!MN) {
+        return ptx::smem_desc(base + kk * 32, 16, 512, 4);
+    } else {
+        return ptx::smem_desc(base + kk * 1024, 32 * kBK * 4, 512, 1);
+    }
+}
+
+template <int BN, int A_MN, int B_MN>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
+                      const __grid_constant__ CUtensorMap tmB, const KParams p) {
+    using C_ = Cfg<BN>;
+    constexpr int STAGES = C_::STAGES;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // align inside the shared window without leaving the shared address space
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C_::STAGE_BYTES);
+    uint64_t* tdone = full + STAGES;
+    uint64_t* empty = tdone + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmA);
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&tdone[s], 4);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 4);
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<C_::TMEM_COLS>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+                const int mt = u % p.num_m_tiles;
+                const int rest = u / p.num_m_tiles;
+                const int nt = rest % p.num_n_tiles;
+                const int sp = rest / p.num_n_tiles;
+                const int m0 = mt * kBM, n0 = nt * BN;
+                const int kb0 = sp * p.kb_per_split;
+                const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[stage], C_::RAW_BYTES);
+                    uint8_t* a_dst = smem + stage * C_::STAGE_BYTES;
+                    uint8_t* b_dst = a_dst + C_::A_BYTES;
+                    const int k0 = kb * kBK;
+                    if constexpr (!A_MN) {
+                        ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < kBM / 32; ++c)
+                            ptx::tma_load_2d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], m0 + 32 * c, k0);
+                    }
+                    if constexpr (!B_MN) {
+                        ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+                    } else {
+#pragma unroll
+                        for (int c = 0; c < BN / 32; ++c)
+                            ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage], n0 + 32 * c, k0);
+                    }
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_tf32(kBM, BN, A_MN, B_MN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int local = 0;
+            for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+                const int rest = u / p.num_m_tiles;
+                const int sp = rest / p.num_n_tiles;
+                const int kb0 = sp * p.kb_per_split;
+                const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+                const int acc = local & 1;
+                const uint32_t use = uint32_t(local >> 1);
+                ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+                for (int kb = kb0; kb < kb1; ++kb) {
+                    ptx::mbar_wait(&full[stage], phase);
+                    if (p.passes == 3) ptx::mbar_wait(&tdone[stage], phase);
+                    ptx::tc_fence_after();
+                    const uint32_t a_raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
+                    const uint32_t b_raw = a_raw + C_::A_BYTES;
+                    const uint32_t a_sml = a_raw + C_::RAW_BYTES;
+                    const uint32_t b_sml = b_raw + C_::RAW_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < kBK / 8; ++kk) {
+                        const uint64_t ad = tile_desc<A_MN>(a_raw, kk);
+                        const uint64_t bd = tile_desc<B_MN>(b_raw, kk);
+                        if (p.passes == 3) {
+                            // small products first, big*big last
+                            ptx::mma_tf32(d_tmem, tile_desc<A_MN>(a_sml, kk), bd, idesc,
+                                          (kb > kb0 || kk > 0) ? 1u : 0u);
+                            ptx::mma_tf32(d_tmem, ad, tile_desc<B_MN>(b_sml, kk), idesc, 1u);
+                            ptx::mma_tf32(d_tmem, ad, bd, idesc, 1u);
+                        } else {
+                            ptx::mma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                        }
+                    }
+                    ptx::mma_commit(&empty[stage]);
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                }
+                ptx::mma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ===================== epilogue =====================
+        const int q = warp & 3;
+        int local = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+            const int mt = u % p.num_m_tiles;
+            const int rest = u / p.num_m_tiles;
+            const int nt = rest % p.num_n_tiles;
+            const int sp = rest / p.num_n_tiles;
+            const int acc = local & 1;
+            const uint32_t use = uint32_t(local >> 1);
+            ptx::mbar_wait(&tfull[acc], use & 1);
+            ptx::tc_fence_after();
+            const int64_t row = int64_t(mt) * kBM + q * 32 + lane;
+            const bool row_ok = row < p.M;
+            int64_t off = 0;
+            if (row_ok) off = (row / p.mdiv) * p.s_mq + (row % p.mdiv) * p.s_mr + int64_t(sp) * p.s_split;
+            const int n0 = nt * BN;
+            const int64_t sn = p.s_n;
+#pragma unroll 1
+            for (int c0 = 0; c0 < BN; c0 += 32) {
+                uint32_t v[32];
+                ptx::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c0), v);
+                ptx::tmem_ld_wait();
+                float* dst = p.C + off + int64_t(n0 + c0) * sn;
+                const int nlim = p.N - (n0 + c0);
+                if (row_ok && nlim >= 32) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        *dst = __uint_as_float(v[j]);
+                        dst += sn;
+                    }
+                } else if (row_ok) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (j < nlim) *dst = __uint_as_float(v[j]);
+                        dst += sn;
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+    } else if (warp >= 8) {
+        // ===================== 3xTF32 transform =====================
+        const int t = threadIdx.x - 256;
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            const int rest = u / p.num_m_tiles;
+            const int sp = rest / p.num_n_tiles;
+            const int kb0 = sp * p.kb_per_split;
+            const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                ptx::mbar_wait(&full[stage], phase);
+                if (p.passes == 3) {
+                    const uint32_t raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
+                    constexpr int n4 = C_::RAW_BYTES / 16;
+#pragma unroll 4
+                    for (int i = t; i < n4; i += 128) {
+                        const float4 v = ptx::lds128(raw + i * 16);
+                        ptx::sts128(raw + C_::RAW_BYTES + i * 16, small_part(v));
+                    }
+                    ptx::fence_proxy_async_smem();
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tdone[stage]);
+                if (++stage == STAGES) { stage = 0; phase ^= 1; }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<C_::TMEM_COLS>(tmem_base);
+    }
+}
+
+// ----------------------------------------------------------------------------
+// host side
+// ----------------------------------------------------------------------------
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    }
+    return fn;
+}
+
+// mn_extent x k_extent logical operand; box_mn rows per (K-major) tile
+bool make_tmap(CUtensorMap* map, const Operand& op, int64_t mn_extent, int64_t k_extent, int box_mn) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2];
+    cuuint64_t strides[1] = {cuuint64_t(op.ld) * 4};
+    cuuint32_t box[2];
+    cuuint32_t estr[2] = {1, 1};
+    CUtensorMapSwizzle sw;
+    if (op.major == Major::K) {
+        dims[0] = cuuint64_t(k_extent);
+        dims[1] = cuuint64_t(mn_extent);
+        box[0] = kBK;
+        box[1] = cuuint32_t(box_mn);
+        sw = CU_TENSOR_MAP_SWIZZLE_64B;
+    } else {
+        dims[0] = cuuint64_t(mn_extent);
+        dims[1] = cuuint64_t(k_extent);
+        box[0] = 32;
+        box[1] = kBK;
+        sw = CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B;
+    }
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(op.ptr), dims, strides,
+                     box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+template <int BN, int A_MN, int B_MN>
+cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, cudaStream_t st) {
+    using C_ = Cfg<BN>;
+    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr_set = true;
+    }
+    const int grid = std::min(kp.units, num_sms());
+    PhaseScope ps(kPhaseGemm, st, 2.0 * double(kp.M) * double(kp.N) * double(kp.K), 0);
+    kern<<<grid, kThreads, C_::SMEM_BYTES, st>>>(ta, tb, kp);
+    note_launch();
+    return cudaGetLastError();
+}
+
+template <int BN>
+cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
+                            const KParams& kp, cudaStream_t st) {
+    const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
+    if (!amn && !bmn) return launch<BN, 0, 0>(ta, tb, kp, st);
+    if (amn && bmn) return launch<BN, 1, 1>(ta, tb, kp, st);
+    if (amn && !bmn) return launch<BN, 1, 0>(ta, tb, kp, st);
+    return launch<BN, 0, 1>(ta, tb, kp, st);
+}
+
+}  // namespace
+
+int choose_bn(int64_t N) {
+    static const int cands[] = {256, 192, 128, 96, 64};
+    int best = 256;
+    int64_t best_pad = INT64_MAX;
+    for (int bn : cands) {
+        const int64_t pad = ((N + bn - 1) / bn) * bn;
+        if (pad < best_pad) { best_pad = pad; best = bn; }
+    }
+    return best;
+}
+
+// The tensor core accumulates fp32 with truncation, so the error of one
+// TMEM accumulation chain grows ~linearly with its length (measured on B200:
+// rel-L2 9e-7 at K=96, 1.6e-5 at K=2400).  Chains are therefore capped at
+// kMaxChainK; longer reductions are split and the partials summed in fp32
+// round-to-nearest by the deterministic reduce kernel.  Short-K problems with
+// too few tiles to fill the machine are also split.
+int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn) {
+    const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + bn - 1) / bn);
+    const int64_t kb = (K + kBK - 1) / kBK;
+    int64_t s = (kb + kMaxChainKB - 1) / kMaxChainKB;  // accuracy floor
+    if (tiles * s < 2 * int64_t(sms) && kb >= 64) {
+        // fill ~2 waves while keeping >= 32 k-blocks per split
+        const int64_t fill = (2 * int64_t(sms) + tiles - 1) / tiles;
+        s = std::max(s, std::min<int64_t>(fill, kb / 32));
+    }
+    return int(std::max<int64_t>(1, s));
+}
+
+cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
+    if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
+    const int bn = g.bn ? g.bn : choose_bn(g.N);
+    KParams kp{};
+    kp.M = int(g.M);
+    kp.N = int(g.N);
+    kp.K = int(g.K);
+    kp.num_m_tiles = int((g.M + kBM - 1) / kBM);
+    kp.num_n_tiles = int((g.N + bn - 1) / bn);
+    kp.kb_total = int((g.K + kBK - 1) / kBK);
+    const int splits = std::max(1, std::min(g.splits, kp.kb_total));
+    kp.kb_per_split = (kp.kb_total + splits - 1) / splits;
+    kp.splits = (kp.kb_total + kp.kb_per_split - 1) / kp.kb_per_split;  // no empty split
+    kp.units = kp.num_m_tiles * kp.num_n_tiles * kp.splits;
+    kp.passes = g.passes;
+    kp.C = g.C.ptr;
+    kp.mdiv = g.C.mdiv;
+    kp.s_mq = g.C.s_mq;
+    kp.s_mr = g.C.s_mr;
+    kp.s_n = g.C.s_n;
+    kp.s_split = g.C.s_split;
+
+    CUtensorMap ta, tb;
+    if (!make_tmap(&ta, g.A, g.M, g.K, kBM)) return cudaErrorInvalidValue;
+    if (!make_tmap(&tb, g.B, g.N, g.K, bn)) return cudaErrorInvalidValue;
+    switch (bn) {
+    case 256: return dispatch_layout<256>(g, ta, tb, kp, stream);
+    case 192: return dispatch_layout<192>(g, ta, tb, kp, stream);
+    case 128: return dispatch_layout<128>(g, ta, tb, kp, stream);
+    case 96: return dispatch_layout<96>(g, ta, tb, kp, stream);
+    case 64: return dispatch_layout<64>(g, ta, tb, kp, stream);
+    default: return cudaErrorInvalidValue;
+    }
+}
+
+}  // namespace cct

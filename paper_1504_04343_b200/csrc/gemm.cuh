@@ -1,0 +1,51 @@
+// gemm.cuh -- host-side description of one lowered GEMM (replaces convlow::multiply,
+// gemm.cpp:93-122) executed by the tcgen05 3xTF32 kernel in gemm.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace cct {
+
+// How an operand is stored in global memory (row-major, leading dim `ld` floats):
+//   KMaj  : rows are the M (or N) index, columns the reduction index K
+//   MNMaj : rows are the reduction index K, columns the M (or N) index
+enum class Major : int { K = 0, MN = 1 };
+
+struct Operand {
+    const float* ptr = nullptr;
+    int64_t ld = 0;  // floats; must be a multiple of 4 (16-byte TMA strides)
+    Major major = Major::K;
+};
+
+// Epilogue address map: element (row m, col n) of split s goes to
+//   ptr + (m / mdiv) * s_mq + (m % mdiv) * s_mr + n * s_n + s * s_split
+// (row = TMEM lane; s_mr == 1 gives fully coalesced stores).
+struct OutMap {
+    float* ptr = nullptr;
+    int64_t mdiv = INT64_MAX;
+    int64_t s_mq = 0, s_mr = 1, s_n = 0, s_split = 0;
+};
+
+struct GemmProblem {
+    int64_t M = 0, N = 0, K = 0;
+    Operand A, B;
+    OutMap C;
+    int splits = 1;  // split-K factor; each split writes its own slice (s_split)
+    int passes = 3;  // 3 = 3xTF32 (fp32-accurate), 1 = plain TF32 (diagnostic only)
+    int bn = 0;      // 0 = choose
+};
+
+// Tile constants shared by the launcher and the kernel.
+constexpr int kBM = 128;
+constexpr int kBK = 16;
+// longest single TMEM accumulation chain, in k-blocks (= 4096 reduction terms)
+constexpr int kMaxChainKB = 256;
+
+int choose_bn(int64_t N);
+// number of k-blocks per split so that splits * tiles fill the machine
+int choose_splits(int64_t M, int64_t N, int64_t K, int num_sms, int bn);
+
+cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream);
+
+}  // namespace cct

@@ -1,0 +1,352 @@
+// lowering.cu -- the HBM-bound kernels of the three lowering types (see lowering.cuh).
+//
+// All kernels are pure gathers (no atomics): every output element is written
+// exactly once by one thread, with the output index fastest-varying across a
+// warp so stores are coalesced, and float4-vectorised when the channel depth is a
+// multiple of 4.  Grids are grid-stride loops sized to a multiple of the SM count.
+#include <algorithm>
+#include <type_traits>
+
+#include "common.cuh"
+#include "lowering.cuh"
+
+namespace cct {
+
+RowMap rowmap_internal(const Geo& g, int type) {
+    RowMap r{};
+    if (type == 1) { r.ny = g.m; r.nc = g.m; }
+    else if (type == 2) { r.ny = g.R; r.nc = g.m; }
+    else { r.ny = g.R; r.nc = g.R; }
+    r.rpi = r.ny * r.nc;
+    r.sr = r.nc;
+    r.sc = 1;
+    return r;
+}
+
+// image block of m^2 (T1) or n^2 (T2/T3) rows, row = c*m + r / c*n + r.
+RowMap rowmap_spec(const Geo& g, int type) {
+    RowMap r{};
+    const int64_t side = (type == 1) ? g.m : g.n;
+    r.ny = side;
+    r.nc = side;
+    r.rpi = side * side;
+    r.sr = 1;
+    r.sc = side;
+    return r;
+}
+
+int64_t lowered_cols(const Geo& g, int type) {
+    return type == 1 ? g.k * g.k * g.d : type == 2 ? g.k * g.d : g.d;
+}
+int64_t lowered_ncols(const Geo& g, int type) {
+    return type == 1 ? g.o : type == 2 ? g.k * g.o : g.k * g.k * g.o;
+}
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// One warp per lowered row (q, y, c).  The row is `nruns` runs of L source
+// floats that are contiguous in x (T1: k runs of k*d; T2: 1 run of k*d; T3: 1
+// run of d).  The in-image part of a run is one contiguous interval, computed
+// once per run, so the copy loop has no per-element index arithmetic.
+template <bool VEC4>
+__global__ void lower_kernel(const float* __restrict__ x, float* __restrict__ dh, Geo g, int type,
+                             RowMap rm, int64_t ld, int cols, int64_t nrows_logical) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+    const int n = int(g.n), d = int(g.d), k = int(g.k), s = int(g.s), p = int(g.p);
+    const int nc = int(rm.nc), ny = int(rm.ny);
+    const int L = (type == 3) ? d : k * d;     // run length (floats)
+    const int nruns = (type == 1) ? k : 1;
+    const int W = VEC4 ? 4 : 1;                 // floats per element moved
+    for (int64_t w = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; w < nrows_logical; w += warps) {
+        const int c = int(w % nc);
+        const int64_t t = w / nc;
+        const int y = int(t % ny);
+        const int64_t q = t / ny;
+        float* row = dh + (q * rm.rpi + int64_t(y) * rm.sr + int64_t(c) * rm.sc) * ld;
+        int ys0, xs0;
+        bool zero_row = false;
+        if (type == 1) { ys0 = s * y - p; xs0 = s * c - p; }
+        else if (type == 2) { ys0 = y - p; xs0 = s * c - p; zero_row = (c >= g.m); }
+        else { ys0 = y - p; xs0 = c - p; }
+        const int taps = (type == 3) ? 1 : k;   // pixels per run
+        // valid pixel interval [jlo, jhi) of the run
+        const int jlo = max(0, -xs0), jhi = min(taps, n - xs0);
+        const float* xq = x + q * int64_t(n) * n * d;
+        for (int i = 0; i < nruns; ++i) {
+            const int ys = ys0 + ((type == 1) ? i : 0);
+            const bool row_ok = !zero_row && ys >= 0 && ys < n && jlo < jhi;
+            const int lo = jlo * d / W, hi = jhi * d / W;  // in elements of W floats
+            const float* src = xq + (int64_t(ys) * n + xs0) * d;
+            float* dst = row + i * L;
+            if constexpr (VEC4) {
+                const float4* s4 = reinterpret_cast<const float4*>(src);
+                float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll 4
+                for (int e = lane; e < L / 4; e += 32) {
+                    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+                    if (row_ok && e >= lo && e < hi) v = __ldg(s4 + e);
+                    d4[e] = v;
+                }
+            } else {
+                for (int e = lane; e < L; e += 32) {
+                    float v = 0.f;
+                    if (row_ok && e >= lo && e < hi) v = __ldg(src + e);
+                    dst[e] = v;
+                }
+            }
+        }
+        for (int e = cols + lane; e < ld; e += 32) row[e] = 0.f;  // pad columns
+    }
+}
+
+// y[q,o,r,c] = sum over taps of Rhat[row(q, s r + i, s c + j), col(o, i, j)].
+// One block-row per output plane (q, o); threads stride over the m*m pixels.
+__global__ void lift_kernel(const float* __restrict__ rh, float* __restrict__ y, Geo g, int type,
+                            RowMap rm, int64_t rs, int64_t cs) {
+    const int m = int(g.m), o = int(g.o), k = int(g.k), s = int(g.s), mm = m * m;
+    const int64_t planes = g.b * o;
+    for (int64_t pl = blockIdx.x; pl < planes; pl += gridDim.x) {
+        const int oj = int(pl % o);
+        const int64_t q = pl / o;
+        const int64_t base = q * rm.rpi;
+        float* yp = y + pl * mm;
+        for (int pix = threadIdx.x; pix < mm; pix += blockDim.x) {
+            const int r = pix / m, c = pix - r * m;
+            float acc = 0.f;
+            if (type == 1) {
+                acc = rh[(base + r * rm.sr + c * rm.sc) * rs + oj * cs];
+            } else if (type == 2) {
+                const float* p0 = rh + (base + int64_t(s) * r * rm.sr + int64_t(c) * rm.sc) * rs + int64_t(oj) * k * cs;
+                const int64_t step = rm.sr * rs + cs;
+                for (int i = 0; i < k; ++i) acc += p0[i * step];
+            } else {
+                const float* p0 = rh + (base + int64_t(s) * r * rm.sr + int64_t(s) * c * rm.sc) * rs +
+                                  int64_t(oj) * k * k * cs;
+                for (int i = 0; i < k; ++i)
+                    for (int j = 0; j < k; ++j) acc += p0[i * rm.sr * rs + j * rm.sc * rs + (i * k + j) * cs];
+            }
+            yp[pix] = acc;
+        }
+    }
+}
+
+// T1 expand: dRhat1^T[o][q*m^2 + pix] = dy[q][o][pix] -- a permutation of the
+// (q, o) planes.  blockIdx.x strides over planes, threads over the m^2 pixels.
+__global__ void expand_t1_kernel(const float* __restrict__ dy, float* __restrict__ drt, int64_t b, int o,
+                                 int mm, int64_t ldr) {
+    const int64_t planes = b * o;
+    for (int64_t pl = blockIdx.x; pl < planes; pl += gridDim.x) {
+        const int oj = int(pl % o);
+        const int64_t q = pl / o;
+        const float* src = dy + pl * mm;
+        float* dst = drt + int64_t(oj) * ldr + q * mm;
+        for (int i = threadIdx.x; i < mm; i += blockDim.x) dst[i] = __ldg(src + i);
+    }
+}
+
+// T2/T3 expand: dRhat^T[col][row] (internal row order), zeros where lift does
+// not read.  blockIdx.y = column (o, i[, j]); threads stride over the rows.
+__global__ void expand_kernel(const float* __restrict__ dy, float* __restrict__ drt, Geo g, int type,
+                              RowMap rm, int64_t ldr) {
+    const int m = int(g.m), o = int(g.o), k = int(g.k), s = int(g.s);
+    const int nc = int(rm.nc), ny = int(rm.ny);
+    const int col = blockIdx.y;
+    int oj, i, j = 0;
+    if (type == 2) { oj = col / k; i = col - oj * k; }
+    else { oj = col / (k * k); const int ij = col - oj * k * k; i = ij / k; j = ij - i * k; }
+    float* out = drt + int64_t(col) * ldr;
+    const int64_t rows = g.b * rm.rpi;
+    for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < rows;
+         row += int64_t(gridDim.x) * blockDim.x) {
+        const int cx = int(row % nc);
+        const int64_t t = row / nc;
+        const int yy = int(t % ny);
+        const int64_t q = t / ny;
+        const int ty = yy - i;
+        int r = -1;
+        if (s == 1) r = ty;
+        else if (ty >= 0 && ty % s == 0) r = ty / s;
+        int c = cx;
+        if (type == 3) {
+            const int tx = cx - j;
+            c = -1;
+            if (s == 1) c = tx;
+            else if (tx >= 0 && tx % s == 0) c = tx / s;
+        }
+        float v = 0.f;
+        if (r >= 0 && r < m && c >= 0 && c < m) v = __ldg(dy + ((q * o + oj) * m + r) * int64_t(m) + c);
+        out[row] = v;
+    }
+}
+
+// dx[q,y,x,ch] (unpadded) = adjoint of lower: sum of the dDhat entries that
+// copied Xp[q,y+p,x+p,ch].  One block-row per input row (q, y); each thread owns
+// VW consecutive channels (float4 when d % 4 == 0) and walks the taps directly
+// (first tap congruent mod s, then step s), several loads in flight.
+template <int VW>
+__global__ void col2im_kernel(const float* __restrict__ dd, int64_t ld, float* __restrict__ dx, Geo g,
+                              int type) {
+    using V = typename std::conditional<VW == 4, float4, float>::type;
+    const int n = int(g.n), d = int(g.d), k = int(g.k), s = int(g.s), p = int(g.p), m = int(g.m),
+              R = int(g.R);
+    const int dv = d / VW;
+    const int64_t rowsq = g.b * n;
+    const int per_row = n * dv;
+    for (int64_t qy = blockIdx.x; qy < rowsq; qy += gridDim.x) {
+        const int yy = int(qy % n);
+        const int64_t q = qy / n;
+        const int py = yy + p;
+        V* out = reinterpret_cast<V*>(dx + qy * int64_t(n) * d);
+        // valid output-row taps i (type 1): r = (py - i)/s in [0, m)
+        for (int e = threadIdx.x; e < per_row; e += blockDim.x) {
+            const int xx = e / dv, cv = e - xx * dv;
+            const int px = xx + p;
+            float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+            auto add = [&](const float* ptr) {
+                if constexpr (VW == 4) {
+                    const float4 v = __ldg(reinterpret_cast<const float4*>(ptr) + cv);
+                    a0 += v.x; a1 += v.y; a2 += v.z; a3 += v.w;
+                } else {
+                    a0 += __ldg(ptr + cv);
+                }
+            };
+            // tap ranges: c = (px - j)/s in [0, m)  <=>  j in [px - s(m-1), px], j == px mod s
+            const int jlo0 = px - s * (m - 1);
+            int jfirst = px % s;
+            if (jfirst < jlo0) jfirst += ((jlo0 - jfirst + s - 1) / s) * s;
+            const int jlast = min(k - 1, px);
+            if (type == 3) {
+                if (py < R && px < R) add(dd + ((q * R + py) * R + px) * ld);
+            } else if (type == 2) {
+                if (py < R) {
+                    const int64_t rowb = (q * R + py) * int64_t(m);
+#pragma unroll 4
+                    for (int j = jfirst; j <= jlast; j += s) add(dd + (rowb + (px - j) / s) * ld + j * d);
+                }
+            } else {
+                const int ilo0 = py - s * (m - 1);
+                int ifirst = py % s;
+                if (ifirst < ilo0) ifirst += ((ilo0 - ifirst + s - 1) / s) * s;
+                const int ilast = min(k - 1, py);
+                for (int i = ifirst; i <= ilast; i += s) {
+                    const int64_t rowb = (q * m + (py - i) / s) * int64_t(m);
+#pragma unroll 4
+                    for (int j = jfirst; j <= jlast; j += s)
+                        add(dd + (rowb + (px - j) / s) * ld + (i * k + j) * d);
+                }
+            }
+            if constexpr (VW == 4) out[e] = make_float4(a0, a1, a2, a3);
+            else out[e] = a0;
+        }
+    }
+}
+
+__global__ void pad_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                                float* __restrict__ dst, int64_t ldd) {
+    const int64_t total = rows * ldd;
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t r = e / ldd, c = e - r * ldd;
+        dst[e] = c < cols ? src[r * lds + c] : 0.f;
+    }
+}
+
+__global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
+                                 float* __restrict__ dst, int64_t ldd) {
+    __shared__ float tile[32][33];
+    const int64_t tiles_c = (cols + 31) / 32, tiles_r = (rows + 31) / 32;
+    for (int64_t tix = blockIdx.x; tix < tiles_r * tiles_c; tix += gridDim.x) {
+        const int64_t r0 = (tix / tiles_c) * 32, c0 = (tix % tiles_c) * 32;
+        for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+            const int64_t r = r0 + i, c = c0 + threadIdx.x;
+            tile[i][threadIdx.x] = (r < rows && c < cols) ? src[r * lds + c] : 0.f;
+        }
+        __syncthreads();
+        for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+            const int64_t c = c0 + i, r = r0 + threadIdx.x;
+            if (r < rows && c < cols) dst[c * ldd + r] = tile[threadIdx.x][i];
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace
+
+cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, float* dhat, int64_t ld,
+                  cudaStream_t st) {
+    const int64_t cols = lowered_cols(g, type);
+    const int64_t nrows = g.b * rm.ny * rm.nc;
+    PhaseScope ps(kPhaseLower, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + nrows * ld));
+    const bool vec = (g.d % 4 == 0) && (ld % 4 == 0) &&
+                     (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(dhat) % 16 == 0);
+    const int grid = grid_for(nrows * 32, kThreads);
+    if (vec) lower_kernel<true><<<grid, kThreads, 0, st>>>(x, dhat, g, type, rm, ld, int(cols), nrows);
+    else lower_kernel<false><<<grid, kThreads, 0, st>>>(x, dhat, g, type, rm, ld, int(cols), nrows);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t lift(const Geo& g, int type, const RowMap& rm, const float* rhat, int64_t rs, int64_t cs,
+                 float* y, cudaStream_t st) {
+    const int64_t planes = g.b * g.o;
+    const int grid = int(std::min<int64_t>(planes, int64_t(num_sms()) * 16));
+    PhaseScope ps(kPhaseLift, st, 0,
+                  4.0 * double(g.b * g.o * g.m * g.m) * (1.0 + (type == 1 ? 1 : type == 2 ? g.k : g.k * g.k)));
+    lift_kernel<<<grid, kThreads, 0, st>>>(rhat, y, g, type, rm, rs, cs);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t expand(const Geo& g, int type, const float* dy, float* drt, int64_t ldr, cudaStream_t st) {
+    const RowMap rm = rowmap_internal(g, type);
+    const int64_t ncols = lowered_ncols(g, type);
+    PhaseScope ps(kPhaseExpand, st, 0, 4.0 * double(g.b * g.o * g.m * g.m + ncols * g.b * rm.rpi));
+    if (type == 1) {
+        const int64_t planes = g.b * g.o;
+        const int grid = int(std::min<int64_t>(planes, int64_t(num_sms()) * 16));
+        expand_t1_kernel<<<grid, kThreads, 0, st>>>(dy, drt, g.b, int(g.o), int(g.m * g.m), ldr);
+    } else {
+        if (ncols > 65535) return cudaErrorInvalidConfiguration;
+        const int64_t rows = g.b * rm.rpi;
+        const int64_t want = (int64_t(num_sms()) * 16 + ncols - 1) / ncols;
+        const int gx = int(std::max<int64_t>(1, std::min<int64_t>(want, cdiv(rows, kThreads))));
+        expand_kernel<<<dim3(gx, unsigned(ncols)), kThreads, 0, st>>>(dy, drt, g, type, rm, ldr);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* dx, cudaStream_t st) {
+    const int64_t rowsq = g.b * g.n;
+    const int grid = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * 16));
+    const RowMap rmi = rowmap_internal(g, type);
+    PhaseScope ps(kPhaseCol2im, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + g.b * rmi.rpi * lowered_cols(g, type)));
+    const bool vec = g.d % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(dd) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(dx) % 16 == 0);
+    if (vec) col2im_kernel<4><<<grid, kThreads, 0, st>>>(dd, ld, dx, g, type);
+    else col2im_kernel<1><<<grid, kThreads, 0, st>>>(dd, ld, dx, g, type);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t pad_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_src, float* dst,
+                     int64_t ld_dst, cudaStream_t st) {
+    PhaseScope ps(kPhaseOther, st, 0, 4.0 * double(rows * (cols + ld_dst)));
+    pad_rows_kernel<<<grid_for(rows * ld_dst, kThreads), kThreads, 0, st>>>(src, rows, cols, ld_src, dst, ld_dst);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t transpose(const float* src, int64_t rows, int64_t cols, int64_t ld_src, float* dst,
+                      int64_t ld_dst, cudaStream_t st) {
+    const int64_t tiles = cdiv(rows, 32) * cdiv(cols, 32);
+    const int grid = int(std::min<int64_t>(tiles, int64_t(num_sms()) * 16));
+    transpose_kernel<<<grid, dim3(32, 8), 0, st>>>(src, rows, cols, ld_src, dst, ld_dst);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace cct

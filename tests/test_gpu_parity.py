@@ -1,0 +1,257 @@
+"""GPU parity: the B200 path (libcct.so through the C ABI) against the oracle.
+
+Tolerance (north_star): relative L2 <= 1e-4 per output / gradient tensor, for
+every lowering type.  Pure data-movement phases (lower, Khat) are bit-exact.
+Sizes: small batches against the oracle and the reference golden vectors;
+BASELINE sizes (b = 256) through size-independent properties (linearity,
+the fwd/bwd adjoint identity, determinism) plus an image-slice oracle check.
+"""
+import glob
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from oracle_py import rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+CONV_CASES = sorted(glob.glob(os.path.join(GOLD, "c*.npz")))
+CAFFENET = [("conv1", 227, 11, 3, 96, 4, 0), ("conv2", 27, 5, 96, 256, 1, 2), ("conv3", 13, 3, 256, 384, 1, 1),
+            ("conv4", 13, 3, 384, 384, 1, 1), ("conv5", 13, 3, 384, 256, 1, 1)]
+
+
+def T(a, dev, *shape):
+    return torch.from_numpy(np.ascontiguousarray(a, np.float32)).to(dev).view(*shape)
+
+
+def run3(cct, dev, x, w, dy, n, k, d, o, b, s, p, t):
+    from paper_1504_04343_b200 import conv
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    m = desc.m
+    xt, wt, dyt = T(x, dev, b, n, n, d), T(w, dev, o, k, k, d), T(dy, dev, b, o, m, m)
+    y = conv.conv_fwd(xt, wt, desc, t)
+    dx = conv.conv_bwd_data(dyt, wt, desc, t)
+    dw = conv.conv_bwd_weight(xt, dyt, desc, t)
+    return y.cpu().numpy().ravel(), dx.cpu().numpy().ravel(), dw.cpu().numpy().ravel()
+
+
+# ------------------------------------------------------------------- GEMM
+def test_gemm_kat(cct, dev):
+    from paper_1504_04343_b200 import conv
+    a = torch.tensor([[1., 2.], [3., 4.]], device=dev)
+    b = torch.tensor([[5., 6.], [7., 8.]], device=dev)
+    assert conv.multiply(a, b).cpu().tolist() == [[19, 22], [43, 50]]
+    e = torch.eye(5, device=dev)
+    bb = torch.rand(5, 7, device=dev)
+    assert torch.equal(conv.multiply(e, bb), bb)  # identity; exact with 3xTF32
+
+
+def test_tf32_operand_truncation(cct, dev):
+    """The tensor core reads fp32 operands as tf32 by truncation: raw fp32 is the 'big' half."""
+    from paper_1504_04343_b200 import conv
+    v = 1.0 + 3 * 2.0 ** -12
+    a = torch.zeros((128, 16), device=dev)
+    a[:, 0] = v
+    b = torch.zeros((16, 128), device=dev)
+    b[0, :] = 1.0
+    assert conv.multiply_passes(a, b, 1)[0, 0].item() == 1.0
+    assert conv.multiply_passes(a, b, 3)[0, 0].item() == v
+
+
+@pytest.mark.parametrize("path", sorted(glob.glob(os.path.join(GOLD, "g*.npz"))))
+def test_gemm_vs_reference_golden(cct, dev, path):
+    from paper_1504_04343_b200 import conv
+    z = np.load(path)
+    c = conv.multiply(torch.from_numpy(z["A"]).to(dev), torch.from_numpy(z["B"]).to(dev)).cpu().numpy()
+    assert rel_l2(c, z["C"]) < 1e-5
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (3, 5, 7), (129, 257, 1000), (1000, 96, 363), (256, 256, 32768)])
+def test_gemm_shapes_and_long_k(cct, dev, orc, M, N, K):
+    from paper_1504_04343_b200 import conv
+    A = orc.uniform(M + 1, M * K).reshape(M, K)
+    B = orc.uniform(N + 2, K * N).reshape(K, N)
+    ref = A.astype(np.float64) @ B.astype(np.float64)
+    c = conv.multiply(torch.from_numpy(A).to(dev), torch.from_numpy(B).to(dev)).cpu().numpy()
+    assert rel_l2(c, ref) < 1e-5  # long K is chain-split (truncating accumulator)
+
+
+def test_gemm_deterministic(cct, dev):
+    from paper_1504_04343_b200 import conv
+    a = torch.rand(300, 5000, device=dev)
+    b = torch.rand(5000, 200, device=dev)
+    c1 = conv.multiply(a, b)
+    c2 = conv.multiply(a, b)
+    assert torch.equal(c1, c2)
+
+
+# ---------------------------------------------------------- lowering phases
+@pytest.mark.parametrize("t", [1, 2, 3])
+def test_lower_spec_bit_exact(cct, dev, orc, t):
+    from paper_1504_04343_b200 import conv
+    b, n, d, k, o = 2, 7, 3, 3, 4
+    x, w = orc.random_problem(31, b, n, d, k, o)
+    desc = cct.ConvDesc(n, k, d, o, b)
+    dh_ref, kh_ref = orc.lower(t, x, w, b, n, d, k, o)
+    dh = conv.lower(T(x, dev, b, n, n, d), desc, t, cct.ROWS_SPEC).cpu().numpy()
+    kh = conv.lower_khat(T(w, dev, o, k, k, d), desc, t).cpu().numpy()
+    assert np.array_equal(dh, dh_ref) and np.array_equal(kh, kh_ref)
+    # lift(Rhat) in the SPEC row order vs the oracle lift
+    rh = orc.multiply(dh_ref, kh_ref)
+    y = conv.lift(torch.from_numpy(rh).to(dev), desc, t, cct.ROWS_SPEC).cpu().numpy().ravel()
+    assert rel_l2(y, orc.lift(t, rh, b, n, d, k, o)) < 1e-6
+
+
+@pytest.mark.parametrize("t", [1, 2, 3])
+@pytest.mark.parametrize("geom", [(9, 3, 4, 1, 0), (11, 3, 8, 1, 1), (13, 5, 4, 2, 2), (23, 11, 3, 4, 0)])
+def test_lower_internal_bit_exact(cct, dev, orc, t, geom):
+    from paper_1504_04343_b200 import conv
+    n, k, d, s, p = geom
+    b = 2
+    x = orc.uniform(41, b * n * n * d)
+    desc = cct.ConvDesc(n, k, d, 5, b, s, p)
+    dh = conv.lower(T(x, dev, b, n, n, d), desc, t, cct.ROWS_INTERNAL).cpu().numpy()
+    assert np.array_equal(dh, orc.lower_internal(t, x, b, n, d, k, s, p))
+
+
+# --------------------------------------------------------- full conv passes
+@pytest.mark.parametrize("t", [1, 2, 3])
+@pytest.mark.parametrize("path", CONV_CASES, ids=[os.path.basename(p)[:-4] for p in CONV_CASES])
+def test_conv_vs_reference_golden(cct, dev, path, t):
+    z = np.load(path)
+    n, k, d, o, b, s, p = (int(v) for v in z["shape"])
+    y, dx, dw = run3(cct, dev, z["x"], z["w"], z["dy"], n, k, d, o, b, s, p, t)
+    errs = rel_l2(y, z["y"]), rel_l2(dx, z["dx"]), rel_l2(dw, z["dw"])
+    assert max(errs) <= TOL, errs
+
+
+@pytest.mark.parametrize("t", [1, 2, 3])
+@pytest.mark.parametrize("layer", CAFFENET, ids=[l[0] for l in CAFFENET])
+def test_caffenet_layers_vs_oracle(cct, dev, orc, layer, t):
+    _, n, k, d, o, s, p = layer
+    b = 2
+    x, w = orc.random_problem(1234, b, n, d, k, o)
+    m = (n + 2 * p - k) // s + 1
+    dy = orc.uniform(1235, b * o * m * m)
+    y, dx, dw = run3(cct, dev, x, w, dy, n, k, d, o, b, s, p, t)
+    errs = (rel_l2(y, orc.conv_fwd(x, w, b, n, d, k, o, s, p)),
+            rel_l2(dx, orc.conv_bwd_data(dy, w, b, n, d, k, o, s, p)),
+            rel_l2(dw, orc.conv_bwd_weight(x, dy, b, n, d, k, o, s, p)))
+    assert max(errs) <= TOL, errs
+
+
+@pytest.mark.parametrize("geom", [(5, 5, 2, 3, 1, 1, 0), (1, 1, 4, 4, 3, 1, 0), (6, 3, 5, 7, 1, 3, 2),
+                                  (4, 4, 1, 1, 1, 1, 3)])
+def test_edge_shapes(cct, dev, orc, geom):
+    """n = k (single output pixel), 1x1 images, ragged stride, pad > k/2."""
+    n, k, d, o, b, s, p = geom
+    x, w = orc.random_problem(7, b, n, d, k, o)
+    m = (n + 2 * p - k) // s + 1
+    dy = orc.uniform(8, b * o * m * m)
+    for t in (1, 2, 3):
+        y, dx, dw = run3(cct, dev, x, w, dy, n, k, d, o, b, s, p, t)
+        assert rel_l2(y, orc.conv_fwd(x, w, b, n, d, k, o, s, p)) <= TOL
+        assert rel_l2(dx, orc.conv_bwd_data(dy, w, b, n, d, k, o, s, p)) <= TOL
+        assert rel_l2(dw, orc.conv_bwd_weight(x, dy, b, n, d, k, o, s, p)) <= TOL
+
+
+def test_auto_lowering_matches_oracle(cct, dev, orc):
+    n, k, d, o, b, s, p = 13, 3, 64, 32, 2, 1, 1
+    x, w = orc.random_problem(3, b, n, d, k, o)
+    m = (n + 2 * p - k) // s + 1
+    dy = orc.uniform(4, b * o * m * m)
+    y, dx, dw = run3(cct, dev, x, w, dy, n, k, d, o, b, s, p, cct.LOWER_AUTO)
+    assert rel_l2(y, orc.conv_fwd(x, w, b, n, d, k, o, s, p)) <= TOL
+
+
+# ------------------------------------------- BASELINE sizes: properties + slice
+@pytest.mark.parametrize("t", [1, 2, 3])
+def test_conv2_b256_properties(cct, dev, orc, t):
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = 27, 5, 96, 256, 256, 1, 2
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    m = desc.m
+    g = torch.Generator(device=dev).manual_seed(5)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    dy = torch.rand((b, o, m, m), generator=g, device=dev) * 2 - 1
+    y = conv.conv_fwd(x, w, desc, t)
+    dx = conv.conv_bwd_data(dy, w, desc, t)
+    dw = conv.conv_bwd_weight(x, dy, desc, t)
+    # determinism (fixed split-K order) and exact linearity (scaling by 2 commutes with the 3xTF32 split)
+    assert torch.equal(conv.conv_fwd(x, w, desc, t), y)
+    assert torch.equal(conv.conv_bwd_weight(x, dy, desc, t), dw)
+    assert torch.equal(conv.conv_fwd(2 * x, w, desc, t), 2 * y)
+    # adjoint identity <conv(x,w),dy> = <x,dgrad(dy,w)> = <w,wgrad(x,dy)>
+    a1 = torch.dot(y.double().ravel(), dy.double().ravel())
+    a2 = torch.dot(x.double().ravel(), dx.double().ravel())
+    a3 = torch.dot(w.double().ravel(), dw.double().ravel())
+    assert abs(a1 - a2) <= 1e-4 * abs(a1) and abs(a1 - a3) <= 1e-4 * abs(a1)
+    # oracle on an image slice of the full-batch outputs (images are independent in fwd / dgrad)
+    q = 2
+    xs, ws, dys = x[:q].cpu().numpy().ravel(), w.cpu().numpy().ravel(), dy[:q].cpu().numpy().ravel()
+    assert rel_l2(y[:q].cpu().numpy().ravel(), orc.conv_fwd(xs, ws, q, n, d, k, o, s, p)) <= TOL
+    assert rel_l2(dx[:q].cpu().numpy().ravel(), orc.conv_bwd_data(dys, ws, q, n, d, k, o, s, p)) <= TOL
+
+
+def test_wgrad_full_batch_vs_fp64_gemm(cct, dev):
+    """conv2 b=256 backward-weight (K = 186,624 reduction terms) against an fp64 GEMM of
+    the same lowered matrices computed by torch on the GPU (checker only)."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = 27, 5, 96, 256, 256, 1, 2
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    g = torch.Generator(device=dev).manual_seed(9)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    dy = torch.rand((b, o, desc.m, desc.m), generator=g, device=dev) * 2 - 1
+    dw = conv.conv_bwd_weight(x, dy, desc, 1).double()
+    dh = conv.lower(x, desc, 1, cct.ROWS_INTERNAL).double()                # (b m^2, k^2 d)
+    dr = dy.double().permute(0, 2, 3, 1).reshape(-1, o)                     # (b m^2, o)
+    ref = (dr.t() @ dh).reshape(o, k, k, d)
+    err = float(torch.linalg.norm(dw - ref) / torch.linalg.norm(ref))
+    assert err <= TOL, err
+
+
+# ------------------------------------------------------------- error behaviour
+def test_misaligned_pointer_is_config_error(cct, dev):
+    from paper_1504_04343_b200 import conv
+    desc = cct.ConvDesc(9, 3, 4, 8, 2)
+    buf = torch.zeros(2 * 9 * 9 * 4 + 1, device=dev)
+    x = buf[1:].view(2, 9, 9, 4)
+    w = torch.zeros(8, 3, 3, 4, device=dev)
+    with pytest.raises(cct.ConfigError):
+        conv.conv_fwd(x, w, desc, 1)
+
+
+def test_small_workspace_is_resource_error(cct, dev):
+    import ctypes as C
+    desc = cct.ConvDesc(9, 3, 4, 8, 2)
+    x = torch.zeros(2, 9, 9, 4, device=dev)
+    w = torch.zeros(8, 3, 3, 4, device=dev)
+    y = torch.zeros(2, 8, 7, 7, device=dev)
+    ws = torch.zeros(16, dtype=torch.uint8, device=dev)
+    st = cct.lib().cct_conv_fwd(C.byref(desc.c()), 1, C.c_void_p(x.data_ptr()), C.c_void_p(w.data_ptr()),
+                                C.c_void_p(y.data_ptr()), C.c_void_p(ws.data_ptr()), 16, None)
+    assert st == 2 and b"workspace too small" in cct.lib().cct_last_error()
+
+
+def test_phase_timings(cct, dev):
+    """PhaseTimings: lower / multiply / lift recorded separately."""
+    import ctypes as C
+    from paper_1504_04343_b200 import conv
+    L = cct.lib()
+    desc = cct.ConvDesc(13, 3, 64, 64, 8, 1, 1)
+    x = torch.rand(8, 13, 13, 64, device=dev)
+    w = torch.rand(64, 3, 3, 64, device=dev)
+    P = C.c_double * 7
+    ms, fl, by = P(), P(), P()
+    n = (C.c_uint64 * 7)()
+    L.cct_profile_read(None, None, None, None, 1)
+    L.cct_profile_enable(1)
+    conv.conv_fwd(x, w, desc, 2)
+    L.cct_profile_enable(0)
+    L.cct_profile_read(ms, fl, by, n, 1)
+    assert n[0] == 1 and n[1] >= 1 and n[2] == 1  # lower, gemm, lift
+    assert ms[1] > 0 and fl[1] > 0
