@@ -368,16 +368,15 @@ def run_e2e(a, st, torch, world, group, dev):
                 e.record(copy)
                 evdy.append(e)
         evdy = evdy[::-1]
-        from paper_1504_04343_b200.conv import conv_bwd_data, conv_bwd_weight, conv_fwd
+        from paper_1504_04343_b200.conv import conv_bwd, conv_fwd_cached
         for i, d in enumerate(st.descs):
             comp.wait_event(evx[i])
-            conv_fwd(st.x[i], st.w[i], d, st.types[i], out=st.y[i], ws=st.ws)
+            conv_fwd_cached(st.x[i], st.w[i], d, st.types[i], cache=st.cache[i], out=st.y[i], ws=st.ws)
         handles = []
         for i in reversed(range(nl)):
             d, t = st.descs[i], st.types[i]
             comp.wait_event(evdy[i])
-            conv_bwd_data(st.dy[i], st.w[i], d, t, out=st.dx[i], ws=st.ws)
-            conv_bwd_weight(st.x[i], st.dy[i], d, t, out=st.dw[i], ws=st.ws)
+            conv_bwd(st.dy[i], st.w[i], d, t, x=st.x[i], cache=st.cache[i], dx=st.dx[i], dw=st.dw[i], ws=st.ws)
             if group is not None:
                 handles.append((i, dist.all_reduce(st.dw[i], group=group, async_op=True)))
             else:

@@ -62,7 +62,8 @@ typedef enum {
     CCT_LOWER_T3 = 3  /* Type 3: expensive lifting             */
 } cct_lowering;
 
-typedef enum { CCT_PASS_FWD = 0, CCT_PASS_BWD_DATA = 1, CCT_PASS_BWD_WEIGHT = 2 } cct_pass;
+/* CCT_PASS_BWD = bwd-data + bwd-weight in one call (cct_conv_bwd). */
+typedef enum { CCT_PASS_FWD = 0, CCT_PASS_BWD_DATA = 1, CCT_PASS_BWD_WEIGHT = 2, CCT_PASS_BWD = 3 } cct_pass;
 
 /* Row order of a lowered matrix returned by cct_lower / consumed by cct_lift.
  * SPEC: the reference's c*m+r (T1) / c*n+r (T2, T3) order with n^2 rows per
@@ -103,6 +104,22 @@ CCT_API cct_status cct_conv_bwd_data(const cct_conv_desc* desc, cct_lowering low
 CCT_API cct_status cct_conv_bwd_weight(const cct_conv_desc* desc, cct_lowering lowering, const float* x,
                                const float* dy, float* dw, void* ws, size_t ws_bytes,
                                void* stream);
+
+/* Training-step entry points (the lowered-matrix cache).
+ * cct_conv_fwd_cached leaves the data-side matrix Dhat of the forward pass in a
+ * caller buffer of cct_lowered_cache_size() bytes (0 when Dhat is the input
+ * itself: Type 3, no padding); cct_conv_bwd then runs bwd-data (dx != NULL)
+ * and bwd-weight (dw != NULL) in one call, expanding dy once and reading Dhat
+ * from the cache instead of lowering x again.  x may be NULL when a cache is
+ * given.  AUTO resolves with the fwd+bwd score so both calls pick the same
+ * type.  Workspace: cct_workspace_size(..., CCT_PASS_FWD / CCT_PASS_BWD). */
+CCT_API cct_status cct_lowered_cache_size(const cct_conv_desc* desc, cct_lowering lowering, size_t* bytes);
+CCT_API cct_status cct_conv_fwd_cached(const cct_conv_desc* desc, cct_lowering lowering, const float* x,
+                                       const float* w, float* y, float* cache, size_t cache_bytes, void* ws,
+                                       size_t ws_bytes, void* stream);
+CCT_API cct_status cct_conv_bwd(const cct_conv_desc* desc, cct_lowering lowering, const float* x,
+                                const float* cache, const float* dy, const float* w, float* dx, float* dw,
+                                void* ws, size_t ws_bytes, void* stream);
 
 /* Phase-level API for PhaseTimings and the bit-exact lowering parity.
  * lower: dhat gets the data-side matrix with row stride ld

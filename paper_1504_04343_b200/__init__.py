@@ -18,7 +18,7 @@ from dataclasses import dataclass
 
 __all__ = [
     "lib", "ConvDesc", "CctError", "ConfigError", "ResourceError",
-    "LOWER_AUTO", "LOWER_T1", "LOWER_T2", "LOWER_T3", "PASS_FWD", "PASS_BWD_DATA", "PASS_BWD_WEIGHT",
+    "LOWER_AUTO", "LOWER_T1", "LOWER_T2", "LOWER_T3", "PASS_FWD", "PASS_BWD_DATA", "PASS_BWD_WEIGHT", "PASS_BWD",
     "ROWS_SPEC", "ROWS_INTERNAL",
 ]
 
@@ -26,7 +26,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libcct.so")
 
 LOWER_AUTO, LOWER_T1, LOWER_T2, LOWER_T3 = 0, 1, 2, 3
-PASS_FWD, PASS_BWD_DATA, PASS_BWD_WEIGHT = 0, 1, 2
+PASS_FWD, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_BWD = 0, 1, 2, 3
 ROWS_SPEC, ROWS_INTERNAL = 0, 1
 OK, ERR_CONFIG, ERR_RESOURCE, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 
@@ -87,6 +87,9 @@ def lib() -> C.CDLL:
         "cct_gemm_workspace_size": [I64, I64, I64, C.c_int, P(SZ)],
         "cct_gemm_passes": [I64, I64, I64, VP, I64, VP, I64, VP, I64, C.c_int, VP],
         "cct_select_lowering": [D, P(Calibration), C.c_int, P(C.c_int), P(CostEstimate)],
+        "cct_lowered_cache_size": [D, C.c_int, P(SZ)],
+        "cct_conv_fwd_cached": [D, C.c_int, VP, VP, VP, VP, SZ, VP, SZ, VP],
+        "cct_conv_bwd": [D, C.c_int, VP, VP, VP, VP, VP, VP, VP, SZ, VP],
         "cct_estimate": [D, C.c_int, P(Calibration), C.c_int, P(CostEstimate)],
     }
     for name, args in sigs.items():
@@ -140,6 +143,12 @@ class ConvDesc:
 def workspace_size(desc: ConvDesc, lowering: int, pass_: int) -> int:
     out = C.c_size_t()
     check(lib().cct_workspace_size(C.byref(desc.c()), lowering, pass_, C.byref(out)))
+    return out.value
+
+
+def lowered_cache_size(desc: ConvDesc, lowering: int) -> int:
+    out = C.c_size_t()
+    check(lib().cct_lowered_cache_size(C.byref(desc.c()), lowering, C.byref(out)))
     return out.value
 
 

@@ -12,10 +12,11 @@ import ctypes as C
 
 import torch
 
-from . import (LOWER_AUTO, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_FWD, ROWS_INTERNAL, ROWS_SPEC, ConfigError,
-               ConvDesc, check, lib, workspace_size)
+from . import (LOWER_AUTO, PASS_BWD, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_FWD, ROWS_INTERNAL, ROWS_SPEC,
+               ConfigError, ConvDesc, check, lib, lowered_cache_size, workspace_size)
 
 __all__ = ["Workspace", "conv_fwd", "conv_bwd_data", "conv_bwd_weight", "convolve_lowered", "lower",
+           "conv_fwd_cached", "conv_bwd", "alloc_cache",
            "lower_khat", "lift", "lowered_shape", "multiply", "multiply_passes"]
 
 
@@ -86,6 +87,43 @@ def conv_bwd_weight(x, dy, desc: ConvDesc, lowering: int = LOWER_AUTO, out=None,
     dw = out if out is not None else torch.empty((desc.o, desc.k, desc.k, desc.d), dtype=torch.float32,
                                                  device=x.device)
     return _run(lib().cct_conv_bwd_weight, desc, lowering, PASS_BWD_WEIGHT, x, dy, dw, ws, stream)
+
+
+def alloc_cache(desc: ConvDesc, lowering: int, device) -> torch.Tensor | None:
+    """Buffer for the forward pass's Dhat (None when Dhat is the input itself)."""
+    n = lowered_cache_size(desc, lowering)
+    return torch.empty(n // 4, dtype=torch.float32, device=device) if n else None
+
+
+def conv_fwd_cached(x, w, desc: ConvDesc, lowering: int = LOWER_AUTO, cache=None, out=None, ws=None, stream=None):
+    """Forward that leaves Dhat in `cache` for conv_bwd (training step)."""
+    _need_cuda_f32(x, w)
+    m = desc.m
+    y = out if out is not None else torch.empty((desc.b, desc.o, m, m), dtype=torch.float32, device=x.device)
+    nbytes = workspace_size(desc, lowering, PASS_FWD) if lowering else max(
+        workspace_size(desc, t, PASS_FWD) for t in (1, 2, 3))
+    buf = _ws(ws, x.device).get(nbytes)
+    cb = cache.numel() * 4 if cache is not None else 0
+    check(lib().cct_conv_fwd_cached(C.byref(desc.c()), lowering, _ptr(x), _ptr(w), _ptr(y), _ptr(cache), cb,
+                                    _ptr(buf), buf.numel(), _stream(stream)))
+    return y
+
+
+def conv_bwd(dy, w, desc: ConvDesc, lowering: int = LOWER_AUTO, x=None, cache=None, dx=None, dw=None,
+             want_dx=True, want_dw=True, ws=None, stream=None):
+    """bwd-data + bwd-weight in one call: dy expanded once, Dhat from `cache` if given."""
+    dev = dy.device
+    if want_dx and dx is None:
+        dx = torch.empty((desc.b, desc.n, desc.n, desc.d), dtype=torch.float32, device=dev)
+    if want_dw and dw is None:
+        dw = torch.empty((desc.o, desc.k, desc.k, desc.d), dtype=torch.float32, device=dev)
+    nbytes = workspace_size(desc, lowering, PASS_BWD) if lowering else max(
+        workspace_size(desc, t, PASS_BWD) for t in (1, 2, 3))
+    buf = _ws(ws, dev).get(nbytes)
+    check(lib().cct_conv_bwd(C.byref(desc.c()), lowering, _ptr(x), _ptr(cache), _ptr(dy), _ptr(w),
+                             _ptr(dx if want_dx else None), _ptr(dw if want_dw else None), _ptr(buf), buf.numel(),
+                             _stream(stream)))
+    return dx, dw
 
 
 def lowered_shape(desc: ConvDesc, lowering: int, order: int = ROWS_SPEC):

@@ -8,6 +8,7 @@
 //   FWD  T3: M=b R^2  N=k^2 o K=d      A=Dhat3 (=Xp)      B=W as (ok^2 x d) C -> Rhat^T, lift_t3
 //   BWD_DATA: M=cols(Dhat) N=rows K=ncols  A=W (MN-major) B=dRhat^T (MN-major) C -> dDhat, col2im
 //   BWD_WEIGHT: M=cols N=ncols K=rows   A=Dhat (MN-major) B=dRhat^T (K-major) C -> dW (split-K)
+#include <algorithm>
 #include <cstdio>
 #include <sstream>
 #include <string>
@@ -130,12 +131,18 @@ const float* weights_view(const Lowered& L, const float* w, Ws& ws, cudaStream_t
     return wp;
 }
 
-// Dhat in internal order; T3 with no padding is the input itself.
-const float* dhat_of(const Geo& g, int type, const Lowered& L, const float* x, Ws& ws, cudaStream_t st,
-                     cudaError_t* err) {
+// True when Dhat of this type is the (unpadded, aligned) input itself.
+bool dhat_is_input(const Geo& g, int type, const float* x) {
+    return type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(x);
+}
+
+// Dhat in internal order, written to `dst` when given (the caller's lowered
+// cache) else to the workspace; T3 with no padding is the input itself.
+const float* dhat_of(const Geo& g, int type, const Lowered& L, const float* x, float* dst, Ws& ws,
+                     cudaStream_t st, cudaError_t* err) {
     *err = cudaSuccess;
-    if (type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(x)) return x;
-    float* dh = ws.take(L.rows * L.ldc);
+    if (dhat_is_input(g, type, x)) return x;
+    float* dh = dst ? dst : ws.take(L.rows * L.ldc);
     if (ws.base) *err = lower(g, type, L.rm, x, dh, L.ldc, st);
     return dh;
 }
@@ -166,14 +173,14 @@ int wgrad_splits(const Lowered& L) {
 // the three passes; ws.base == nullptr plans sizes only
 // ---------------------------------------------------------------------------
 
-cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float* y, Ws& ws,
+cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
                    cudaStream_t st) {
     const Lowered L = lowered_of(g, type);
     cudaError_t e;
     int64_t ldw;
     const float* wv = weights_view(L, w, ws, st, &ldw, &e);
     CCT_TRY(e, "pad weights");
-    const float* dh = dhat_of(g, type, L, x, ws, st, &e);
+    const float* dh = dhat_of(g, type, L, x, cache, ws, st, &e);
     CCT_TRY(e, "lower");
     const int64_t ldd = (dh == x) ? g.d : L.ldc;
     GemmProblem gp;
@@ -206,58 +213,65 @@ cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float
     return CCT_OK;
 }
 
-cct_status run_bwd_data(const Geo& g, int type, const float* dy, const float* w, float* dx, Ws& ws,
-                        cudaStream_t st) {
+// Backward: dRhat^T is expanded once and shared by bwd-data (dx != null) and
+// bwd-weight (dw != null).  bwd-weight reads Dhat from `cache` when given (as
+// left there by cct_conv_fwd_cached), else lowers x again.  The two passes run
+// in stream order and reuse the same scratch region after dRhat^T.
+cct_status run_bwd(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
+                   float* dx, float* dw, Ws& ws, cudaStream_t st) {
     const Lowered L = lowered_of(g, type);
     cudaError_t e;
-    int64_t ldw;
-    const float* wv = weights_view(L, w, ws, st, &ldw, &e);
-    CCT_TRY(e, "pad weights");
     float* drt = ws.take(L.ncols * L.ldr);
-    const bool direct = (type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(dx));
-    float* dd = direct ? dx : ws.take(L.rows * L.ldc);
-    const int64_t ldd = direct ? g.d : L.ldc;
     if (ws.base) CCT_TRY(expand(g, type, dy, drt, L.ldr, st), "expand");
-    GemmProblem gp;
-    gp.M = L.cols;
-    gp.N = L.rows;
-    gp.K = L.ncols;
-    gp.A = {wv, ldw, Major::MN};
-    gp.B = {drt, L.ldr, Major::MN};
-    gp.C.s_mr = 1;
-    gp.C.s_n = ldd;
-    cct_status s = gemm_capped(gp, dd, L.rows * ldd, ws, st, "gemm (bwd-data)");
-    if (s != CCT_OK || !ws.base) return s;
-    if (!direct) CCT_TRY(col2im(g, type, dd, ldd, dx, st), "col2im");
-    return CCT_OK;
-}
-
-cct_status run_bwd_weight(const Geo& g, int type, const float* x, const float* dy, float* dw, Ws& ws,
-                          cudaStream_t st) {
-    const Lowered L = lowered_of(g, type);
-    cudaError_t e;
-    const float* dh = dhat_of(g, type, L, x, ws, st, &e);
-    CCT_TRY(e, "lower");
-    const int64_t ldd = (dh == x) ? g.d : L.ldc;
-    float* drt = ws.take(L.ncols * L.ldr);
-    const int splits = wgrad_splits(L);
-    const int64_t wsize = L.ncols * L.cols;
-    float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
-    if (!ws.base) return CCT_OK;
-    CCT_TRY(expand(g, type, dy, drt, L.ldr, st), "expand");
-    GemmProblem gp;
-    gp.M = L.cols;
-    gp.N = L.ncols;
-    gp.K = L.rows;
-    gp.A = {dh, ldd, Major::MN};
-    gp.B = {drt, L.ldr, Major::K};
-    gp.C.ptr = parts;
-    gp.C.s_mr = 1;
-    gp.C.s_n = L.cols;
-    gp.C.s_split = wsize;
-    gp.splits = splits;
-    CCT_TRY(run_gemm(gp, st), "gemm (bwd-weight)");
-    if (splits > 1) CCT_TRY(splitk_reduce(parts, wsize, splits, 1, wsize, wsize, dw, wsize, st), "split-K reduce");
+    const size_t mark = ws.off;
+    size_t hi = mark;
+    if (dx) {
+        int64_t ldw;
+        const float* wv = weights_view(L, w, ws, st, &ldw, &e);
+        CCT_TRY(e, "pad weights");
+        const bool direct = (type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(dx));
+        float* dd = direct ? dx : ws.take(L.rows * L.ldc);
+        const int64_t ldd = direct ? g.d : L.ldc;
+        GemmProblem gp;
+        gp.M = L.cols;
+        gp.N = L.rows;
+        gp.K = L.ncols;
+        gp.A = {wv, ldw, Major::MN};
+        gp.B = {drt, L.ldr, Major::MN};
+        gp.C.s_mr = 1;
+        gp.C.s_n = ldd;
+        cct_status s = gemm_capped(gp, dd, L.rows * ldd, ws, st, "gemm (bwd-data)");
+        if (s != CCT_OK) return s;
+        if (ws.base && !direct) CCT_TRY(col2im(g, type, dd, ldd, dx, st), "col2im");
+        hi = std::max(hi, ws.off);
+        ws.off = mark;  // stream order: bwd-weight may reuse the bwd-data scratch
+    }
+    if (dw) {
+        const float* dh = (cache && !dhat_is_input(g, type, x)) ? cache : dhat_of(g, type, L, x, nullptr, ws, st, &e);
+        CCT_TRY(e, "lower");
+        const int64_t ldd = (dh == x) ? g.d : L.ldc;
+        const int splits = wgrad_splits(L);
+        const int64_t wsize = L.ncols * L.cols;
+        float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
+        if (ws.base) {
+            GemmProblem gp;
+            gp.M = L.cols;
+            gp.N = L.ncols;
+            gp.K = L.rows;
+            gp.A = {dh, ldd, Major::MN};
+            gp.B = {drt, L.ldr, Major::K};
+            gp.C.ptr = parts;
+            gp.C.s_mr = 1;
+            gp.C.s_n = L.cols;
+            gp.C.s_split = wsize;
+            gp.splits = splits;
+            CCT_TRY(run_gemm(gp, st), "gemm (bwd-weight)");
+            if (splits > 1)
+                CCT_TRY(splitk_reduce(parts, wsize, splits, 1, wsize, wsize, dw, wsize, st), "split-K reduce");
+        }
+        hi = std::max(hi, ws.off);
+    }
+    ws.off = hi;
     return CCT_OK;
 }
 
@@ -302,10 +316,12 @@ cct_status cct_workspace_size(const cct_conv_desc* desc, cct_lowering lowering, 
     Ws ws(nullptr);
     // dummy, 16-byte aligned non-null pointers so zero-copy decisions match the real call
     const float* dummy = reinterpret_cast<const float*>(uintptr_t(256));
-    switch (pass) {
-    case CCT_PASS_FWD: s = run_fwd(g, type, dummy, dummy, nullptr, ws, nullptr); break;
-    case CCT_PASS_BWD_DATA: s = run_bwd_data(g, type, dummy, dummy, reinterpret_cast<float*>(uintptr_t(256)), ws, nullptr); break;
-    case CCT_PASS_BWD_WEIGHT: s = run_bwd_weight(g, type, dummy, dummy, nullptr, ws, nullptr); break;
+    float* dout = reinterpret_cast<float*>(uintptr_t(256));
+    switch (int(pass)) {
+    case CCT_PASS_FWD: s = run_fwd(g, type, dummy, dummy, nullptr, nullptr, ws, nullptr); break;
+    case CCT_PASS_BWD_DATA: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, dout, nullptr, ws, nullptr); break;
+    case CCT_PASS_BWD_WEIGHT: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, nullptr, dout, ws, nullptr); break;
+    case CCT_PASS_BWD: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, dout, dout, ws, nullptr); break;
     default: return fail(CCT_ERR_CONFIG, "unknown pass");
     }
     *bytes = ws.off + 256;
@@ -331,9 +347,9 @@ static cct_status run_pass(const cct_conv_desc* desc, cct_lowering lowering, cct
     Ws ws(wsp);
     cudaStream_t st = as_stream(stream);
     switch (pass) {
-    case CCT_PASS_FWD: return run_fwd(g, type, a, b, out, ws, st);
-    case CCT_PASS_BWD_DATA: return run_bwd_data(g, type, a, b, out, ws, st);
-    default: return run_bwd_weight(g, type, a, b, out, ws, st);
+    case CCT_PASS_FWD: return run_fwd(g, type, a, b, out, nullptr, ws, st);
+    case CCT_PASS_BWD_DATA: return run_bwd(g, type, nullptr, nullptr, a, b, out, nullptr, ws, st);
+    default: return run_bwd(g, type, a, nullptr, b, nullptr, nullptr, out, ws, st);
     }
 }
 
@@ -350,6 +366,65 @@ cct_status cct_conv_bwd_data(const cct_conv_desc* desc, cct_lowering lowering, c
 cct_status cct_conv_bwd_weight(const cct_conv_desc* desc, cct_lowering lowering, const float* x,
                                const float* dy, float* dw, void* ws, size_t ws_bytes, void* stream) {
     return run_pass(desc, lowering, CCT_PASS_BWD_WEIGHT, x, dy, dw, ws, ws_bytes, stream);
+}
+
+static int resolve_train(const cct_conv_desc* d, cct_lowering l) {
+    // fwd_cached and bwd must agree on the type (the cache layout depends on it):
+    // AUTO scores fwd + bwd together.
+    return resolve(d, l, cct_pass(CCT_PASS_BWD));
+}
+
+cct_status cct_lowered_cache_size(const cct_conv_desc* desc, cct_lowering lowering, size_t* bytes) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    if (!bytes) return fail(CCT_ERR_CONFIG, "null size pointer");
+    const Geo g = geo_of(desc);
+    const int type = resolve_train(desc, lowering);
+    const Lowered L = lowered_of(g, type);
+    const float* aligned = reinterpret_cast<const float*>(uintptr_t(256));
+    *bytes = dhat_is_input(g, type, aligned) ? 0 : size_t(L.rows * L.ldc) * sizeof(float);
+    return CCT_OK;
+}
+
+cct_status cct_conv_fwd_cached(const cct_conv_desc* desc, cct_lowering lowering, const float* x, const float* w,
+                               float* y, float* cache, size_t cache_bytes, void* wsp, size_t ws_bytes,
+                               void* stream) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    if ((s = check_ptrs({x, w, y})) != CCT_OK) return s;
+    if (!aligned16(x) || !aligned16(w) || !aligned16(y) || (cache && !aligned16(cache)))
+        return fail(CCT_ERR_CONFIG, "tensor pointers must be 16-byte aligned");
+    const int type = resolve_train(desc, lowering);
+    size_t need = 0, cneed = 0;
+    cct_workspace_size(desc, cct_lowering(type), CCT_PASS_FWD, &need);
+    cct_lowered_cache_size(desc, cct_lowering(type), &cneed);
+    if (cache && cache_bytes < cneed) return fail(CCT_ERR_RESOURCE, "lowered cache too small for " + desc_str(desc));
+    if (!wsp || ws_bytes < need) return fail(CCT_ERR_RESOURCE, "workspace too small for " + desc_str(desc));
+    Ws ws(wsp);
+    return run_fwd(geo_of(desc), type, x, w, y, cneed ? cache : nullptr, ws, as_stream(stream));
+}
+
+cct_status cct_conv_bwd(const cct_conv_desc* desc, cct_lowering lowering, const float* x, const float* cache,
+                        const float* dy, const float* w, float* dx, float* dw, void* wsp, size_t ws_bytes,
+                        void* stream) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    if (!dy || (!dx && !dw)) return fail(CCT_ERR_CONFIG, "cct_conv_bwd needs dy and at least one of dx, dw");
+    if (dx && !w) return fail(CCT_ERR_CONFIG, "bwd-data needs w");
+    if (dw && !x && !cache) return fail(CCT_ERR_CONFIG, "bwd-weight needs x or a lowered cache");
+    for (const void* p : {static_cast<const void*>(x), static_cast<const void*>(cache), static_cast<const void*>(dy),
+                          static_cast<const void*>(w), static_cast<const void*>(dx), static_cast<const void*>(dw)})
+        if (p && !aligned16(p)) return fail(CCT_ERR_CONFIG, "tensor pointers must be 16-byte aligned");
+    const int type = resolve_train(desc, lowering);
+    size_t need = 0;
+    cct_workspace_size(desc, cct_lowering(type), CCT_PASS_BWD, &need);
+    if (!wsp || ws_bytes < need) return fail(CCT_ERR_RESOURCE, "workspace too small for " + desc_str(desc));
+    Ws ws(wsp);
+    const Geo g = geo_of(desc);
+    // a cache is only meaningful when Dhat is not the input itself
+    const float* c = (cache && !(x && dhat_is_input(g, type, x))) ? cache : nullptr;
+    if (dw && !x && !c) return fail(CCT_ERR_CONFIG, "bwd-weight needs x for this lowering");
+    return run_bwd(g, type, x, c, dy, w, dx, dw, ws, as_stream(stream));
 }
 
 // ---- phase-level API ---------------------------------------------------------

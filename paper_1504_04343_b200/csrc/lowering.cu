@@ -75,27 +75,32 @@ __global__ void lower_kernel(const float* __restrict__ x, float* __restrict__ dh
         // valid pixel interval [jlo, jhi) of the run
         const int jlo = max(0, -xs0), jhi = min(taps, n - xs0);
         const float* xq = x + q * int64_t(n) * n * d;
-        for (int i = 0; i < nruns; ++i) {
-            const int ys = ys0 + ((type == 1) ? i : 0);
-            const bool row_ok = !zero_row && ys >= 0 && ys < n && jlo < jhi;
-            const int lo = jlo * d / W, hi = jhi * d / W;  // in elements of W floats
-            const float* src = xq + (int64_t(ys) * n + xs0) * d;
-            float* dst = row + i * L;
-            if constexpr (VEC4) {
-                const float4* s4 = reinterpret_cast<const float4*>(src);
-                float4* d4 = reinterpret_cast<float4*>(dst);
+        if constexpr (VEC4) {
+            for (int i = 0; i < nruns; ++i) {
+                const int ys = ys0 + ((type == 1) ? i : 0);
+                const bool row_ok = !zero_row && ys >= 0 && ys < n && jlo < jhi;
+                const int lo = jlo * d / W, hi = jhi * d / W;  // in elements of W floats
+                const float4* s4 = reinterpret_cast<const float4*>(xq + (int64_t(ys) * n + xs0) * d);
+                float4* d4 = reinterpret_cast<float4*>(row + i * L);
 #pragma unroll 4
                 for (int e = lane; e < L / 4; e += 32) {
                     float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
                     if (row_ok && e >= lo && e < hi) v = __ldg(s4 + e);
                     d4[e] = v;
                 }
-            } else {
-                for (int e = lane; e < L; e += 32) {
-                    float v = 0.f;
-                    if (row_ok && e >= lo && e < hi) v = __ldg(src + e);
-                    dst[e] = v;
-                }
+            }
+        } else {
+            // flattened over the whole row so every lane works (run length k*d
+            // is rarely a multiple of 32 when d is small, e.g. conv1 d = 3)
+            const int lo = jlo * d, hi = jhi * d;
+#pragma unroll 4
+            for (int e = lane; e < cols; e += 32) {
+                const int i = e / L, r = e - i * L;
+                const int ys = ys0 + ((type == 1) ? i : 0);
+                float v = 0.f;
+                if (!zero_row && ys >= 0 && ys < n && r >= lo && r < hi)
+                    v = __ldg(xq + (int64_t(ys) * n + xs0) * d + r);
+                row[e] = v;
             }
         }
         for (int e = cols + lane; e < ld; e += 32) row[e] = 0.f;  // pad columns

@@ -17,8 +17,8 @@ from dataclasses import dataclass
 
 import torch
 
-from . import LOWER_AUTO, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_FWD, ConvDesc, select_lowering, workspace_size
-from .conv import Workspace, conv_bwd_data, conv_bwd_weight, conv_fwd
+from . import LOWER_AUTO, PASS_BWD, PASS_FWD, ConvDesc, select_lowering, workspace_size
+from .conv import Workspace, alloc_cache, conv_bwd, conv_fwd_cached
 
 __all__ = ["LayerSpec", "CAFFENET", "ConvStack", "stack_flops_per_image"]
 
@@ -81,8 +81,10 @@ class ConvStack:
         self.y = [torch.empty_like(t) for t in self.dy]
         self.dx = [torch.empty_like(t) for t in self.x]
         self.dw = [torch.empty_like(t) for t in self.w]
+        # Dhat of every layer stays resident from fwd to bwd-weight (lowered once)
+        self.cache = [alloc_cache(d, t, device) for d, t in zip(self.descs, self.types)]
         need = max(workspace_size(d, t, p) for d, t in zip(self.descs, self.types)
-                   for p in (PASS_FWD, PASS_BWD_DATA, PASS_BWD_WEIGHT))
+                   for p in (PASS_FWD, PASS_BWD))
         self.ws = Workspace(device)
         self.ws.get(need)
         self.ws_bytes = need
@@ -92,14 +94,15 @@ class ConvStack:
 
     def forward(self, stream=None):
         for i, d in enumerate(self.descs):
-            conv_fwd(self.x[i], self.w[i], d, self.types[i], out=self.y[i], ws=self.ws, stream=stream)
+            conv_fwd_cached(self.x[i], self.w[i], d, self.types[i], cache=self.cache[i], out=self.y[i],
+                            ws=self.ws, stream=stream)
 
     def backward(self, stream=None, allreduce: bool = True):
         handles = []
         for i in reversed(range(len(self.descs))):
             d, t = self.descs[i], self.types[i]
-            conv_bwd_data(self.dy[i], self.w[i], d, t, out=self.dx[i], ws=self.ws, stream=stream)
-            conv_bwd_weight(self.x[i], self.dy[i], d, t, out=self.dw[i], ws=self.ws, stream=stream)
+            conv_bwd(self.dy[i], self.w[i], d, t, x=self.x[i], cache=self.cache[i], dx=self.dx[i],
+                     dw=self.dw[i], ws=self.ws, stream=stream)
             if allreduce and self.group is not None:
                 import torch.distributed as dist
                 # NCCL waits on the current stream, then reduces on its own stream,
