@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "gemm.cuh"
@@ -45,13 +46,18 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
     return (2 * bn) <= 32 ? 32 : (2 * bn) <= 64 ? 64 : (2 * bn) <= 128 ? 128 : (2 * bn) <= 256 ? 256 : 512;
 }
 
-template <int BN>
+// Per-CTA tile geometry.  CG = 1: one CTA computes 128 x BN.  CG = 2 (CTA
+// pair, tcgen05 cta_group::2): the pair computes 256 x BN; each CTA holds its
+// 128 rows of A and BN/2 rows of B in smem and its 128 rows of D in TMEM.
+template <int BN, int CG>
 struct Cfg {
+    static constexpr int BNL = BN / CG;  // B rows loaded by this CTA
     static constexpr uint32_t A_BYTES = kBM * kBK * 4;
-    static constexpr uint32_t B_BYTES = BN * kBK * 4;
+    static constexpr uint32_t B_BYTES = BNL * kBK * 4;
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t STAGE_BYTES = 2 * RAW_BYTES;  // raw | small
-    static constexpr int STAGES = (200 * 1024 / STAGE_BYTES) > 8 ? 8 : (200 * 1024 / STAGE_BYTES);
+    // as many ring stages as fit next to the barriers (227 KB opt-in smem per CTA)
+    static constexpr int STAGES = ((225 * 1024) / STAGE_BYTES) > 8 ? 8 : ((225 * 1024) / STAGE_BYTES);
     static constexpr uint32_t BAR_BYTES = (3 * STAGES + 4) * 8 + 16;
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
     static constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
@@ -83,12 +89,13 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int kk) {
     }
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const KParams p) {
-    using C_ = Cfg<BN>;
+    using C_ = Cfg<BN, CG>;
     constexpr int STAGES = C_::STAGES;
+    constexpr int BNL = C_::BNL;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align inside the shared window without leaving the shared address space
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -101,38 +108,48 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
+    const uint32_t rank = (CG == 2) ? ptx::cluster_rank() : 0u;
+    const bool leader = rank == 0;
+    // work is distributed per CTA group (cluster)
+    const int group = blockIdx.x / CG;
+    const int ngroups = gridDim.x / CG;
 
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&tdone[s], 4);
+            ptx::mbar_init(&tdone[s], 4 * CG);   // transform warps of every CTA in the group
             ptx::mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
-            ptx::mbar_init(&tempty[a], 4);
+            ptx::mbar_init(&tempty[a], 4 * CG);  // epilogue warps of every CTA in the group
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc<C_::TMEM_COLS>(tmem_slot);
+    if (warp == 2) ptx::tmem_alloc<C_::TMEM_COLS, CG>(tmem_slot);
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync();
+    else __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    // leader-CTA barriers seen from this CTA (remote arrive targets)
+    const uint32_t tdone_leader = (CG == 2) ? ptx::mapa(ptx::smem_u32(tdone), 0) : 0u;
+    const uint32_t tempty_leader = (CG == 2) ? ptx::mapa(ptx::smem_u32(tempty), 0) : 0u;
 
     if (warp == 0) {
-        // ===================== TMA producer =====================
+        // ===================== TMA producer (every CTA loads its own share) =====================
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+            for (int u = group; u < p.units; u += ngroups) {
                 const int mt = u % p.num_m_tiles;
                 const int rest = u / p.num_m_tiles;
                 const int nt = rest % p.num_n_tiles;
                 const int sp = rest / p.num_n_tiles;
-                const int m0 = mt * kBM, n0 = nt * BN;
+                const int m0 = mt * (kBM * CG) + int(rank) * kBM;
+                const int n0 = nt * BN + int(rank) * BNL;
                 const int kb0 = sp * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
                 for (int kb = kb0; kb < kb1; ++kb) {
@@ -152,7 +169,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
                     } else {
 #pragma unroll
-                        for (int c = 0; c < BN / 32; ++c)
+                        for (int c = 0; c < BNL / 32; ++c)
                             ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage], n0 + 32 * c, k0);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -160,13 +177,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     } else if (warp == 1) {
-        // ===================== MMA issuer =====================
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_tf32(kBM, BN, A_MN, B_MN);
+        // ===================== MMA issuer (leader CTA only) =====================
+        if (lane == 0 && leader) {
+            constexpr uint32_t idesc = ptx::idesc_tf32(kBM * CG, BN, A_MN, B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+            for (int u = group; u < p.units; u += ngroups, ++local) {
                 const int rest = u / p.num_m_tiles;
                 const int sp = rest / p.num_n_tiles;
                 const int kb0 = sp * p.kb_per_split;
@@ -177,8 +194,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
                 for (int kb = kb0; kb < kb1; ++kb) {
-                    ptx::mbar_wait(&full[stage], phase);
-                    if (p.passes == 3) ptx::mbar_wait(&tdone[stage], phase);
+                    // tdone implies the raw tiles of every CTA in the group landed
+                    // (each transform warp waited on its own CTA's full barrier)
+                    ptx::mbar_wait(&tdone[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a_raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
                     const uint32_t b_raw = a_raw + C_::A_BYTES;
@@ -188,27 +206,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int kk = 0; kk < kBK / 8; ++kk) {
                         const uint64_t ad = tile_desc<A_MN>(a_raw, kk);
                         const uint64_t bd = tile_desc<B_MN>(b_raw, kk);
-                        if (p.passes == 3) {
-                            // small products first, big*big last
-                            ptx::mma_tf32(d_tmem, tile_desc<A_MN>(a_sml, kk), bd, idesc,
-                                          (kb > kb0 || kk > 0) ? 1u : 0u);
-                            ptx::mma_tf32(d_tmem, ad, tile_desc<B_MN>(b_sml, kk), idesc, 1u);
-                            ptx::mma_tf32(d_tmem, ad, bd, idesc, 1u);
+                        const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
+                        if constexpr (CG == 1) {
+                            if (p.passes == 3) {
+                                // small products first, big*big last
+                                ptx::mma_tf32(d_tmem, tile_desc<A_MN>(a_sml, kk), bd, idesc, first);
+                                ptx::mma_tf32(d_tmem, ad, tile_desc<B_MN>(b_sml, kk), idesc, 1u);
+                                ptx::mma_tf32(d_tmem, ad, bd, idesc, 1u);
+                            } else {
+                                ptx::mma_tf32(d_tmem, ad, bd, idesc, first);
+                            }
                         } else {
-                            ptx::mma_tf32(d_tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
+                            if (p.passes == 3) {
+                                ptx::mma_tf32_cg2(d_tmem, tile_desc<A_MN>(a_sml, kk), bd, idesc, first);
+                                ptx::mma_tf32_cg2(d_tmem, ad, tile_desc<B_MN>(b_sml, kk), idesc, 1u);
+                                ptx::mma_tf32_cg2(d_tmem, ad, bd, idesc, 1u);
+                            } else {
+                                ptx::mma_tf32_cg2(d_tmem, ad, bd, idesc, first);
+                            }
                         }
                     }
-                    ptx::mma_commit(&empty[stage]);
+                    if constexpr (CG == 1) ptx::mma_commit(&empty[stage]);
+                    else ptx::mma_commit_cg2(&empty[stage], 0x3);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                ptx::mma_commit(&tfull[acc]);
+                if constexpr (CG == 1) ptx::mma_commit(&tfull[acc]);
+                else ptx::mma_commit_cg2(&tfull[acc], 0x3);
             }
         }
     } else if (warp >= 4 && warp < 8) {
-        // ===================== epilogue =====================
+        // ===================== epilogue (own TMEM lanes = own 128 rows) =====================
         const int q = warp & 3;
         int local = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x, ++local) {
+        for (int u = group; u < p.units; u += ngroups, ++local) {
             const int mt = u % p.num_m_tiles;
             const int rest = u / p.num_m_tiles;
             const int nt = rest % p.num_n_tiles;
@@ -217,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t use = uint32_t(local >> 1);
             ptx::mbar_wait(&tfull[acc], use & 1);
             ptx::tc_fence_after();
-            const int64_t row = int64_t(mt) * kBM + q * 32 + lane;
+            const int64_t row = int64_t(mt) * (kBM * CG) + int64_t(rank) * kBM + q * 32 + lane;
             const bool row_ok = row < p.M;
             int64_t off = 0;
             if (row_ok) off = (row / p.mdiv) * p.s_mq + (row % p.mdiv) * p.s_mr + int64_t(sp) * p.s_split;
@@ -246,14 +276,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+            if (lane == 0) {
+                if constexpr (CG == 1) ptx::mbar_arrive(&tempty[acc]);
+                else ptx::mbar_arrive_remote(tempty_leader + uint32_t(acc * 8));
+            }
         }
     } else if (warp >= 8) {
-        // ===================== 3xTF32 transform =====================
+        // ===================== 3xTF32 transform (own tiles) =====================
         const int t = threadIdx.x - 256;
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        for (int u = group; u < p.units; u += ngroups) {
             const int rest = u / p.num_m_tiles;
             const int sp = rest / p.num_n_tiles;
             const int kb0 = sp * p.kb_per_split;
@@ -271,17 +304,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::fence_proxy_async_smem();
                 }
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&tdone[stage]);
+                if (lane == 0) {
+                    if constexpr (CG == 1) ptx::mbar_arrive(&tdone[stage]);
+                    else ptx::mbar_arrive_remote(tdone_leader + uint32_t(stage * 8));
+                }
                 if (++stage == STAGES) { stage = 0; phase ^= 1; }
             }
         }
     }
 
     ptx::tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) ptx::cluster_sync();
+    else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<C_::TMEM_COLS>(tmem_base);
+        ptx::tmem_dealloc<C_::TMEM_COLS, CG>(tmem_base);
     }
 }
 
@@ -330,31 +367,58 @@ bool make_tmap(CUtensorMap* map, const Operand& op, int64_t mn_extent, int64_t k
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int A_MN, int B_MN>
+template <int BN, int A_MN, int B_MN, int CG>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, cudaStream_t st) {
-    using C_ = Cfg<BN>;
-    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN>;
+    using C_ = Cfg<BN, CG>;
+    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr_set = true;
     }
-    const int grid = std::min(kp.units, num_sms());
+    const int sms = num_sms() / CG * CG;
+    const int grid = std::min(kp.units * CG, sms);
     PhaseScope ps(kPhaseGemm, st, 2.0 * double(kp.M) * double(kp.N) * double(kp.K), 0);
-    kern<<<grid, kThreads, C_::SMEM_BYTES, st>>>(ta, tb, kp);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(unsigned(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C_::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ta, tb, kp);
     note_launch();
+    if (e != cudaSuccess) return e;
     return cudaGetLastError();
 }
 
-template <int BN>
+template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
-    if (!amn && !bmn) return launch<BN, 0, 0>(ta, tb, kp, st);
-    if (amn && bmn) return launch<BN, 1, 1>(ta, tb, kp, st);
-    if (amn && !bmn) return launch<BN, 1, 0>(ta, tb, kp, st);
-    return launch<BN, 0, 1>(ta, tb, kp, st);
+    if (!amn && !bmn) return launch<BN, 0, 0, CG>(ta, tb, kp, st);
+    if (amn && bmn) return launch<BN, 1, 1, CG>(ta, tb, kp, st);
+    if (amn && !bmn) return launch<BN, 1, 0, CG>(ta, tb, kp, st);
+    return launch<BN, 0, 1, CG>(ta, tb, kp, st);
+}
+
+// CTA-pair mode needs >= 2 row tiles and, for an MN-major B, B halves that are
+// whole 32-column TMA boxes.
+int choose_cg(const GemmProblem& g, int bn) {
+    static const int forced = [] {
+        const char* e = getenv("CCT_GEMM_CG");
+        return e ? atoi(e) : 0;
+    }();
+    const bool ok2 = (g.B.major == Major::K) ? (bn / 2) % 8 == 0 : (bn / 2) % 32 == 0;
+    if (forced == 1 || !ok2) return 1;
+    if (forced == 2) return 2;
+    return (g.M > kBM) ? 2 : 1;
 }
 
 }  // namespace
@@ -410,15 +474,28 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.s_n = g.C.s_n;
     kp.s_split = g.C.s_split;
 
+    const int cg = choose_cg(g, bn);
+    kp.num_m_tiles = int((g.M + kBM * cg - 1) / (kBM * cg));
+    kp.units = kp.num_m_tiles * kp.num_n_tiles * kp.splits;
     CUtensorMap ta, tb;
     if (!make_tmap(&ta, g.A, g.M, g.K, kBM)) return cudaErrorInvalidValue;
-    if (!make_tmap(&tb, g.B, g.N, g.K, bn)) return cudaErrorInvalidValue;
+    if (!make_tmap(&tb, g.B, g.N, g.K, bn / cg)) return cudaErrorInvalidValue;
+    if (cg == 2) {
+        switch (bn) {
+        case 256: return dispatch_layout<256, 2>(g, ta, tb, kp, stream);
+        case 192: return dispatch_layout<192, 2>(g, ta, tb, kp, stream);
+        case 128: return dispatch_layout<128, 2>(g, ta, tb, kp, stream);
+        case 96: return dispatch_layout<96, 2>(g, ta, tb, kp, stream);
+        case 64: return dispatch_layout<64, 2>(g, ta, tb, kp, stream);
+        default: return cudaErrorInvalidValue;
+        }
+    }
     switch (bn) {
-    case 256: return dispatch_layout<256>(g, ta, tb, kp, stream);
-    case 192: return dispatch_layout<192>(g, ta, tb, kp, stream);
-    case 128: return dispatch_layout<128>(g, ta, tb, kp, stream);
-    case 96: return dispatch_layout<96>(g, ta, tb, kp, stream);
-    case 64: return dispatch_layout<64>(g, ta, tb, kp, stream);
+    case 256: return dispatch_layout<256, 1>(g, ta, tb, kp, stream);
+    case 192: return dispatch_layout<192, 1>(g, ta, tb, kp, stream);
+    case 128: return dispatch_layout<128, 1>(g, ta, tb, kp, stream);
+    case 96: return dispatch_layout<96, 1>(g, ta, tb, kp, stream);
+    case 64: return dispatch_layout<64, 1>(g, ta, tb, kp, stream);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -28,7 +28,7 @@ SHAPES = {
 }
 
 
-def run(M, N, K, amaj, bmaj, passes, bn=0, reps=10):
+def run(M, N, K, amaj, bmaj, passes, bn=0, reps=10, cmaj=0):
     dev = torch.device("cuda")
     A = torch.rand((K, M) if amaj else (M, K), device=dev)
     B = torch.rand((K, N) if bmaj else (N, K), device=dev)
@@ -36,8 +36,10 @@ def run(M, N, K, amaj, bmaj, passes, bn=0, reps=10):
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
     def go():
+        # cmaj = 1: column-major C (lanes = rows contiguous), as the conv passes store
+        ldm, ldn = (1, M) if cmaj else (N, 1)
         rc = L.cct_debug_gemm(M, N, K, A.data_ptr(), A.shape[1], amaj, B.data_ptr(), B.shape[1], bmaj,
-                              Cm.data_ptr(), N, 1, passes, bn, st)
+                              Cm.data_ptr(), ldm, ldn, passes, bn, st)
         assert rc == 0, L.cct_last_error()
 
     for _ in range(3):
@@ -58,14 +60,17 @@ if __name__ == "__main__":
     ap.add_argument("--only", default=None)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--bn", type=int, default=0)
+    ap.add_argument("--layouts", default="kk,mm,mk,km")
+    ap.add_argument("--passes", default="1,3")
     a = ap.parse_args()
     for name, (M, N, K) in SHAPES.items():
         if a.only and a.only != name:
             continue
-        for amaj, bmaj in ((0, 0), (1, 1), (1, 0), (0, 1)):
+        lay = {"kk": (0, 0), "mm": (1, 1), "mk": (1, 0), "km": (0, 1)}
+        for amaj, bmaj in (lay[x] for x in a.layouts.split(",")):
             res = []
-            for passes in (1, 3):
-                ms, tf = run(M, N, K, amaj, bmaj, passes, a.bn, a.reps)
+            for passes in (int(x) for x in a.passes.split(",")):
+                ms, tf = run(M, N, K, amaj, bmaj, passes, a.bn, a.reps, cmaj=1)
                 res.append(f"p{passes}: {ms:7.3f} ms {tf:6.1f} TF/s")
             print(f"{name:11s} M={M} N={N} K={K} A={'MN' if amaj else 'K '} B={'MN' if bmaj else 'K '} | "
                   + " | ".join(res), flush=True)

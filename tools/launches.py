@@ -20,5 +20,5 @@ for (i, k), v in sorted(agg.items()):
     t = v.get("gpu__time_duration.sum", 0) / 1e3
     by = (v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0)) / 1e6
     tot += t
-    print(f"{i:>4} {k[:44]:44s} {t:9.1f} us {by:9.1f} MB {by / t / 1e3 if t else 0:6.2f} TB/s")
+    print(f"{i:>4} {k[:44]:44s} {t:9.1f} us {by:9.1f} MB {by / t if t else 0:6.2f} TB/s")
 print(f"total {tot:.1f} us")
