@@ -418,7 +418,11 @@ int choose_cg(const GemmProblem& g, int bn) {
     const bool ok2 = (g.B.major == Major::K) ? (bn / 2) % 8 == 0 : (bn / 2) % 32 == 0;
     if (forced == 1 || !ok2) return 1;
     if (forced == 2) return 2;
-    return (g.M > kBM) ? 2 : 1;
+    if (g.M <= kBM) return 1;
+    // pairs tile M by 256: only when that adds (almost) no padding over 128-row tiles
+    const int64_t pad1 = (g.M + kBM - 1) / kBM * kBM - g.M;
+    const int64_t pad2 = (g.M + 2 * kBM - 1) / (2 * kBM) * (2 * kBM) - g.M;
+    return (pad2 - pad1) * 20 <= g.M ? 2 : 1;
 }
 
 }  // namespace

@@ -46,6 +46,15 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// 4-byte asynchronous global -> shared copy (LDGSTS): the staging loops issue
+// every copy before waiting, instead of one blocking load per iteration.
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+                 "l"(gsrc)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // One warp per lowered row (q, y, c).  The row is `nruns` runs of L source
 // floats that are contiguous in x (T1: k runs of k*d; T2: 1 run of k*d; T3: 1
 // run of d).  The in-image part of a run is one contiguous interval, computed
@@ -249,6 +258,120 @@ __global__ void col2im_kernel(const float* __restrict__ dd, int64_t ld, float* _
     }
 }
 
+// ---- small-channel Type 1 kernels (d % 4 != 0, e.g. conv1 d = 3) -----------
+// The generic kernels move 4-byte elements with run lengths (k*d) that are not
+// multiples of 4; these stage the data through shared memory so every global
+// access is a float4 (or a contiguous run) and each byte moves once.
+
+// Lowering: one CTA per output row (q, r).  The k input rows it needs
+// (s*r - p + i, zero rows outside the image) are staged in smem with async
+// copies, zero-padded to the padded width; each lowered row (q, r, c) is then
+// written as float4s by one warp through an offset table.  All index tables
+// are built once per CTA, so the per-row loops do no integer division.
+__global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restrict__ dh, Geo g, RowMap rm,
+                                     int64_t ld, int cols) {
+    extern __shared__ float sm[];
+    const int n = int(g.n), d = int(g.d), k = int(g.k), s = int(g.s), p = int(g.p), m = int(g.m);
+    const int Wp = n + 2 * p;
+    const int rowf = Wp * d;                                   // floats per staged row
+    float* tile = sm;                                          // k x rowf
+    int* offs = reinterpret_cast<int*>(sm + k * rowf);         // cols: lowered column -> tile index (c = 0)
+    int* soff = offs + cols;                                   // rowf: staged float -> x offset in row, or -1
+    for (int e = threadIdx.x; e < cols; e += blockDim.x) {
+        const int i = e / (k * d), rr = e - i * (k * d), j = rr / d, ch = rr - j * d;
+        offs[e] = i * rowf + j * d + ch;
+    }
+    for (int e = threadIdx.x; e < rowf; e += blockDim.x) {
+        const int xs = e / d - p;
+        soff[e] = (xs >= 0 && xs < n) ? xs * d + (e - (e / d) * d) : -1;
+    }
+    const int ld4 = int(ld / 4);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    const int64_t nqr = g.b * m;
+    for (int64_t qr = blockIdx.x; qr < nqr; qr += gridDim.x) {
+        const int r = int(qr % m);
+        const int64_t q = qr / m;
+        __syncthreads();  // tables ready / previous tile consumed
+        for (int e = threadIdx.x; e < rowf; e += blockDim.x) {
+            const int so = soff[e];
+            for (int i = 0; i < k; ++i) {
+                const int ys = s * r - p + i;
+                if (so >= 0 && ys >= 0 && ys < n) cp_async4(tile + i * rowf + e, x + ((q * n + ys) * int64_t(n)) * d + so);
+                else tile[i * rowf + e] = 0.f;
+            }
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        for (int c = warp; c < m; c += nwarps) {
+            const int base = s * c * d;
+            float4* row = reinterpret_cast<float4*>(dh + (q * rm.rpi + int64_t(r) * rm.sr + int64_t(c) * rm.sc) * ld);
+            for (int e4 = lane; e4 < ld4; e4 += 32) {
+                const int e = 4 * e4;
+                float4 v;
+                v.x = e < cols ? tile[offs[e] + base] : 0.f;
+                v.y = e + 1 < cols ? tile[offs[e + 1] + base] : 0.f;
+                v.z = e + 2 < cols ? tile[offs[e + 2] + base] : 0.f;
+                v.w = e + 3 < cols ? tile[offs[e + 3] + base] : 0.f;
+                row[e4] = v;
+            }
+        }
+    }
+}
+
+// col2im (Type 1): one CTA per input row (q, y).  The (r, i) pairs with
+// s*r + i == y + p contribute; for each, the k*d-float slice i of the m rows
+// (q, r, c) is staged in smem (async copies through a precomputed offset
+// table), then every dx element of the row sums its taps from smem using
+// per-element tap metadata built once.  Each dDhat element is read once.
+__global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t ld, float* __restrict__ dx, Geo g) {
+    extern __shared__ float sm[];
+    const int n = int(g.n), d = int(g.d), k = int(g.k), s = int(g.s), p = int(g.p), m = int(g.m);
+    const int kd = k * d, slab = m * kd;
+    const int npair_max = (k + s - 1) / s;
+    int* stab = reinterpret_cast<int*>(sm + npair_max * slab);  // slab: staged float -> c*ld + rr
+    int* meta = stab + slab;                                     // n*d: (ch | j0 << 8 | c0 << 16)
+    for (int e = threadIdx.x; e < slab; e += blockDim.x) {
+        const int c = e / kd;
+        stab[e] = c * int(ld) + (e - c * kd);
+    }
+    for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
+        const int xx = e / d, ch = e - xx * d, px = xx + p;
+        meta[e] = ch | ((px % s) << 8) | ((px / s) << 16);
+    }
+    const int64_t nqy = g.b * n;
+    for (int64_t qy = blockIdx.x; qy < nqy; qy += gridDim.x) {
+        const int yy = int(qy % n);
+        const int64_t q = qy / n;
+        const int py = yy + p;
+        // pairs (r, i), ascending i: r from min(m-1, py/s) down while i = py - s r < k
+        const int rtop = min(m - 1, py / s);
+        int np = 0;
+        while (np < npair_max && rtop - np >= 0 && py - s * (rtop - np) < k) ++np;
+        __syncthreads();  // previous slabs consumed
+        for (int a = 0; a < np; ++a) {
+            const int r = rtop - a, i = py - s * r;
+            const float* src = dd + ((q * m + r) * int64_t(m)) * ld + int64_t(i) * kd;
+            float* dst = sm + a * slab;
+            for (int e = threadIdx.x; e < slab; e += blockDim.x) cp_async4(dst + e, src + stab[e]);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        float* out = dx + qy * int64_t(n) * d;
+        for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
+            const int mt = meta[e];
+            const int ch = mt & 0xFF, j0 = (mt >> 8) & 0xFF, c0 = mt >> 16;
+            float acc = 0.f;
+            for (int a = 0; a < np; ++a) {
+                const float* sl = sm + a * slab + ch;
+                int c = c0;
+                for (int j = j0; j < k && c >= 0; j += s, --c)
+                    if (c < m) acc += sl[c * kd + j * d];
+            }
+            out[e] = acc;
+        }
+    }
+}
+
 __global__ void pad_rows_kernel(const float* __restrict__ src, int64_t rows, int64_t cols, int64_t lds,
                                 float* __restrict__ dst, int64_t ldd) {
     const int64_t total = rows * ldd;
@@ -287,6 +410,21 @@ cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, floa
     PhaseScope ps(kPhaseLower, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + nrows * ld));
     const bool vec = (g.d % 4 == 0) && (ld % 4 == 0) &&
                      (reinterpret_cast<uintptr_t>(x) % 16 == 0) && (reinterpret_cast<uintptr_t>(dhat) % 16 == 0);
+    // small-channel Type 1 (e.g. conv1, d = 3): shared-memory staged rows
+    const size_t smem1 = size_t(g.k * (g.n + 2 * g.p) * g.d) * 4 + size_t(cols) * 4 + size_t((g.n + 2 * g.p) * g.d) * 4;
+    if (type == 1 && !vec && ld % 4 == 0 && reinterpret_cast<uintptr_t>(dhat) % 16 == 0 && smem1 <= 96 * 1024 &&
+        rm.ny == g.m && rm.nc == g.m) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(lower_t1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            attr = true;
+        }
+        const int64_t nqr = g.b * g.m;
+        const int grid1 = int(std::min<int64_t>(nqr, int64_t(num_sms()) * 4));
+        lower_t1_smem_kernel<<<grid1, 512, smem1, st>>>(x, dhat, g, rm, ld, int(cols));
+        note_launch();
+        return cudaGetLastError();
+    }
     const int grid = grid_for(nrows * 32, kThreads);
     if (vec) lower_kernel<true><<<grid, kThreads, 0, st>>>(x, dhat, g, type, rm, ld, int(cols), nrows);
     else lower_kernel<false><<<grid, kThreads, 0, st>>>(x, dhat, g, type, rm, ld, int(cols), nrows);
@@ -331,6 +469,19 @@ cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* d
     PhaseScope ps(kPhaseCol2im, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + g.b * rmi.rpi * lowered_cols(g, type)));
     const bool vec = g.d % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(dd) % 16 == 0) &&
                      (reinterpret_cast<uintptr_t>(dx) % 16 == 0);
+    const size_t slab = size_t(g.m * g.k * g.d);
+    const size_t smem1 = (size_t((g.k + g.s - 1) / g.s) * slab + slab + size_t(g.n * g.d)) * 4;
+    if (type == 1 && !vec && g.d < 256 && g.s < 256 && smem1 <= 96 * 1024) {
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(col2im_t1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            attr = true;
+        }
+        const int grid1 = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * 4));
+        col2im_t1_smem_kernel<<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
+        note_launch();
+        return cudaGetLastError();
+    }
     if (vec) col2im_kernel<4><<<grid, kThreads, 0, st>>>(dd, ld, dx, g, type);
     else col2im_kernel<1><<<grid, kThreads, 0, st>>>(dd, ld, dx, g, type);
     note_launch();
