@@ -154,6 +154,16 @@ CCT_API cct_status cct_gemm_passes(int64_t M, int64_t N, int64_t K, const float*
                            const float* B, int64_t ldb, float* C, int64_t ldc, int passes,
                            void* stream);
 
+/* The reference's ORACLE entry points on the device (not the hot path):
+ * direct_convolve (tensor.cpp:77-106) and multiply_reference (gemm.cpp:124-141)
+ * with their exact arithmetic -- fp64 accumulator in the reference loop order,
+ * explicitly rounded multiply and add -- so results are bit-identical to the
+ * reference.  The conv variant accepts stride / pad like the oracle. */
+CCT_API cct_status cct_direct_conv_fwd_exact(const cct_conv_desc* desc, const float* x, const float* w, float* y,
+                                             void* stream);
+CCT_API cct_status cct_gemm_exact(int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+                                  int64_t ldb, float* C, int64_t ldc, void* stream);
+
 /* Diagnostic: one raw kernel launch with explicit operand storage.
  * a_major/b_major: 0 = K-major (rows = M|N, cols = K), 1 = MN-major (rows = K).
  * C(m, n) at C + m*ldc_m + n*ldc_n.  bn = 0 chooses the tile width. */
