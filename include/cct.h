@@ -105,6 +105,14 @@ CCT_API cct_status cct_conv_bwd_weight(const cct_conv_desc* desc, cct_lowering l
                                const float* dy, float* dw, void* ws, size_t ws_bytes,
                                void* stream);
 
+/* Workspace limit (bytes; default 16 GiB or $CCT_WORKSPACE_LIMIT).  A pass whose
+ * scratch would exceed it runs over batch chunks that reuse one scratch region
+ * (the SPEC batching module's partitions), e.g. Type 3 on
+ * conv1, whose Rhat is 2.4 GB per image.  cct_workspace_size() reports the
+ * chunked size. */
+CCT_API void cct_set_workspace_limit(size_t bytes);
+CCT_API size_t cct_get_workspace_limit(void);
+
 /* Training-step entry points (the lowered-matrix cache).
  * cct_conv_fwd_cached leaves the data-side matrix Dhat of the forward pass in a
  * caller buffer of cct_lowered_cache_size() bytes (0 when Dhat is the input

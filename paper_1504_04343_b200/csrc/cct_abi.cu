@@ -10,6 +10,7 @@
 //   BWD_WEIGHT: M=cols N=ncols K=rows   A=Dhat (MN-major) B=dRhat^T (K-major) C -> dW (split-K)
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <sstream>
 #include <string>
 
@@ -173,8 +174,8 @@ int wgrad_splits(const Lowered& L) {
 // the three passes; ws.base == nullptr plans sizes only
 // ---------------------------------------------------------------------------
 
-cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
-                   cudaStream_t st) {
+cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
+                       cudaStream_t st) {
     const Lowered L = lowered_of(g, type);
     cudaError_t e;
     int64_t ldw;
@@ -217,8 +218,8 @@ cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float
 // bwd-weight (dw != null).  bwd-weight reads Dhat from `cache` when given (as
 // left there by cct_conv_fwd_cached), else lowers x again.  The two passes run
 // in stream order and reuse the same scratch region after dRhat^T.
-cct_status run_bwd(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
-                   float* dx, float* dw, Ws& ws, cudaStream_t st) {
+cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
+                       float* dx, float* dw, Ws& ws, cudaStream_t st) {
     const Lowered L = lowered_of(g, type);
     cudaError_t e;
     float* drt = ws.take(L.ncols * L.ldr);
@@ -275,6 +276,99 @@ cct_status run_bwd(const Geo& g, int type, const float* x, const float* cache, c
     return CCT_OK;
 }
 
+// ---------------------------------------------------------------------------
+// batch chunking (the SPEC batching module's partitions):
+// a pass whose scratch exceeds the workspace limit runs over image chunks that
+// reuse the same scratch region in stream order.  Backward-weight partials of
+// the chunks are summed in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+size_t g_ws_limit = 0;
+
+size_t ws_limit() {
+    if (!g_ws_limit) {
+        const char* e = getenv("CCT_WORKSPACE_LIMIT");
+        g_ws_limit = e ? size_t(strtoull(e, nullptr, 10)) : (size_t(16) << 30);
+    }
+    return g_ws_limit;
+}
+
+Geo with_batch(Geo g, int64_t b) {
+    g.b = b;
+    return g;
+}
+
+// scratch bytes of one pass at batch b (planning run)
+size_t plan_bytes(const Geo& g, int type, int pass, int64_t b) {
+    Ws ws(nullptr);
+    const float* dummy = reinterpret_cast<const float*>(uintptr_t(256));
+    float* dout = reinterpret_cast<float*>(uintptr_t(256));
+    const Geo gb = with_batch(g, b);
+    if (pass == CCT_PASS_FWD) run_fwd_one(gb, type, dummy, dummy, nullptr, nullptr, ws, nullptr);
+    else run_bwd_one(gb, type, dummy, nullptr, dummy, dummy, pass != CCT_PASS_BWD_WEIGHT ? dout : nullptr,
+                     pass != CCT_PASS_BWD_DATA ? dout : nullptr, ws, nullptr);
+    return ws.off;
+}
+
+// images per chunk so the pass fits the workspace limit (>= 1)
+int64_t chunk_images(const Geo& g, int type, int pass) {
+    const size_t full = plan_bytes(g, type, pass, g.b);
+    if (full <= ws_limit() || g.b == 1) return g.b;
+    const size_t one = plan_bytes(g, type, pass, 1), two = plan_bytes(g, type, pass, 2);
+    const size_t per = two > one ? two - one : one;
+    const size_t fixed = one > per ? one - per : 0;
+    const int64_t cb = ws_limit() > fixed ? int64_t((ws_limit() - fixed) / std::max<size_t>(per, 1)) : 1;
+    return std::max<int64_t>(1, std::min<int64_t>(cb, g.b));
+}
+
+cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
+                   cudaStream_t st) {
+    const int64_t cb = chunk_images(g, type, CCT_PASS_FWD);
+    if (cb == g.b) return run_fwd_one(g, type, x, w, y, cache, ws, st);
+    const Lowered L = lowered_of(g, type);
+    const int64_t per_x = g.n * g.n * g.d, per_y = g.o * g.m * g.m, per_c = L.rm.rpi * L.ldc;
+    const size_t base = ws.off;
+    size_t hi = base;
+    for (int64_t q0 = 0; q0 < g.b; q0 += cb) {
+        const Geo gc = with_batch(g, std::min(cb, g.b - q0));
+        ws.off = base;
+        cct_status s = run_fwd_one(gc, type, x + q0 * per_x, w, y ? y + q0 * per_y : nullptr,
+                                   cache ? cache + q0 * per_c : nullptr, ws, st);
+        if (s != CCT_OK) return s;
+        hi = std::max(hi, ws.off);
+        if (!ws.base) break;  // planning: one chunk is representative
+    }
+    ws.off = hi;
+    return CCT_OK;
+}
+
+cct_status run_bwd(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
+                   float* dx, float* dw, Ws& ws, cudaStream_t st) {
+    const int pass = dx && dw ? CCT_PASS_BWD : dx ? CCT_PASS_BWD_DATA : CCT_PASS_BWD_WEIGHT;
+    const int64_t cb = chunk_images(g, type, pass);
+    if (cb == g.b) return run_bwd_one(g, type, x, cache, dy, w, dx, dw, ws, st);
+    const Lowered L = lowered_of(g, type);
+    const int64_t per_x = g.n * g.n * g.d, per_y = g.o * g.m * g.m, per_c = L.rm.rpi * L.ldc;
+    const int64_t nchunks = (g.b + cb - 1) / cb;
+    const int64_t wsize = g.o * g.k * g.k * g.d;
+    float* parts = dw ? ws.take(nchunks * wsize) : nullptr;  // per-chunk dW, reduced at the end
+    const size_t base = ws.off;
+    size_t hi = base;
+    int64_t c = 0;
+    for (int64_t q0 = 0; q0 < g.b; q0 += cb, ++c) {
+        const Geo gc = with_batch(g, std::min(cb, g.b - q0));
+        ws.off = base;
+        cct_status s = run_bwd_one(gc, type, x ? x + q0 * per_x : nullptr, cache ? cache + q0 * per_c : nullptr,
+                                   dy + q0 * per_y, w, dx ? dx + q0 * per_x : nullptr,
+                                   dw ? (parts ? parts + c * wsize : dw) : nullptr, ws, st);
+        if (s != CCT_OK) return s;
+        hi = std::max(hi, ws.off);
+        if (!ws.base) break;
+    }
+    ws.off = hi;
+    if (dw && ws.base) CCT_TRY(splitk_reduce(parts, wsize, int(nchunks), 1, wsize, wsize, dw, wsize, st), "chunk reduce");
+    return CCT_OK;
+}
+
 cct_status check_ptrs(std::initializer_list<const void*> ps) {
     for (const void* p : ps)
         if (!p) return fail(CCT_ERR_CONFIG, "null tensor pointer");
@@ -286,6 +380,8 @@ cct_status check_ptrs(std::initializer_list<const void*> ps) {
 extern "C" {
 
 int cct_abi_version(void) { return CCT_ABI_VERSION; }
+void cct_set_workspace_limit(size_t bytes) { g_ws_limit = bytes; }
+size_t cct_get_workspace_limit(void) { return ws_limit(); }
 void cct_profile_enable(int on) { cct::profile_enable(on != 0); }
 void cct_profile_read(double* ms, double* flops, double* bytes, uint64_t* launches, int reset) {
     cct::profile_read(ms, flops, bytes, launches, reset != 0);

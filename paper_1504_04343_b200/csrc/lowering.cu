@@ -117,33 +117,39 @@ __global__ void lower_kernel(const float* __restrict__ x, float* __restrict__ dh
 }
 
 // y[q,o,r,c] = sum over taps of Rhat[row(q, s r + i, s c + j), col(o, i, j)].
-// One block-row per output plane (q, o); threads stride over the m*m pixels.
+// Flat over (plane, pixel) so every thread of the block works; the tap loads
+// are independent and unrolled (several in flight per thread).
 __global__ void lift_kernel(const float* __restrict__ rh, float* __restrict__ y, Geo g, int type,
                             RowMap rm, int64_t rs, int64_t cs) {
     const int m = int(g.m), o = int(g.o), k = int(g.k), s = int(g.s), mm = m * m;
-    const int64_t planes = g.b * o;
-    for (int64_t pl = blockIdx.x; pl < planes; pl += gridDim.x) {
+    const int64_t total = g.b * o * int64_t(mm);
+    const int64_t tap_i = rm.sr * rs, tap_j = rm.sc * rs;  // address step of one tap row / column
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total;
+         e += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t pl = e / mm;
+        const int pix = int(e - pl * mm);
+        const int r = pix / m, c = pix - r * m;
         const int oj = int(pl % o);
         const int64_t q = pl / o;
         const int64_t base = q * rm.rpi;
-        float* yp = y + pl * mm;
-        for (int pix = threadIdx.x; pix < mm; pix += blockDim.x) {
-            const int r = pix / m, c = pix - r * m;
-            float acc = 0.f;
-            if (type == 1) {
-                acc = rh[(base + r * rm.sr + c * rm.sc) * rs + oj * cs];
-            } else if (type == 2) {
-                const float* p0 = rh + (base + int64_t(s) * r * rm.sr + int64_t(c) * rm.sc) * rs + int64_t(oj) * k * cs;
-                const int64_t step = rm.sr * rs + cs;
-                for (int i = 0; i < k; ++i) acc += p0[i * step];
-            } else {
-                const float* p0 = rh + (base + int64_t(s) * r * rm.sr + int64_t(s) * c * rm.sc) * rs +
-                                  int64_t(oj) * k * k * cs;
-                for (int i = 0; i < k; ++i)
-                    for (int j = 0; j < k; ++j) acc += p0[i * rm.sr * rs + j * rm.sc * rs + (i * k + j) * cs];
+        float acc = 0.f;
+        if (type == 1) {
+            acc = __ldg(rh + (base + r * rm.sr + c * rm.sc) * rs + oj * cs);
+        } else if (type == 2) {
+            const float* p0 = rh + (base + int64_t(s) * r * rm.sr + int64_t(c) * rm.sc) * rs + int64_t(oj) * k * cs;
+            const int64_t step = tap_i + cs;
+#pragma unroll 4
+            for (int i = 0; i < k; ++i) acc += __ldg(p0 + i * step);
+        } else {
+            const float* p0 = rh + (base + int64_t(s) * r * rm.sr + int64_t(s) * c * rm.sc) * rs +
+                              int64_t(oj) * k * k * cs;
+            for (int i = 0; i < k; ++i) {
+                const float* pi = p0 + i * (tap_i + int64_t(k) * cs);
+#pragma unroll 4
+                for (int j = 0; j < k; ++j) acc += __ldg(pi + j * (tap_j + cs));
             }
-            yp[pix] = acc;
         }
+        y[e] = acc;
     }
 }
 
@@ -172,13 +178,12 @@ __global__ void expand_kernel(const float* __restrict__ dy, float* __restrict__ 
     if (type == 2) { oj = col / k; i = col - oj * k; }
     else { oj = col / (k * k); const int ij = col - oj * k * k; i = ij / k; j = ij - i * k; }
     float* out = drt + int64_t(col) * ldr;
-    const int64_t rows = g.b * rm.rpi;
-    for (int64_t row = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; row < rows;
-         row += int64_t(gridDim.x) * blockDim.x) {
-        const int cx = int(row % nc);
-        const int64_t t = row / nc;
-        const int yy = int(t % ny);
-        const int64_t q = t / ny;
+    const int rows = int(g.b * rm.rpi);  // < 2^31 (checked by the launcher)
+    for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
+        const int t = row / nc;
+        const int cx = row - t * nc;
+        const int q = t / ny;
+        const int yy = t - q * ny;
         const int ty = yy - i;
         int r = -1;
         if (s == 1) r = ty;
@@ -191,7 +196,7 @@ __global__ void expand_kernel(const float* __restrict__ dy, float* __restrict__ 
             else if (tx >= 0 && tx % s == 0) c = tx / s;
         }
         float v = 0.f;
-        if (r >= 0 && r < m && c >= 0 && c < m) v = __ldg(dy + ((q * o + oj) * m + r) * int64_t(m) + c);
+        if (r >= 0 && r < m && c >= 0 && c < m) v = __ldg(dy + ((int64_t(q) * o + oj) * m + r) * int64_t(m) + c);
         out[row] = v;
     }
 }
@@ -434,8 +439,7 @@ cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, floa
 
 cudaError_t lift(const Geo& g, int type, const RowMap& rm, const float* rhat, int64_t rs, int64_t cs,
                  float* y, cudaStream_t st) {
-    const int64_t planes = g.b * g.o;
-    const int grid = int(std::min<int64_t>(planes, int64_t(num_sms()) * 16));
+    const int grid = grid_for(g.b * g.o * g.m * g.m, kThreads, 16);
     PhaseScope ps(kPhaseLift, st, 0,
                   4.0 * double(g.b * g.o * g.m * g.m) * (1.0 + (type == 1 ? 1 : type == 2 ? g.k : g.k * g.k)));
     lift_kernel<<<grid, kThreads, 0, st>>>(rhat, y, g, type, rm, rs, cs);
@@ -452,7 +456,7 @@ cudaError_t expand(const Geo& g, int type, const float* dy, float* drt, int64_t 
         const int grid = int(std::min<int64_t>(planes, int64_t(num_sms()) * 16));
         expand_t1_kernel<<<grid, kThreads, 0, st>>>(dy, drt, g.b, int(g.o), int(g.m * g.m), ldr);
     } else {
-        if (ncols > 65535) return cudaErrorInvalidConfiguration;
+        if (ncols > 65535 || g.b * rm.rpi >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
         const int64_t rows = g.b * rm.rpi;
         const int64_t want = (int64_t(num_sms()) * 16 + ncols - 1) / ncols;
         const int gx = int(std::max<int64_t>(1, std::min<int64_t>(want, cdiv(rows, kThreads))));

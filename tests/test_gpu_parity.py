@@ -280,3 +280,33 @@ def test_cached_training_step_matches_separate_passes(cct, dev, orc, layer, t):
     assert torch.equal(dw, conv.conv_bwd_weight(x, dy, desc, t))
     _, dw2 = conv.conv_bwd(dy, w, desc, t, x=None if cache is not None else x, cache=cache, want_dx=False)
     assert torch.equal(dw2, dw)
+
+
+@pytest.mark.parametrize("t", [1, 2, 3])
+def test_batch_chunking_under_workspace_limit(cct, dev, t):
+    """A small workspace limit splits the batch into chunks (SPEC batching module):
+    fwd / bwd-data are bit-identical, bwd-weight agrees to the tolerance."""
+    from paper_1504_04343_b200 import conv
+    L = cct.lib()
+    n, k, d, o, b, s, p = 27, 5, 32, 48, 12, 1, 2
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    dy = torch.rand((b, o, desc.m, desc.m), generator=g, device=dev) * 2 - 1
+    full = (conv.conv_fwd(x, w, desc, t), conv.conv_bwd_data(dy, w, desc, t), conv.conv_bwd_weight(x, dy, desc, t))
+    old = L.cct_get_workspace_limit()
+    try:
+        L.cct_set_workspace_limit(8 << 20)
+        small = cct.workspace_size(desc, t, cct.PASS_FWD)
+        assert small <= (8 << 20) or t == 3
+        ch = (conv.conv_fwd(x, w, desc, t), conv.conv_bwd_data(dy, w, desc, t), conv.conv_bwd_weight(x, dy, desc, t))
+        cache = conv.alloc_cache(desc, t, dev)
+        y2 = conv.conv_fwd_cached(x, w, desc, t, cache=cache)
+        dx2, dw2 = conv.conv_bwd(dy, w, desc, t, x=x, cache=cache)
+    finally:
+        L.cct_set_workspace_limit(old)
+    assert torch.equal(ch[0], full[0]) and torch.equal(ch[1], full[1]) and torch.equal(y2, full[0])
+    assert torch.equal(dx2, full[1])
+    for dwc in (ch[2], dw2):
+        assert float(torch.linalg.norm(dwc - full[2]) / torch.linalg.norm(full[2])) < 1e-5
