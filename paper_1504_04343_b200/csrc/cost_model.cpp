@@ -35,8 +35,42 @@ G geo(const cct_conv_desc* d) {
 
 double rup(double v, double q) { return std::ceil(v / q) * q; }
 
-// GEMM time of the tcgen05 kernel: 128 x BN tiles (BN chosen like the kernel),
-// 16-wide k-blocks, persistent over 148 SMs.
+// Measured 3xTF32 GEMM rate (TF/s) of gemm3xtf32_kernel on B200 by tile width
+// BN (rows) and reduction length K (cols): tools/gemm_bench.py --rate-table,
+// M = 65536, profiles/r01/gemm_rate_table.json.  Longer K is chain-split at 4096.
+const double kBN[5] = {64, 96, 128, 192, 256};
+const double kK[4] = {64, 256, 1024, 4096};
+const double kRate[5][4] = {
+    {31.7, 56.0, 72.7, 79.3},     // BN 64
+    {46.4, 83.9, 106.7, 116.7},   // BN 96
+    {60.2, 109.4, 142.2, 156.0},  // BN 128
+    {80.6, 152.4, 206.1, 223.3},  // BN 192
+    {90.3, 189.8, 251.9, 264.7},  // BN 256
+};
+const double kRateRef = 264.7e12;  // table entry the calibration's gemm_flops_per_s scales
+
+double interp_rate(double bn, double k) {
+    auto pos = [](const double* xs, int n, double v, int* i0, double* f) {
+        v = std::log(std::max(xs[0], std::min(xs[n - 1], v)));
+        for (int i = 0; i < n - 1; ++i)
+            if (v <= std::log(xs[i + 1])) {
+                *i0 = i;
+                *f = (v - std::log(xs[i])) / (std::log(xs[i + 1]) - std::log(xs[i]));
+                return;
+            }
+        *i0 = n - 2;
+        *f = 1.0;
+    };
+    int ib, ik;
+    double fb, fk;
+    pos(kBN, 5, bn, &ib, &fb);
+    pos(kK, 4, k, &ik, &fk);
+    const double r0 = kRate[ib][ik] * (1 - fk) + kRate[ib][ik + 1] * fk;
+    const double r1 = kRate[ib + 1][ik] * (1 - fk) + kRate[ib + 1][ik + 1] * fk;
+    return (r0 * (1 - fb) + r1 * fb) * 1e12;
+}
+
+// GEMM time: padded flops / measured rate for the tile width the kernel picks.
 double gemm_seconds(double M, double N, double K, const cct_calibration* c) {
     static const double cands[] = {256, 192, 128, 96, 64};
     double bn = 256, best = 1e300;
@@ -44,13 +78,8 @@ double gemm_seconds(double M, double N, double K, const cct_calibration* c) {
         const double pad = rup(N, x);
         if (pad < best) { best = pad; bn = x; }
     }
-    const double tiles = std::ceil(M / 128) * std::ceil(N / bn);
-    const double sms = 148;
-    double waves = std::ceil(tiles / sms);
-    // split-K covers the few-tile case (backward-weight); model it as perfect fill
-    if (tiles < sms) waves = tiles / sms;
-    const double eff_flops = 2.0 * (waves * sms / std::max(tiles, 1.0)) * rup(M, 128) * rup(N, bn) * rup(K, 16);
-    return eff_flops / c->gemm_flops_per_s;
+    const double rate = interp_rate(bn, std::min(K, 4096.0)) * (c->gemm_flops_per_s / kRateRef);
+    return 2.0 * rup(M, 128) * rup(N, bn) * K / rate;
 }
 
 // counts + model for one pass.  pass: 0 fwd, 1 bwd-data, 2 bwd-weight
@@ -64,7 +93,11 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     const double dhat = rows * rup(cols, 4) * f, rhat = rows * ncols * f;
     const bool t3_zero_copy = (type == 3 && g.p == 0 && g.R == g.n && std::fmod(g.d, 4) == 0);
     double t = 0, by = 0, launches = 0;
+    // measured class rates (sweep, profiles/r01): lift and expand gather, so they
+    // run below the copy-like lower / col2im kernels
+    const double lift_bw = c->hbm_bytes_per_s * 0.55, expand_bw = c->hbm_bytes_per_s * 0.40;
     auto hbm = [&](double b) { by += b; t += b / c->hbm_bytes_per_s; launches += 1; };
+    auto hbm_at = [&](double b, double bw) { by += b; t += b / bw; launches += 1; };
     if (pass == 0) {
         if (!t3_zero_copy) hbm(xin + dhat);                // lower
         const double gt = gemm_seconds(rows, ncols, cols, c);
@@ -72,23 +105,42 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         t += std::max(gt, gb / c->hbm_bytes_per_s);        // GEMM (A streamed once)
         by += gb;
         launches += 1;
-        if (type != 1) hbm(rhat + yout);                   // lift
+        if (type != 1) hbm_at(rhat + yout, lift_bw);       // lift
     } else if (pass == 1) {
-        hbm(yout + rhat);                                  // expand (T1: permute)
+        hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand
         const double gt = gemm_seconds(cols, rows, ncols, c);
         const double gb = rhat + dhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
         launches += 1;
         if (!t3_zero_copy) hbm(dhat + xin);                // col2im / crop
-    } else {
+    } else if (pass == 2) {
         if (!t3_zero_copy) hbm(xin + dhat);                // lower
-        hbm(yout + rhat);                                  // expand
+        hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand
         const double gt = gemm_seconds(cols, ncols, rows, c);
         const double gb = dhat + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
         launches += 2;                                     // GEMM + split-K reduce
+    } else {
+        // training step (cct_conv_fwd_cached + cct_conv_bwd): one lowering, one expand
+        if (!t3_zero_copy) hbm(xin + dhat);                // lower (fwd, cached)
+        double gt = gemm_seconds(rows, ncols, cols, c);
+        double gb = dhat + (type == 1 ? yout : rhat);
+        t += std::max(gt, gb / c->hbm_bytes_per_s);
+        by += gb;
+        if (type != 1) hbm_at(rhat + yout, lift_bw);       // lift
+        hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand (shared)
+        gt = gemm_seconds(cols, rows, ncols, c);           // bwd-data GEMM
+        gb = rhat + dhat;
+        t += std::max(gt, gb / c->hbm_bytes_per_s);
+        by += gb;
+        if (!t3_zero_copy) hbm(dhat + xin);                // col2im / crop
+        gt = gemm_seconds(cols, ncols, rows, c);           // bwd-weight GEMM (Dhat from the cache)
+        gb = dhat + rhat;
+        t += std::max(gt, gb / c->hbm_bytes_per_s);
+        by += gb;
+        launches += 4;                                     // 3 GEMMs + split-K reduce
     }
     *secs = t + launches * c->launch_s;
     *bytes = by;
@@ -102,9 +154,9 @@ extern "C" {
 // sustained lowering-kernel copy rate and sustained 3xTF32 algorithmic GEMM rate.
 void cct_calibration_default(cct_calibration* cal) {
     if (!cal) return;
-    cal->hbm_bytes_per_s = 5.5e12;
-    cal->gemm_flops_per_s = 1.6e14;
-    cal->launch_s = 4e-6;
+    cal->hbm_bytes_per_s = 4.5e12;   // measured lower / col2im rate (sweep, profiles/r01)
+    cal->gemm_flops_per_s = 2.647e14; // measured 3xTF32 rate at BN 256, K 4096 (rate table)
+    cal->launch_s = 5e-6;
     cal->alpha = 4.0 / cal->hbm_bytes_per_s * 2.0;  // one element read + written
     cal->beta = 1.0 / cal->gemm_flops_per_s;
 }
@@ -136,13 +188,8 @@ cct_status cct_estimate(const cct_conv_desc* desc, cct_lowering lowering, const 
     double secs = 0, bytes = 0;
     if (pass >= 0 && pass <= 2) {
         one_pass(g, type, pass, cal, &secs, &bytes);
-    } else {  // fwd + bwd-data + bwd-weight
-        for (int p = 0; p < 3; ++p) {
-            double s_, b_;
-            one_pass(g, type, p, cal, &s_, &b_);
-            secs += s_;
-            bytes += b_;
-        }
+    } else {  // training step: fwd (Dhat cached) + bwd-data + bwd-weight sharing one expand
+        one_pass(g, type, 3, cal, &secs, &bytes);
     }
     est->model_seconds = secs;
     est->hbm_bytes = uint64_t(bytes);

@@ -154,21 +154,37 @@ __global__ void lift_kernel(const float* __restrict__ rh, float* __restrict__ y,
 }
 
 // T1 expand: dRhat1^T[o][q*m^2 + pix] = dy[q][o][pix] -- a permutation of the
-// (q, o) planes.  blockIdx.x strides over planes, threads over the m^2 pixels.
+// (q, o) planes.  Thread per source element (coalesced reads); the writes are
+// contiguous runs of m^2 floats.  Four independent elements per thread.
 __global__ void expand_t1_kernel(const float* __restrict__ dy, float* __restrict__ drt, int64_t b, int o,
                                  int mm, int64_t ldr) {
-    const int64_t planes = b * o;
-    for (int64_t pl = blockIdx.x; pl < planes; pl += gridDim.x) {
-        const int oj = int(pl % o);
-        const int64_t q = pl / o;
-        const float* src = dy + pl * mm;
-        float* dst = drt + int64_t(oj) * ldr + q * mm;
-        for (int i = threadIdx.x; i < mm; i += blockDim.x) dst[i] = __ldg(src + i);
+    const int64_t total = b * o * int64_t(mm);
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t e0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e0 < total; e0 += 4 * stride) {
+        float v[4];
+        int64_t dst[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int64_t e = e0 + u * stride;
+            dst[u] = -1;
+            if (e < total) {
+                const int64_t pl = e / mm;
+                const int pix = int(e - pl * mm);
+                const int oj = int(pl % o);
+                const int64_t q = pl / o;
+                v[u] = __ldg(dy + e);
+                dst[u] = int64_t(oj) * ldr + q * mm + pix;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            if (dst[u] >= 0) drt[dst[u]] = v[u];
     }
 }
 
 // T2/T3 expand: dRhat^T[col][row] (internal row order), zeros where lift does
-// not read.  blockIdx.y = column (o, i[, j]); threads stride over the rows.
+// not read.  blockIdx.y = column (o, i[, j]); each thread writes 4 consecutive
+// rows as one float4, walking (q, y, x) incrementally (one division per 4 rows).
 __global__ void expand_kernel(const float* __restrict__ dy, float* __restrict__ drt, Geo g, int type,
                               RowMap rm, int64_t ldr) {
     const int m = int(g.m), o = int(g.o), k = int(g.k), s = int(g.s);
@@ -177,27 +193,41 @@ __global__ void expand_kernel(const float* __restrict__ dy, float* __restrict__ 
     int oj, i, j = 0;
     if (type == 2) { oj = col / k; i = col - oj * k; }
     else { oj = col / (k * k); const int ij = col - oj * k * k; i = ij / k; j = ij - i * k; }
-    float* out = drt + int64_t(col) * ldr;
+    float4* out = reinterpret_cast<float4*>(drt + int64_t(col) * ldr);
     const int rows = int(g.b * rm.rpi);  // < 2^31 (checked by the launcher)
-    for (int row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
-        const int t = row / nc;
-        const int cx = row - t * nc;
-        const int q = t / ny;
-        const int yy = t - q * ny;
-        const int ty = yy - i;
-        int r = -1;
-        if (s == 1) r = ty;
-        else if (ty >= 0 && ty % s == 0) r = ty / s;
-        int c = cx;
-        if (type == 3) {
-            const int tx = cx - j;
-            c = -1;
-            if (s == 1) c = tx;
-            else if (tx >= 0 && tx % s == 0) c = tx / s;
+    const int rows4 = int(ldr / 4);
+    for (int r4 = blockIdx.x * blockDim.x + threadIdx.x; r4 < rows4; r4 += gridDim.x * blockDim.x) {
+        int row = 4 * r4;
+        int t = row / nc;
+        int cx = row - t * nc;
+        int q = t / ny;
+        int yy = t - q * ny;
+        float v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            float val = 0.f;
+            if (row + u < rows) {
+                const int ty = yy - i;
+                int r = -1;
+                if (s == 1) r = ty;
+                else if (ty >= 0 && ty % s == 0) r = ty / s;
+                int c = cx;
+                if (type == 3) {
+                    const int tx = cx - j;
+                    c = -1;
+                    if (s == 1) c = tx;
+                    else if (tx >= 0 && tx % s == 0) c = tx / s;
+                }
+                if (r >= 0 && r < m && c >= 0 && c < m)
+                    val = __ldg(dy + ((int64_t(q) * o + oj) * m + r) * int64_t(m) + c);
+            }
+            v[u] = val;
+            if (++cx == nc) {  // walk to the next row of the (q, y) grid
+                cx = 0;
+                if (++yy == ny) { yy = 0; ++q; }
+            }
         }
-        float v = 0.f;
-        if (r >= 0 && r < m && c >= 0 && c < m) v = __ldg(dy + ((int64_t(q) * o + oj) * m + r) * int64_t(m) + c);
-        out[row] = v;
+        out[r4] = make_float4(v[0], v[1], v[2], v[3]);
     }
 }
 
@@ -452,14 +482,13 @@ cudaError_t expand(const Geo& g, int type, const float* dy, float* drt, int64_t 
     const int64_t ncols = lowered_ncols(g, type);
     PhaseScope ps(kPhaseExpand, st, 0, 4.0 * double(g.b * g.o * g.m * g.m + ncols * g.b * rm.rpi));
     if (type == 1) {
-        const int64_t planes = g.b * g.o;
-        const int grid = int(std::min<int64_t>(planes, int64_t(num_sms()) * 16));
+        const int grid = grid_for(g.b * g.o * g.m * g.m / 4 + 1, kThreads, 16);
         expand_t1_kernel<<<grid, kThreads, 0, st>>>(dy, drt, g.b, int(g.o), int(g.m * g.m), ldr);
     } else {
         if (ncols > 65535 || g.b * rm.rpi >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;
-        const int64_t rows = g.b * rm.rpi;
-        const int64_t want = (int64_t(num_sms()) * 16 + ncols - 1) / ncols;
-        const int gx = int(std::max<int64_t>(1, std::min<int64_t>(want, cdiv(rows, kThreads))));
+        if (ldr % 4 || reinterpret_cast<uintptr_t>(drt) % 16) return cudaErrorInvalidValue;
+        const int64_t want = (int64_t(num_sms()) * 32 + ncols - 1) / ncols;
+        const int gx = int(std::max<int64_t>(1, std::min<int64_t>(want, cdiv(ldr / 4, kThreads))));
         expand_kernel<<<dim3(gx, unsigned(ncols)), kThreads, 0, st>>>(dy, drt, g, type, rm, ldr);
     }
     note_launch();

@@ -55,6 +55,18 @@ def run(M, N, K, amaj, bmaj, passes, bn=0, reps=10, cmaj=0):
     return ms, 2.0 * M * N * K / ms / 1e9
 
 
+def rate_table(reps=5):
+    """GEMM rate vs tile width N and reduction length K (cost-model calibration)."""
+    out = {}
+    for N in (64, 96, 128, 192, 256, 384, 1024):
+        for K in (64, 256, 1024, 4096):
+            M = 65536 if N < 1024 else 16384
+            ms, tf = run(M, N, K, 0, 0, 3, 0, reps, cmaj=1)
+            out[f"{N},{K}"] = tf
+            print(f"rate N={N:5d} K={K:5d}: {tf:6.1f} TF/s", flush=True)
+    return out
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=None)
@@ -62,7 +74,12 @@ if __name__ == "__main__":
     ap.add_argument("--bn", type=int, default=0)
     ap.add_argument("--layouts", default="kk,mm,mk,km")
     ap.add_argument("--passes", default="1,3")
+    ap.add_argument("--rate-table", action="store_true")
     a = ap.parse_args()
+    if a.rate_table:
+        import json
+        print(json.dumps(rate_table()))
+        raise SystemExit(0)
     for name, (M, N, K) in SHAPES.items():
         if a.only and a.only != name:
             continue
@@ -74,3 +91,4 @@ if __name__ == "__main__":
                 res.append(f"p{passes}: {ms:7.3f} ms {tf:6.1f} TF/s")
             print(f"{name:11s} M={M} N={N} K={K} A={'MN' if amaj else 'K '} B={'MN' if bmaj else 'K '} | "
                   + " | ".join(res), flush=True)
+
