@@ -223,11 +223,18 @@ def run_ours(a):
     world, rank, local = dist_env()
     if world != a.gpus:
         a.gpus = world if world > 1 else a.gpus
+    # CCT_BENCH_BACKEND=gloo lets several ranks share one GPU to exercise the
+    # multi-rank path where only one device is available (validation only).
+    backend = os.environ.get("CCT_BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         group = dist.group.WORLD
     L = cct.lib()
     if a.lowering == "auto":

@@ -422,7 +422,7 @@ int choose_cg(const GemmProblem& g, int bn) {
     // pairs tile M by 256: only when that adds (almost) no padding over 128-row tiles
     const int64_t pad1 = (g.M + kBM - 1) / kBM * kBM - g.M;
     const int64_t pad2 = (g.M + 2 * kBM - 1) / (2 * kBM) * (2 * kBM) - g.M;
-    return (pad2 - pad1) * 20 <= g.M ? 2 : 1;
+    return (pad2 - pad1) * 10 <= g.M ? 2 : 1;  // pairs are ~10-15% faster per useful flop
 }
 
 }  // namespace
