@@ -113,6 +113,14 @@ CCT_API cct_status cct_conv_bwd_weight(const cct_conv_desc* desc, cct_lowering l
 CCT_API void cct_set_workspace_limit(size_t bytes);
 CCT_API size_t cct_get_workspace_limit(void);
 
+/* Implicit Type 1 lowering (default on; $CCT_IMPLICIT=0 disables): for Type 1
+ * layers with d % 32 == 0 the forward and backward-weight GEMMs read their
+ * lowered operand straight from x through TMA im2col tiles -- Dhat never
+ * exists in HBM (the paper's "fusion").  Off: Dhat is
+ * materialised by the lowering kernel (bit-identical results). */
+CCT_API void cct_set_implicit_lowering(int on);
+CCT_API int cct_get_implicit_lowering(void);
+
 /* Training-step entry points (the lowered-matrix cache).
  * cct_conv_fwd_cached leaves the data-side matrix Dhat of the forward pass in a
  * caller buffer of cct_lowered_cache_size() bytes (0 when Dhat is the input

@@ -103,6 +103,9 @@ def lib() -> C.CDLL:
     L.cct_set_workspace_limit.argtypes = [C.c_size_t]
     L.cct_set_workspace_limit.restype = None
     L.cct_get_workspace_limit.restype = C.c_size_t
+    L.cct_set_implicit_lowering.argtypes = [C.c_int]
+    L.cct_set_implicit_lowering.restype = None
+    L.cct_get_implicit_lowering.restype = C.c_int
     L.cct_launch_count.restype = C.c_uint64
     L.cct_reset_launch_count.restype = None
     _lib = L

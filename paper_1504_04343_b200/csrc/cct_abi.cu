@@ -132,6 +132,30 @@ const float* weights_view(const Lowered& L, const float* w, Ws& ws, cudaStream_t
     return wp;
 }
 
+// Implicit Type 1 lowering (TMA im2col A operand) -- on by default; the
+// materialised path stays available for parity tests and small-channel layers.
+int g_implicit = -1;
+bool implicit_enabled() {
+    if (g_implicit < 0) {
+        const char* e = getenv("CCT_IMPLICIT");
+        g_implicit = e ? (atoi(e) != 0) : 1;
+    }
+    return g_implicit != 0;
+}
+
+// Type 1 with d % 32 == 0 runs forward and backward-weight on the input itself.
+bool t1_implicit(const Geo& g, int type, const float* x) {
+    return implicit_enabled() && type == 1 && im2col_ok(g.d, true) && x && aligned16(x) &&
+           g.n * g.n * g.d * g.b < (int64_t(1) << 40) && g.b * g.m * g.m < (int64_t(1) << 31);
+}
+
+Im2col im2col_of(const Geo& g, const float* x) {
+    Im2col ic;
+    ic.x = x;
+    ic.b = g.b; ic.n = g.n; ic.d = g.d; ic.k = g.k; ic.s = g.s; ic.p = g.p; ic.m = g.m;
+    return ic;
+}
+
 // True when Dhat of this type is the (unpadded, aligned) input itself.
 bool dhat_is_input(const Geo& g, int type, const float* x) {
     return type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(x);
@@ -181,7 +205,8 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
     int64_t ldw;
     const float* wv = weights_view(L, w, ws, st, &ldw, &e);
     CCT_TRY(e, "pad weights");
-    const float* dh = dhat_of(g, type, L, x, cache, ws, st, &e);
+    const bool implicit = t1_implicit(g, type, x);
+    const float* dh = implicit ? nullptr : dhat_of(g, type, L, x, cache, ws, st, &e);
     CCT_TRY(e, "lower");
     const int64_t ldd = (dh == x) ? g.d : L.ldc;
     GemmProblem gp;
@@ -190,6 +215,7 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
     gp.K = L.cols;
     gp.A = {dh, ldd, Major::K};
     gp.B = {wv, ldw, Major::K};
+    if (implicit) gp.im2col = im2col_of(g, x);
     float* rht = nullptr;
     float* out;
     int64_t span;
@@ -248,7 +274,10 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
         ws.off = mark;  // stream order: bwd-weight may reuse the bwd-data scratch
     }
     if (dw) {
-        const float* dh = (cache && !dhat_is_input(g, type, x)) ? cache : dhat_of(g, type, L, x, nullptr, ws, st, &e);
+        const bool implicit = t1_implicit(g, type, x);
+        const float* dh = implicit ? nullptr
+                          : (cache && !dhat_is_input(g, type, x)) ? cache
+                                                                  : dhat_of(g, type, L, x, nullptr, ws, st, &e);
         CCT_TRY(e, "lower");
         const int64_t ldd = (dh == x) ? g.d : L.ldc;
         const int splits = wgrad_splits(L);
@@ -261,6 +290,7 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
             gp.K = L.rows;
             gp.A = {dh, ldd, Major::MN};
             gp.B = {drt, L.ldr, Major::K};
+            if (implicit) gp.im2col = im2col_of(g, x);
             gp.C.ptr = parts;
             gp.C.s_mr = 1;
             gp.C.s_n = L.cols;
@@ -381,6 +411,8 @@ extern "C" {
 
 int cct_abi_version(void) { return CCT_ABI_VERSION; }
 void cct_set_workspace_limit(size_t bytes) { g_ws_limit = bytes; }
+void cct_set_implicit_lowering(int on) { g_implicit = on ? 1 : 0; }
+int cct_get_implicit_lowering(void) { return implicit_enabled() ? 1 : 0; }
 size_t cct_get_workspace_limit(void) { return ws_limit(); }
 void cct_profile_enable(int on) { cct::profile_enable(on != 0); }
 void cct_profile_read(double* ms, double* flops, double* bytes, uint64_t* launches, int reset) {
@@ -478,7 +510,8 @@ cct_status cct_lowered_cache_size(const cct_conv_desc* desc, cct_lowering loweri
     const int type = resolve_train(desc, lowering);
     const Lowered L = lowered_of(g, type);
     const float* aligned = reinterpret_cast<const float*>(uintptr_t(256));
-    *bytes = dhat_is_input(g, type, aligned) ? 0 : size_t(L.rows * L.ldc) * sizeof(float);
+    *bytes = (dhat_is_input(g, type, aligned) || t1_implicit(g, type, aligned)) ? 0
+                                                                             : size_t(L.rows * L.ldc) * sizeof(float);
     return CCT_OK;
 }
 

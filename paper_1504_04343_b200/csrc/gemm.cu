@@ -38,6 +38,8 @@ struct KParams {
     int passes;
     float* C;
     int64_t mdiv, s_mq, s_mr, s_n, s_split;
+    // implicit (im2col) A: layer geometry
+    int ic_d, ic_k, ic_s, ic_p, ic_m, ic_mm, ic_cpt;
 };
 
 constexpr int kThreads = 384;
@@ -89,7 +91,20 @@ __device__ __forceinline__ uint64_t tile_desc(uint32_t base, int kk) {
     }
 }
 
-template <int BN, int A_MN, int B_MN, int CG>
+// first output pixel (q, r, c) of a flat pixel index
+struct Pix {
+    int q, r, c;
+};
+__device__ __forceinline__ Pix pix_of(int idx, const KParams& p) {
+    Pix x;
+    x.q = idx / p.ic_mm;
+    const int rem = idx - x.q * p.ic_mm;
+    x.r = rem / p.ic_m;
+    x.c = rem - x.r * p.ic_m;
+    return x;
+}
+
+template <int BN, int A_MN, int B_MN, int CG, int A_IM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const KParams p) {
@@ -152,13 +167,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int n0 = nt * BN + int(rank) * BNL;
                 const int kb0 = sp * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+                Pix tile_px{};
+                if constexpr (A_IM && !A_MN) tile_px = pix_of(m0, p);  // forward: rows are pixels
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], C_::RAW_BYTES);
                     uint8_t* a_dst = smem + stage * C_::STAGE_BYTES;
                     uint8_t* b_dst = a_dst + C_::A_BYTES;
                     const int k0 = kb * kBK;
-                    if constexpr (!A_MN) {
+                    if constexpr (A_IM && !A_MN) {
+                        // implicit lowering, forward: 128 pixels x 16 channels of filter tap (ti, tj)
+                        const int tap = kb / p.ic_cpt;
+                        const int ch0 = (kb - tap * p.ic_cpt) * kBK;
+                        const int ti = tap / p.ic_k, tj = tap - ti * p.ic_k;
+                        ptx::tma_load_im2col_4d(a_dst, &tmA, &full[stage], ch0, p.ic_s * tile_px.c - p.ic_p,
+                                                p.ic_s * tile_px.r - p.ic_p, tile_px.q, uint16_t(tj), uint16_t(ti));
+                    } else if constexpr (A_IM && A_MN) {
+                        // implicit lowering, backward-weight: K rows = 16 pixels, M = (tap, ch)
+                        const Pix px = pix_of(k0, p);
+                        const int kkd = p.ic_k * p.ic_k * p.ic_d;
+#pragma unroll
+                        for (int c = 0; c < kBM / 32; ++c) {
+                            const int mcol = min(m0 + 32 * c, kkd - 32);  // rows >= M are masked later
+                            const int tap = mcol / p.ic_d;
+                            const int ch0 = mcol - tap * p.ic_d;
+                            const int ti = tap / p.ic_k, tj = tap - ti * p.ic_k;
+                            ptx::tma_load_im2col_4d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], ch0,
+                                                    p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
+                                                    uint16_t(tj), uint16_t(ti));
+                        }
+                    } else if constexpr (!A_MN) {
                         ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
                     } else {
 #pragma unroll
@@ -367,10 +405,47 @@ bool make_tmap(CUtensorMap* map, const Operand& op, int64_t mn_extent, int64_t k
     return r == CUDA_SUCCESS;
 }
 
-template <int BN, int A_MN, int B_MN, int CG>
+PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
+    static PFN_cuTensorMapEncodeIm2col_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeIm2col_v12000>(p);
+    }
+    return fn;
+}
+
+// NHWC input as a 4D (c, w, h, n) im2col map: bounding box lower corner -p,
+// upper corner p - (k - 1), traversal stride s (output pixels along W, H, N).
+bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major) {
+    auto enc = encode_im2col_fn();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {cuuint64_t(ic.d), cuuint64_t(ic.n), cuuint64_t(ic.n), cuuint64_t(ic.b)};
+    cuuint64_t strides[3] = {cuuint64_t(ic.d) * 4, cuuint64_t(ic.n * ic.d) * 4, cuuint64_t(ic.n * ic.n * ic.d) * 4};
+    int lower[2] = {int(-ic.p), int(-ic.p)};
+    int upper[2] = {int(ic.p - (ic.k - 1)), int(ic.p - (ic.k - 1))};
+    cuuint32_t estr[4] = {1, cuuint32_t(ic.s), cuuint32_t(ic.s), 1};
+    const cuuint32_t chans = mn_major ? 32 : kBK;
+    const cuuint32_t pixels = mn_major ? kBK : kBM;
+    CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(ic.x), dims, strides, lower, upper,
+                     chans, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_64B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return false;
+    // Older drivers mis-handle im2col maps of tensors < 128 KiB unless bit 21 of
+    // the second descriptor word is cleared (same workaround as CUTLASS).
+    int drv = 0;
+    cudaDriverGetVersion(&drv);
+    if (drv <= 13010 && ic.b * ic.n * ic.n * ic.d * 4 < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+    return true;
+}
+
+template <int BN, int A_MN, int B_MN, int CG, int A_IM>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, cudaStream_t st) {
     using C_ = Cfg<BN, CG>;
-    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG>;
+    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
@@ -402,10 +477,15 @@ template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
-    if (!amn && !bmn) return launch<BN, 0, 0, CG>(ta, tb, kp, st);
-    if (amn && bmn) return launch<BN, 1, 1, CG>(ta, tb, kp, st);
-    if (amn && !bmn) return launch<BN, 1, 0, CG>(ta, tb, kp, st);
-    return launch<BN, 0, 1, CG>(ta, tb, kp, st);
+    if (g.im2col.x) {  // implicit Type 1: forward (K, K) and backward-weight (MN, K)
+        if (!amn && !bmn) return launch<BN, 0, 0, CG, 1>(ta, tb, kp, st);
+        if (amn && !bmn) return launch<BN, 1, 0, CG, 1>(ta, tb, kp, st);
+        return cudaErrorInvalidValue;
+    }
+    if (!amn && !bmn) return launch<BN, 0, 0, CG, 0>(ta, tb, kp, st);
+    if (amn && bmn) return launch<BN, 1, 1, CG, 0>(ta, tb, kp, st);
+    if (amn && !bmn) return launch<BN, 1, 0, CG, 0>(ta, tb, kp, st);
+    return launch<BN, 0, 1, CG, 0>(ta, tb, kp, st);
 }
 
 // CTA-pair mode needs >= 2 row tiles and, for an MN-major B, B halves that are
@@ -426,6 +506,8 @@ int choose_cg(const GemmProblem& g, int bn) {
 }
 
 }  // namespace
+
+bool im2col_ok(int64_t d, bool mn_major) { return mn_major ? d % 32 == 0 : d % kBK == 0; }
 
 int choose_bn(int64_t N) {
     static const int cands[] = {256, 192, 128, 96, 64};
@@ -482,7 +564,20 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.num_m_tiles = int((g.M + kBM * cg - 1) / (kBM * cg));
     kp.units = kp.num_m_tiles * kp.num_n_tiles * kp.splits;
     CUtensorMap ta, tb;
-    if (!make_tmap(&ta, g.A, g.M, g.K, kBM)) return cudaErrorInvalidValue;
+    if (g.im2col.x) {
+        const Im2col& ic = g.im2col;
+        kp.ic_d = int(ic.d);
+        kp.ic_k = int(ic.k);
+        kp.ic_s = int(ic.s);
+        kp.ic_p = int(ic.p);
+        kp.ic_m = int(ic.m);
+        kp.ic_mm = int(ic.m * ic.m);
+        kp.ic_cpt = int(ic.d / kBK);
+        if (!im2col_ok(ic.d, g.A.major == Major::MN)) return cudaErrorInvalidValue;
+        if (!make_tmap_im2col(&ta, ic, g.A.major == Major::MN)) return cudaErrorInvalidValue;
+    } else if (!make_tmap(&ta, g.A, g.M, g.K, kBM)) {
+        return cudaErrorInvalidValue;
+    }
     if (!make_tmap(&tb, g.B, g.N, g.K, bn / cg)) return cudaErrorInvalidValue;
     if (cg == 2) {
         switch (bn) {

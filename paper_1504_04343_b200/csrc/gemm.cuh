@@ -27,6 +27,17 @@ struct OutMap {
     int64_t s_mq = 0, s_mr = 1, s_n = 0, s_split = 0;
 };
 
+// Implicit Type 1 lowering: operand A is read straight from the NHWC input x
+// through a TMA im2col tensor map (no Dhat in HBM).  Row (or K) index = output
+// pixel (q, r, c); lowered column = (i, j, ch) with ch fastest -- the same order
+// as the materialised Dhat, so B (the KernelBank) is unchanged.
+//   A.major == K  (forward):         tile = 128 pixels x 16 channels of one tap
+//   A.major == MN (backward-weight): tile = 16 pixels x (4 x 32 channels)
+struct Im2col {
+    const float* x = nullptr;  // nullptr: A is an ordinary (materialised) matrix
+    int64_t b = 0, n = 0, d = 0, k = 0, s = 1, p = 0, m = 0;
+};
+
 struct GemmProblem {
     int64_t M = 0, N = 0, K = 0;
     Operand A, B;
@@ -34,7 +45,12 @@ struct GemmProblem {
     int splits = 1;  // split-K factor; each split writes its own slice (s_split)
     int passes = 3;  // 3 = 3xTF32 (fp32-accurate), 1 = plain TF32 (diagnostic only)
     int bn = 0;      // 0 = choose
+    Im2col im2col;   // implicit lowering of A (Type 1)
 };
+
+// Can this layer use the implicit (im2col) A operand?  fwd needs d % 16 == 0,
+// backward-weight d % 32 == 0 (one TMA box never straddles a filter tap).
+bool im2col_ok(int64_t d, bool mn_major);
 
 // Tile constants shared by the launcher and the kernel.
 constexpr int kBM = 128;

@@ -72,11 +72,23 @@ def test_lowered_shapes_match_spec(cct):
 
 
 def test_workspace_sizes(cct):
-    for t in (1, 2, 3):
-        for p in (0, 1, 2):
-            small = cct.workspace_size(cct.ConvDesc(27, 5, 96, 256, 2, 1, 2), t, p)
-            big = cct.workspace_size(cct.ConvDesc(27, 5, 96, 256, 8, 1, 2), t, p)
-            assert 0 < small < big  # footprint grows with the batch
+    L = cct.lib()
+    old = L.cct_get_implicit_lowering()
+    try:
+        for implicit in (0, 1):
+            L.cct_set_implicit_lowering(implicit)
+            for t in (1, 2, 3):
+                for p in (0, 1, 2):
+                    small = cct.workspace_size(cct.ConvDesc(27, 5, 96, 256, 2, 1, 2), t, p)
+                    big = cct.workspace_size(cct.ConvDesc(27, 5, 96, 256, 8, 1, 2), t, p)
+                    if implicit and t == 1 and p == 0:
+                        assert small == big  # implicit lowering: no Dhat, no scratch
+                    else:
+                        assert 0 < small < big  # footprint grows with the batch
+            # implicit Type 1 keeps no lowered cache
+            assert (cct.lowered_cache_size(cct.ConvDesc(27, 5, 96, 256, 8, 1, 2), 1) == 0) == bool(implicit)
+    finally:
+        L.cct_set_implicit_lowering(old)
 
 
 def test_compute_without_gpu_fails_loudly(cct):

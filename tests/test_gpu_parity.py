@@ -310,3 +310,37 @@ def test_batch_chunking_under_workspace_limit(cct, dev, t):
     assert torch.equal(dx2, full[1])
     for dwc in (ch[2], dw2):
         assert float(torch.linalg.norm(dwc - full[2]) / torch.linalg.norm(full[2])) < 1e-5
+
+
+@pytest.mark.parametrize("layer", [("conv2s", 27, 5, 96, 64, 1, 2), ("conv3", 13, 3, 256, 384, 1, 1),
+                                   ("s2p1", 15, 3, 32, 40, 2, 1), ("ragged", 14, 4, 64, 48, 3, 2)],
+                         ids=lambda l: l[0])
+def test_implicit_lowering_matches_materialised(cct, dev, orc, layer):
+    """Implicit Type 1 (TMA im2col operands, no Dhat in HBM) == materialised Type 1,
+    bit for bit (same K order, same GEMM), and both match the oracle."""
+    from paper_1504_04343_b200 import conv
+    L = cct.lib()
+    _, n, k, d, o, s, p = layer
+    b = 3
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    x_np, w_np = orc.random_problem(77, b, n, d, k, o)
+    dy_np = orc.uniform(78, b * o * desc.m * desc.m)
+    x = T(x_np, dev, b, n, n, d)
+    w = T(w_np, dev, o, k, k, d)
+    dy = T(dy_np, dev, b, o, desc.m, desc.m)
+    old = L.cct_get_implicit_lowering()
+    try:
+        L.cct_set_implicit_lowering(1)
+        assert cct.lowered_cache_size(desc, 1) == 0
+        yi, dwi = conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_weight(x, dy, desc, 1)
+        cache = conv.alloc_cache(desc, 1, dev)
+        yc = conv.conv_fwd_cached(x, w, desc, 1, cache=cache)
+        _, dwc = conv.conv_bwd(dy, w, desc, 1, x=x, cache=cache)
+        L.cct_set_implicit_lowering(0)
+        ym, dwm = conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_weight(x, dy, desc, 1)
+    finally:
+        L.cct_set_implicit_lowering(old)
+    assert torch.equal(yi, ym) and torch.equal(yc, ym)
+    assert torch.equal(dwi, dwm) and torch.equal(dwc, dwm)
+    assert rel_l2(yi.cpu().numpy().ravel(), orc.conv_fwd(x_np, w_np, b, n, d, k, o, s, p)) <= TOL
+    assert rel_l2(dwi.cpu().numpy().ravel(), orc.conv_bwd_weight(x_np, dy_np, b, n, d, k, o, s, p)) <= TOL
