@@ -201,7 +201,7 @@ int wgrad_splits(const Lowered& L) {
 cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
                        cudaStream_t st) {
     const Lowered L = lowered_of(g, type);
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     int64_t ldw;
     const float* wv = weights_view(L, w, ws, st, &ldw, &e);
     CCT_TRY(e, "pad weights");
@@ -247,7 +247,7 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
 cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
                        float* dx, float* dw, Ws& ws, cudaStream_t st) {
     const Lowered L = lowered_of(g, type);
-    cudaError_t e;
+    cudaError_t e = cudaSuccess;
     float* drt = ws.take(L.ncols * L.ldr);
     if (ws.base) CCT_TRY(expand(g, type, dy, drt, L.ldr, st), "expand");
     const size_t mark = ws.off;
