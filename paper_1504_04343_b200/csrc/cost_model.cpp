@@ -92,16 +92,20 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     const double xin = g.b * g.n * g.n * g.d * f, yout = g.b * g.o * g.m * g.m * f;
     const double dhat = rows * rup(cols, 4) * f, rhat = rows * ncols * f;
     const bool t3_zero_copy = (type == 3 && g.p == 0 && g.R == g.n && std::fmod(g.d, 4) == 0);
+    // implicit Type 1 (TMA im2col operands, d % 32 == 0): no lowering, A read from x;
+    // backward-weight through im2col measured ~10% slower than from a materialised Dhat
+    const bool t1_implicit = (type == 1 && std::fmod(g.d, 32) == 0 && cct_get_implicit_lowering());
     double t = 0, by = 0, launches = 0;
     // measured class rates (sweep, profiles/r01): lift and expand gather, so they
     // run below the copy-like lower / col2im kernels
     const double lift_bw = c->hbm_bytes_per_s * 0.55, expand_bw = c->hbm_bytes_per_s * 0.40;
     auto hbm = [&](double b) { by += b; t += b / c->hbm_bytes_per_s; launches += 1; };
     auto hbm_at = [&](double b, double bw) { by += b; t += b / bw; launches += 1; };
+    const double a_in = t1_implicit ? xin : dhat;         // bytes of the A operand stream
     if (pass == 0) {
-        if (!t3_zero_copy) hbm(xin + dhat);                // lower
+        if (!t3_zero_copy && !t1_implicit) hbm(xin + dhat); // lower
         const double gt = gemm_seconds(rows, ncols, cols, c);
-        const double gb = dhat + (type == 1 ? yout : rhat);
+        const double gb = a_in + (type == 1 ? yout : rhat);
         t += std::max(gt, gb / c->hbm_bytes_per_s);        // GEMM (A streamed once)
         by += gb;
         launches += 1;
@@ -115,18 +119,18 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         launches += 1;
         if (!t3_zero_copy) hbm(dhat + xin);                // col2im / crop
     } else if (pass == 2) {
-        if (!t3_zero_copy) hbm(xin + dhat);                // lower
+        if (!t3_zero_copy && !t1_implicit) hbm(xin + dhat); // lower
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand
-        const double gt = gemm_seconds(cols, ncols, rows, c);
-        const double gb = dhat + rhat;
+        const double gt = gemm_seconds(cols, ncols, rows, c) * (t1_implicit ? 1.1 : 1.0);
+        const double gb = a_in + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
         launches += 2;                                     // GEMM + split-K reduce
     } else {
         // training step (cct_conv_fwd_cached + cct_conv_bwd): one lowering, one expand
-        if (!t3_zero_copy) hbm(xin + dhat);                // lower (fwd, cached)
+        if (!t3_zero_copy && !t1_implicit) hbm(xin + dhat); // lower (fwd, cached)
         double gt = gemm_seconds(rows, ncols, cols, c);
-        double gb = dhat + (type == 1 ? yout : rhat);
+        double gb = a_in + (type == 1 ? yout : rhat);
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
         if (type != 1) hbm_at(rhat + yout, lift_bw);       // lift
@@ -136,8 +140,8 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
         if (!t3_zero_copy) hbm(dhat + xin);                // col2im / crop
-        gt = gemm_seconds(cols, ncols, rows, c);           // bwd-weight GEMM (Dhat from the cache)
-        gb = dhat + rhat;
+        gt = gemm_seconds(cols, ncols, rows, c) * (t1_implicit ? 1.1 : 1.0);  // bwd-weight GEMM
+        gb = a_in + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
         launches += 4;                                     // 3 GEMMs + split-K reduce

@@ -337,18 +337,13 @@ __global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restr
         }
         cp_async_wait_all();
         __syncthreads();
+        // one warp per lowered row; lane-consecutive elements: conflict-free smem
+        // gathers and 128-byte coalesced stores
         for (int c = warp; c < m; c += nwarps) {
             const int base = s * c * d;
-            float4* row = reinterpret_cast<float4*>(dh + (q * rm.rpi + int64_t(r) * rm.sr + int64_t(c) * rm.sc) * ld);
-            for (int e4 = lane; e4 < ld4; e4 += 32) {
-                const int e = 4 * e4;
-                float4 v;
-                v.x = e < cols ? tile[offs[e] + base] : 0.f;
-                v.y = e + 1 < cols ? tile[offs[e + 1] + base] : 0.f;
-                v.z = e + 2 < cols ? tile[offs[e + 2] + base] : 0.f;
-                v.w = e + 3 < cols ? tile[offs[e + 3] + base] : 0.f;
-                row[e4] = v;
-            }
+            float* row = dh + (q * rm.rpi + int64_t(r) * rm.sr + int64_t(c) * rm.sc) * ld;
+#pragma unroll 4
+            for (int e = lane; e < ld4 * 4; e += 32) row[e] = e < cols ? tile[offs[e] + base] : 0.f;
         }
     }
 }
@@ -364,14 +359,21 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t ld, 
     const int kd = k * d, slab = m * kd;
     const int npair_max = (k + s - 1) / s;
     int* stab = reinterpret_cast<int*>(sm + npair_max * slab);  // slab: staged float -> c*ld + rr
-    int* meta = stab + slab;                                     // n*d: (ch | j0 << 8 | c0 << 16)
+    int* meta = stab + slab;                                     // n*d: tap run per output
     for (int e = threadIdx.x; e < slab; e += blockDim.x) {
         const int c = e / kd;
         stab[e] = c * int(ld) + (e - c * kd);
     }
+    // per dx column element: slab offset of its first valid tap (c < m) and the
+    // number of taps (j = j0 + t s, c = c0 - t, 0 <= c < m, j < k): branch-free sums
     for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
         const int xx = e / d, ch = e - xx * d, px = xx + p;
-        meta[e] = ch | ((px % s) << 8) | ((px / s) << 16);
+        int j = px % s, c = px / s;
+        while (c >= m && j < k) { j += s; --c; }   // skip taps whose window starts past the image
+        int cnt = 0;
+        for (int jj = j, cc = c; jj < k && cc >= 0; jj += s, --cc) ++cnt;
+        const int off = (cnt > 0) ? c * kd + j * d + ch : 0;
+        meta[e] = off | (cnt << 24);                // off < 2^24 (slab <= 96 KiB)
     }
     const int64_t nqy = g.b * n;
     for (int64_t qy = blockIdx.x; qy < nqy; qy += gridDim.x) {
@@ -392,15 +394,14 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t ld, 
         cp_async_wait_all();
         __syncthreads();
         float* out = dx + qy * int64_t(n) * d;
+        const int delta = s * d - kd;  // slab step from tap t to t + 1
         for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
             const int mt = meta[e];
-            const int ch = mt & 0xFF, j0 = (mt >> 8) & 0xFF, c0 = mt >> 16;
+            const int off = mt & 0xFFFFFF, cnt = mt >> 24;
             float acc = 0.f;
             for (int a = 0; a < np; ++a) {
-                const float* sl = sm + a * slab + ch;
-                int c = c0;
-                for (int j = j0; j < k && c >= 0; j += s, --c)
-                    if (c < m) acc += sl[c * kd + j * d];
+                const float* sl = sm + a * slab + off;
+                for (int t = 0; t < cnt; ++t) acc += sl[t * delta];
             }
             out[e] = acc;
         }

@@ -1,6 +1,8 @@
 // reduce.cu -- deterministic split-K reduction for the backward-weight GEMMs.
 // Each output element sums its split partials in ascending split order, so the
 // result is run-to-run bit-identical (no atomics).
+#include <algorithm>
+
 #include "common.cuh"
 #include "reduce.cuh"
 
@@ -22,10 +24,38 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ part, int64_t sst
 }
 }  // namespace
 
+// first level of a two-level reduce: group g sums splits [g*G, min((g+1)*G, S))
+// into tmp[g] (ascending order), so the final result is a fixed-order sum.
+__global__ void splitk_group_kernel(const float* part, int64_t sstride, int splits, int group, int64_t n,
+                                    float* tmp) {
+    const int g = blockIdx.y;
+    const int s0 = g * group, s1 = min(splits, s0 + group);
+    for (int64_t e = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < n; e += int64_t(gridDim.x) * blockDim.x) {
+        float acc = 0.f;
+#pragma unroll 4
+        for (int s = s0; s < s1; ++s) acc += part[int64_t(s) * sstride + e];
+        tmp[int64_t(s0) * sstride + e] = acc;  // in place: the group's first slice
+    }
+}
+
 cudaError_t splitk_reduce(const float* part, int64_t split_stride, int splits, int64_t rows,
                           int64_t cols, int64_t ld_in, float* out, int64_t ld_out, cudaStream_t st) {
     const int threads = 256;
     PhaseScope ps(kPhaseReduce, st, 0, 4.0 * double(rows * cols) * double(splits + 1));
+    // Many partials (long-K backward-weight): two fixed-order levels, the first
+    // in place over groups of 16 slices, so thousands of threads stream instead
+    // of each summing hundreds of dependent loads.
+    constexpr int kGroup = 16;
+    if (splits > kGroup && ld_in == cols) {
+        const int64_t n = rows * cols;
+        const int ngroups = (splits + kGroup - 1) / kGroup;
+        const int gx = std::max(1, int(std::min<int64_t>(cdiv(n, threads), int64_t(num_sms()) * 16 / ngroups + 1)));
+        splitk_group_kernel<<<dim3(gx, ngroups), threads, 0, st>>>(part, split_stride, splits, kGroup, n,
+                                                                   const_cast<float*>(part));
+        note_launch();
+        split_stride *= kGroup;
+        splits = ngroups;
+    }
     splitk_reduce_kernel<<<grid_for(rows * cols, threads), threads, 0, st>>>(
         part, split_stride, splits, rows, cols, ld_in, out, ld_out);
     note_launch();
