@@ -193,6 +193,16 @@ def measured_peaks():
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
 
 
+def gemm_traffic():
+    """DRAM bytes per GEMM launch from the committed ncu launch list of this
+    command (profiles/r01/gemm_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r01", "gemm_traffic.json")
+    try:
+        return json.load(open(p))["avg_dram_bytes_per_launch"]
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def tf32_cublas_probe(torch):
     """cuBLAS dense TF32 throughput on this box (context for the roofline)."""
     n = 8192
@@ -310,7 +320,7 @@ def run_ours(a):
         "frac": (achieved / peak) if achieved else None,
         "peak_source": f"{peak_src} bf16_tflops_sustained / 2 (TF32 rate) / 3 (3xTF32 products)",
         "tf32_cublas_tflops_measured": tf32_meas,
-        "traffic": None,
+        "traffic": gemm_traffic(),
         "gemm_share_of_step": (gemm_ms / ms) if ms else None,
     }
 
