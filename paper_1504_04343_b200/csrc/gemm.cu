@@ -42,7 +42,9 @@ struct KParams {
     int ic_d, ic_k, ic_s, ic_p, ic_m, ic_mm, ic_cpt;
 };
 
-constexpr int kThreads = 384;
+// warps 0-3 control (TMA, MMA, TMEM alloc, spare), 4-7 epilogue, 8.. transform
+constexpr int kTransformWarps = 4;
+constexpr int kThreads = 256 + 32 * kTransformWarps;
 
 __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
     return (2 * bn) <= 32 ? 32 : (2 * bn) <= 64 ? 64 : (2 * bn) <= 128 ? 128 : (2 * bn) <= 256 ? 256 : 512;
@@ -59,10 +61,14 @@ struct Cfg {
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t STAGE_BYTES = 2 * RAW_BYTES;  // raw | small
     // as many ring stages as fit next to the barriers (227 KB opt-in smem per CTA)
-    static constexpr int STAGES = ((225 * 1024) / STAGE_BYTES) > 8 ? 8 : ((225 * 1024) / STAGE_BYTES);
+    static constexpr int STAGES = ((225 * 1024) / STAGE_BYTES) > 12 ? 12 : ((225 * 1024) / STAGE_BYTES);
     static constexpr uint32_t BAR_BYTES = (3 * STAGES + 4) * 8 + 16;
     static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
-    static constexpr uint32_t TMEM_COLS = tmem_cols_for(BN);
+    // Narrow tiles keep two sub-accumulators per tile (even / odd 8-wide K steps):
+    // consecutive MMAs then target different TMEM regions and overlap instead of
+    // serialising on one accumulator (measured: N=96 MMAs were latency-bound).
+    static constexpr int NACC = (BN <= 128) ? 2 : 1;
+    static constexpr uint32_t TMEM_COLS = tmem_cols_for(NACC * BN);
 };
 
 // a = big + small; big is what the tensor core reads from an fp32 operand in
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&tdone[s], 4 * CG);   // transform warps of every CTA in the group
+            ptx::mbar_init(&tdone[s], kTransformWarps * CG);  // transform warps of every CTA in the group
             ptx::mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -230,7 +236,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t use = uint32_t(local >> 1);
                 ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + uint32_t(acc * BN);
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * C_::NACC * BN);
+                auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
+                    if constexpr (CG == 1) ptx::mma_tf32(d, a, b, idesc, accumulate);
+                    else ptx::mma_tf32_cg2(d, a, b, idesc, accumulate);
+                };
                 for (int kb = kb0; kb < kb1; ++kb) {
                     // tdone implies the raw tiles of every CTA in the group landed
                     // (each transform warp waited on its own CTA's full barrier)
@@ -240,28 +250,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_raw = a_raw + C_::A_BYTES;
                     const uint32_t a_sml = a_raw + C_::RAW_BYTES;
                     const uint32_t b_sml = b_raw + C_::RAW_BYTES;
+                    if constexpr (C_::NACC == 1) {
 #pragma unroll
-                    for (int kk = 0; kk < kBK / 8; ++kk) {
-                        const uint64_t ad = tile_desc<A_MN>(a_raw, kk);
-                        const uint64_t bd = tile_desc<B_MN>(b_raw, kk);
-                        const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
-                        if constexpr (CG == 1) {
+                        for (int kk = 0; kk < kBK / 8; ++kk) {
+                            const uint64_t ad = tile_desc<A_MN>(a_raw, kk);
+                            const uint64_t bd = tile_desc<B_MN>(b_raw, kk);
+                            const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
                             if (p.passes == 3) {
                                 // small products first, big*big last
-                                ptx::mma_tf32(d_tmem, tile_desc<A_MN>(a_sml, kk), bd, idesc, first);
-                                ptx::mma_tf32(d_tmem, ad, tile_desc<B_MN>(b_sml, kk), idesc, 1u);
-                                ptx::mma_tf32(d_tmem, ad, bd, idesc, 1u);
+                                mma(d_tmem, tile_desc<A_MN>(a_sml, kk), bd, first);
+                                mma(d_tmem, ad, tile_desc<B_MN>(b_sml, kk), 1u);
+                                mma(d_tmem, ad, bd, 1u);
                             } else {
-                                ptx::mma_tf32(d_tmem, ad, bd, idesc, first);
+                                mma(d_tmem, ad, bd, first);
                             }
+                        }
+                    } else {
+                        // K step kk accumulates into sub-accumulator kk; passes interleave
+                        // the two so neighbouring MMAs are independent
+                        const uint32_t first = (kb > kb0) ? 1u : 0u;
+                        if (p.passes == 3) {
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                mma(d_tmem + kk * BN, tile_desc<A_MN>(a_sml, kk), tile_desc<B_MN>(b_raw, kk), first);
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                mma(d_tmem + kk * BN, tile_desc<A_MN>(a_raw, kk), tile_desc<B_MN>(b_sml, kk), 1u);
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                mma(d_tmem + kk * BN, tile_desc<A_MN>(a_raw, kk), tile_desc<B_MN>(b_raw, kk), 1u);
                         } else {
-                            if (p.passes == 3) {
-                                ptx::mma_tf32_cg2(d_tmem, tile_desc<A_MN>(a_sml, kk), bd, idesc, first);
-                                ptx::mma_tf32_cg2(d_tmem, ad, tile_desc<B_MN>(b_sml, kk), idesc, 1u);
-                                ptx::mma_tf32_cg2(d_tmem, ad, bd, idesc, 1u);
-                            } else {
-                                ptx::mma_tf32_cg2(d_tmem, ad, bd, idesc, first);
-                            }
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                mma(d_tmem + kk * BN, tile_desc<A_MN>(a_raw, kk), tile_desc<B_MN>(b_raw, kk), first);
                         }
                     }
                     if constexpr (CG == 1) ptx::mma_commit(&empty[stage]);
@@ -294,7 +315,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t v[32];
-                ptx::tmem_ld_32x32b_x32(tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * BN + c0), v);
+                const uint32_t tcol = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * C_::NACC * BN + c0);
+                ptx::tmem_ld_32x32b_x32(tcol, v);
+                if constexpr (C_::NACC == 2) {
+                    uint32_t v2[32];
+                    ptx::tmem_ld_32x32b_x32(tcol + BN, v2);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
+                }
                 ptx::tmem_ld_wait();
                 float* dst = p.C + off + int64_t(n0 + c0) * sn;
                 const int nlim = p.N - (n0 + c0);
@@ -335,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
                     constexpr int n4 = C_::RAW_BYTES / 16;
 #pragma unroll 4
-                    for (int i = t; i < n4; i += 128) {
+                    for (int i = t; i < n4; i += 32 * kTransformWarps) {
                         const float4 v = ptx::lds128(raw + i * 16);
                         ptx::sts128(raw + C_::RAW_BYTES + i * 16, small_part(v));
                     }
@@ -529,13 +558,24 @@ int choose_bn(int64_t N) {
 int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn) {
     const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + bn - 1) / bn);
     const int64_t kb = (K + kBK - 1) / kBK;
-    int64_t s = (kb + kMaxChainKB - 1) / kMaxChainKB;  // accuracy floor
-    if (tiles * s < 2 * int64_t(sms) && kb >= 64) {
-        // fill ~2 waves while keeping >= 32 k-blocks per split
-        const int64_t fill = (2 * int64_t(sms) + tiles - 1) / tiles;
-        s = std::max(s, std::min<int64_t>(fill, kb / 32));
+    const int64_t s_min = std::max<int64_t>(1, (kb + kMaxChainKB - 1) / kMaxChainKB);  // accuracy floor
+    if (kb < 64) return int(s_min);
+    // Pick the split count in [s_min, 4 s_min] (>= 16 k-blocks per split) whose
+    // units fill the last wave best; the (pair-)units run on sms/2 clusters when
+    // pairs are used, so evaluate on 128-row tiles and the full SM count (both
+    // scale alike).  Ties keep the smaller split count.
+    int64_t best = s_min;
+    double best_eff = 0.0;
+    for (int64_t s = s_min; s <= 4 * s_min && kb / s >= 16; ++s) {
+        const int64_t units = tiles * s;
+        const int64_t waves = (units + sms - 1) / sms;
+        const double eff = double(units) / double(waves * sms);
+        if (eff > best_eff + 0.02) {
+            best_eff = eff;
+            best = s;
+        }
     }
-    return int(std::max<int64_t>(1, s));
+    return int(best);
 }
 
 cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {

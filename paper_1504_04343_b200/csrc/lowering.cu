@@ -154,31 +154,27 @@ __global__ void lift_kernel(const float* __restrict__ rh, float* __restrict__ y,
 }
 
 // T1 expand: dRhat1^T[o][q*m^2 + pix] = dy[q][o][pix] -- a permutation of the
-// (q, o) planes.  Thread per source element (coalesced reads); the writes are
-// contiguous runs of m^2 floats.  Four independent elements per thread.
+// (q, o) planes.  One block-row per group of planes; each warp copies one plane
+// as a contiguous run (coalesced on both sides), 32-bit index math only.
 __global__ void expand_t1_kernel(const float* __restrict__ dy, float* __restrict__ drt, int64_t b, int o,
                                  int mm, int64_t ldr) {
-    const int64_t total = b * o * int64_t(mm);
-    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
-    for (int64_t e0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; e0 < total; e0 += 4 * stride) {
-        float v[4];
-        int64_t dst[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int64_t e = e0 + u * stride;
-            dst[u] = -1;
-            if (e < total) {
-                const int64_t pl = e / mm;
-                const int pix = int(e - pl * mm);
-                const int oj = int(pl % o);
-                const int64_t q = pl / o;
-                v[u] = __ldg(dy + e);
-                dst[u] = int64_t(oj) * ldr + q * mm + pix;
-            }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const int64_t planes = b * o;
+    for (int64_t pl = int64_t(blockIdx.x) * nw + warp; pl < planes; pl += int64_t(gridDim.x) * nw) {
+        const int oj = int(pl % o);
+        const int64_t q = pl / o;
+        const float* src = dy + pl * mm;
+        float* dst = drt + int64_t(oj) * ldr + q * mm;
+        int e = lane;
+        for (; e + 96 < mm; e += 128) {  // four loads in flight per lane
+            const float v0 = __ldg(src + e), v1 = __ldg(src + e + 32), v2 = __ldg(src + e + 64),
+                        v3 = __ldg(src + e + 96);
+            dst[e] = v0;
+            dst[e + 32] = v1;
+            dst[e + 64] = v2;
+            dst[e + 96] = v3;
         }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-            if (dst[u] >= 0) drt[dst[u]] = v[u];
+        for (; e < mm; e += 32) dst[e] = __ldg(src + e);
     }
 }
 
@@ -483,7 +479,7 @@ cudaError_t expand(const Geo& g, int type, const float* dy, float* drt, int64_t 
     const int64_t ncols = lowered_ncols(g, type);
     PhaseScope ps(kPhaseExpand, st, 0, 4.0 * double(g.b * g.o * g.m * g.m + ncols * g.b * rm.rpi));
     if (type == 1) {
-        const int grid = grid_for(g.b * g.o * g.m * g.m / 4 + 1, kThreads, 16);
+        const int grid = grid_for(g.b * g.o * 32, kThreads, 16);  // one warp per plane
         expand_t1_kernel<<<grid, kThreads, 0, st>>>(dy, drt, g.b, int(g.o), int(g.m * g.m), ldr);
     } else {
         if (ncols > 65535 || g.b * rm.rpi >= (int64_t(1) << 31)) return cudaErrorInvalidConfiguration;

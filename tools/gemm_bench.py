@@ -25,6 +25,8 @@ SHAPES = {
     "dgrad_like": (2400, 186624, 256),
     "wgrad_like": (2400, 256, 4096),
     "square": (8192, 8192, 2048),
+    "narrow96": (65536, 96, 4096),
+    "mid192": (65536, 192, 4096),
 }
 
 
