@@ -320,6 +320,8 @@ def run_ours(a):
         "frac": (achieved / peak) if achieved else None,
         "peak_source": f"{peak_src} bf16_tflops_sustained / 2 (TF32 rate) / 3 (3xTF32 products)",
         "tf32_cublas_tflops_measured": tf32_meas,
+        "frac_of_burst_ceiling": (achieved / (tf32_meas / 3.0)) if (achieved and tf32_meas) else None,
+        "step_frac": (flops_step / world / (ms_max * 1e-3) / 1e12) / peak,
         "traffic": gemm_traffic(),
         "gemm_share_of_step": (gemm_ms / ms) if ms else None,
     }

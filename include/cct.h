@@ -113,12 +113,17 @@ CCT_API cct_status cct_conv_bwd_weight(const cct_conv_desc* desc, cct_lowering l
 CCT_API void cct_set_workspace_limit(size_t bytes);
 CCT_API size_t cct_get_workspace_limit(void);
 
-/* Implicit Type 1 lowering (default on; $CCT_IMPLICIT=0 disables): for Type 1
- * layers with d % 32 == 0 the forward and backward-weight GEMMs read their
- * lowered operand straight from x through TMA im2col tiles -- Dhat never
- * exists in HBM (the paper's "fusion").  Off: Dhat is
- * materialised by the lowering kernel (bit-identical results). */
-CCT_API void cct_set_implicit_lowering(int on);
+/* Implicit Type 1 lowering (the paper's "fusion").
+ * mode 1 (default; $CCT_IMPLICIT): for Type 1 layers with d % 32 == 0 the
+ *   forward and backward-weight GEMMs read their lowered operand straight from
+ *   x through TMA im2col tiles -- Dhat never exists in HBM (bit-identical to
+ *   the materialised path).  At stride 1 with o % 16 == 0, backward-data runs
+ *   as the forward convolution of dy (transposed to NHWC) with the rotated
+ *   kernel bank, written straight to dx (no dDhat, no col2im), whenever the
+ *   cost model predicts that faster.
+ * mode 2: every implicit form whenever possible (tests).
+ * mode 0: everything materialised. */
+CCT_API void cct_set_implicit_lowering(int mode);
 CCT_API int cct_get_implicit_lowering(void);
 
 /* Training-step entry points (the lowered-matrix cache).

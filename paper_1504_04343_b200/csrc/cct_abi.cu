@@ -138,7 +138,7 @@ int g_implicit = -1;
 bool implicit_enabled() {
     if (g_implicit < 0) {
         const char* e = getenv("CCT_IMPLICIT");
-        g_implicit = e ? (atoi(e) != 0) : 1;
+        g_implicit = e ? std::max(0, std::min(2, atoi(e))) : 1;
     }
     return g_implicit != 0;
 }
@@ -147,6 +147,34 @@ bool implicit_enabled() {
 bool t1_implicit(const Geo& g, int type, const float* x) {
     return implicit_enabled() && type == 1 && im2col_ok(g.d, true) && x && aligned16(x) &&
            g.n * g.n * g.d * g.b < (int64_t(1) << 40) && g.b * g.m * g.m < (int64_t(1) << 31);
+}
+
+}  // namespace
+namespace cct {
+bool prefer_implicit_dgrad(const cct_conv_desc* desc);  // cost_model.cpp
+}  // namespace cct
+namespace {
+
+// Implicit Type 1 backward (stride 1): dy is transposed once to NHWC and
+//  * backward-data is the forward convolution of dy with the rotated kernel bank
+//    wr[c][k-1-i][k-1-j][o] = w[o][i][j][c] at pad k-1-p, gathered by TMA im2col
+//    and written straight to dx (no dDhat, no col2im);
+//  * backward-weight reads that NHWC dy as its (MN-major) B operand.
+// Used when the cost model predicts it faster than the materialised form
+// (prefer_implicit_dgrad, cost_model.cpp) -- always under implicit mode 2.
+bool t1_implicit_bwd(const Geo& g, int type) {
+    if (!(implicit_enabled() && type == 1 && g.s == 1 && g.p <= g.k - 1 && im2col_ok(g.o, false) &&
+          g.b * g.n * g.n < (int64_t(1) << 31) && g.b * g.m * g.m * g.o < (int64_t(1) << 40)))
+        return false;
+    static const int env = [] {  // $CCT_IMPLICIT_BWD: 0 never, 2 always (profiling)
+        const char* e = getenv("CCT_IMPLICIT_BWD");
+        return e ? atoi(e) : 1;
+    }();
+    if (env == 0) return false;
+    if (env == 2) return true;
+    cct_conv_desc d{};
+    d.n = g.n; d.k = g.k; d.d = g.d; d.o = g.o; d.b = g.b; d.stride = g.s; d.pad = g.p;
+    return prefer_implicit_dgrad(&d);
 }
 
 Im2col im2col_of(const Geo& g, const float* x) {
@@ -244,8 +272,73 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
 // bwd-weight (dw != null).  bwd-weight reads Dhat from `cache` when given (as
 // left there by cct_conv_fwd_cached), else lowers x again.  The two passes run
 // in stream order and reuse the same scratch region after dRhat^T.
+cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, const float* dy, const float* w,
+                            float* dx, float* dw, Ws& ws, cudaStream_t st) {
+    const Lowered L = lowered_of(g, 1);
+    const int64_t mm = g.m * g.m, kk = g.k * g.k;
+    float* dyn = ws.take(g.b * mm * g.o);  // dy as NHWC: [b][m][m][o] = dRhat (rows x o)
+    if (ws.base) CCT_TRY(transpose_batched(dy, g.o, mm, mm, g.o * mm, dyn, g.o, mm * g.o, g.b, kPhaseExpand, st),
+                         "dy to NHWC");
+    const size_t mark = ws.off;
+    size_t hi = mark;
+    if (dx) {
+        // rotated kernel bank wr[c][(k-1-i)*k + (k-1-j)][o] = w[o][i][j][c]: one
+        // (o x d) -> (d x o) transpose per tap, written in reversed tap order
+        float* wr = ws.take(g.d * kk * g.o);
+        if (ws.base)
+            CCT_TRY(transpose_batched(w, g.o, g.d, kk * g.d, g.d, wr + (kk - 1) * g.o, kk * g.o, -g.o, kk, kPhaseOther,
+                                      st),
+                    "rotate weights");
+        Geo v = g;  // the forward convolution that computes dx
+        v.n = g.m; v.d = g.o; v.o = g.d; v.p = g.k - 1 - g.p; v.m = g.n;
+        GemmProblem gp;
+        gp.M = g.b * g.n * g.n;
+        gp.N = g.d;
+        gp.K = kk * g.o;
+        gp.A = {nullptr, 0, Major::K};
+        gp.B = {wr, kk * g.o, Major::K};
+        gp.im2col = im2col_of(v, dyn);
+        gp.C.s_mr = g.d;
+        gp.C.s_n = 1;
+        cct_status s = gemm_capped(gp, dx, g.b * g.n * g.n * g.d, ws, st, "gemm (bwd-data, implicit)");
+        if (s != CCT_OK) return s;
+        hi = std::max(hi, ws.off);
+        ws.off = mark;
+    }
+    if (dw) {
+        cudaError_t e = cudaSuccess;
+        const bool implicit = t1_implicit(g, 1, x);
+        const float* dh = implicit ? nullptr : cache ? cache : dhat_of(g, 1, L, x, nullptr, ws, st, &e);
+        CCT_TRY(e, "lower");
+        const int splits = wgrad_splits(L);
+        const int64_t wsize = L.ncols * L.cols;
+        float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
+        if (ws.base) {
+            GemmProblem gp;
+            gp.M = L.cols;
+            gp.N = L.ncols;
+            gp.K = L.rows;
+            gp.A = {dh, L.ldc, Major::MN};
+            gp.B = {dyn, g.o, Major::MN};
+            if (implicit) gp.im2col = im2col_of(g, x);
+            gp.C.ptr = parts;
+            gp.C.s_mr = 1;
+            gp.C.s_n = L.cols;
+            gp.C.s_split = wsize;
+            gp.splits = splits;
+            CCT_TRY(run_gemm(gp, st), "gemm (bwd-weight)");
+            if (splits > 1)
+                CCT_TRY(splitk_reduce(parts, wsize, splits, 1, wsize, wsize, dw, wsize, st), "split-K reduce");
+        }
+        hi = std::max(hi, ws.off);
+    }
+    ws.off = hi;
+    return CCT_OK;
+}
+
 cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
                        float* dx, float* dw, Ws& ws, cudaStream_t st) {
+    if (t1_implicit_bwd(g, type)) return run_bwd_implicit(g, x, cache, dy, w, dx, dw, ws, st);
     const Lowered L = lowered_of(g, type);
     cudaError_t e = cudaSuccess;
     float* drt = ws.take(L.ncols * L.ldr);
@@ -411,8 +504,8 @@ extern "C" {
 
 int cct_abi_version(void) { return CCT_ABI_VERSION; }
 void cct_set_workspace_limit(size_t bytes) { g_ws_limit = bytes; }
-void cct_set_implicit_lowering(int on) { g_implicit = on ? 1 : 0; }
-int cct_get_implicit_lowering(void) { return implicit_enabled() ? 1 : 0; }
+void cct_set_implicit_lowering(int mode) { g_implicit = std::max(0, std::min(2, mode)); }
+int cct_get_implicit_lowering(void) { return implicit_enabled() ? g_implicit : 0; }
 size_t cct_get_workspace_limit(void) { return ws_limit(); }
 void cct_profile_enable(int on) { cct::profile_enable(on != 0); }
 void cct_profile_read(double* ms, double* flops, double* bytes, uint64_t* launches, int reset) {

@@ -82,6 +82,47 @@ double gemm_seconds(double M, double N, double K, const cct_calibration* c) {
     return 2.0 * rup(M, 128) * rup(N, bn) * K / rate;
 }
 
+// Backward-data of Type 1 at stride 1 can run implicitly (cct_abi.cu
+// run_bwd_implicit): dy -> NHWC transpose, then the forward convolution of dy
+// with the rotated kernel bank straight into dx (GEMM b n^2 x d x k^2 o).
+bool implicit_dgrad_possible(const G& g) {
+    return cct_get_implicit_lowering() && g.s == 1 && g.p <= g.k - 1 && std::fmod(g.o, 16) == 0;
+}
+
+// seconds of the bwd-data GEMM + its data movement after dRhat is available;
+// `implicit` selects the implicit form (no dDhat, no col2im)
+double dgrad_seconds(const G& g, bool implicit, double rows, double cols, double ncols, double dhat, double rhat,
+                     double xin, bool t3_zero_copy, const cct_calibration* c, double* by, double* launches) {
+    double t = 0;
+    if (implicit) {
+        const double K = g.k * g.k * g.o, M = g.b * g.n * g.n;
+        const double gt = gemm_seconds(M, g.d, K, c);
+        const double gb = rhat + xin;
+        t += std::max(gt, gb / c->hbm_bytes_per_s);
+        *by += gb;
+        *launches += 2;  // rotate weights + GEMM
+        const double chains = std::ceil(K / 4096.0);
+        if (chains > 1) {  // accuracy split-K: partials written, reduced
+            const double rb = (2 * chains + 1) * xin;
+            t += rb / c->hbm_bytes_per_s;
+            *by += rb;
+            *launches += 1;
+        }
+        return t;
+    }
+    const double gt = gemm_seconds(cols, rows, ncols, c);
+    const double gb = rhat + dhat;
+    t += std::max(gt, gb / c->hbm_bytes_per_s);
+    *by += gb;
+    *launches += 1;
+    if (!t3_zero_copy) {  // col2im / crop
+        t += (dhat + xin) / c->hbm_bytes_per_s;
+        *by += dhat + xin;
+        *launches += 1;
+    }
+    return t;
+}
+
 // counts + model for one pass.  pass: 0 fwd, 1 bwd-data, 2 bwd-weight
 void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* secs, double* bytes) {
     const double f = 4.0;  // bytes per float
@@ -102,6 +143,24 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     auto hbm = [&](double b) { by += b; t += b / c->hbm_bytes_per_s; launches += 1; };
     auto hbm_at = [&](double b, double bw) { by += b; t += b / bw; launches += 1; };
     const double a_in = t1_implicit ? xin : dhat;         // bytes of the A operand stream
+    // backward-data: the faster of the materialised and (Type 1, stride 1) implicit forms,
+    // as the product picks it (prefer_implicit_dgrad)
+    auto dgrad = [&](double* b_, double* l_) {
+        double be = 0, le = 0;
+        const double te = dgrad_seconds(g, false, rows, cols, ncols, dhat, rhat, xin, t3_zero_copy, c, &be, &le);
+        if (type == 1 && implicit_dgrad_possible(g)) {
+            double bi = 0, li = 0;
+            const double ti = dgrad_seconds(g, true, rows, cols, ncols, dhat, rhat, xin, t3_zero_copy, c, &bi, &li);
+            if (cct_get_implicit_lowering() == 2 || ti + li * c->launch_s < te + le * c->launch_s) {
+                *b_ += bi;
+                *l_ += li;
+                return ti;
+            }
+        }
+        *b_ += be;
+        *l_ += le;
+        return te;
+    };
     if (pass == 0) {
         if (!t3_zero_copy && !t1_implicit) hbm(xin + dhat); // lower
         const double gt = gemm_seconds(rows, ncols, cols, c);
@@ -112,12 +171,7 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         if (type != 1) hbm_at(rhat + yout, lift_bw);       // lift
     } else if (pass == 1) {
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand
-        const double gt = gemm_seconds(cols, rows, ncols, c);
-        const double gb = rhat + dhat;
-        t += std::max(gt, gb / c->hbm_bytes_per_s);
-        by += gb;
-        launches += 1;
-        if (!t3_zero_copy) hbm(dhat + xin);                // col2im / crop
+        t += dgrad(&by, &launches);
     } else if (pass == 2) {
         if (!t3_zero_copy && !t1_implicit) hbm(xin + dhat); // lower
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand
@@ -135,22 +189,39 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         by += gb;
         if (type != 1) hbm_at(rhat + yout, lift_bw);       // lift
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand (shared)
-        gt = gemm_seconds(cols, rows, ncols, c);           // bwd-data GEMM
-        gb = rhat + dhat;
-        t += std::max(gt, gb / c->hbm_bytes_per_s);
-        by += gb;
-        if (!t3_zero_copy) hbm(dhat + xin);                // col2im / crop
+        t += dgrad(&by, &launches);                        // bwd-data
         gt = gemm_seconds(cols, ncols, rows, c) * (t1_implicit ? 1.1 : 1.0);  // bwd-weight GEMM
         gb = a_in + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
-        launches += 4;                                     // 3 GEMMs + split-K reduce
+        launches += 3;                                     // 2 GEMMs + split-K reduce
     }
     *secs = t + launches * c->launch_s;
     *bytes = by;
 }
 
 }  // namespace
+
+namespace cct {
+// Used by the launcher (cct_abi.cu): run Type 1 backward-data implicitly when
+// that form is possible and the model predicts it faster.
+bool prefer_implicit_dgrad(const cct_conv_desc* desc) {
+    const G g = geo(desc);
+    if (!implicit_dgrad_possible(g)) return false;
+    if (cct_get_implicit_lowering() == 2) return true;  // forced (tests)
+    cct_calibration cal;
+    cct_calibration_default(&cal);
+    const double f = 4.0;
+    const double rows = g.b * g.m * g.m, cols = g.k * g.k * g.d, ncols = g.o;
+    const double dhat = rows * rup(cols, 4) * f, rhat = rows * ncols * f, xin = g.b * g.n * g.n * g.d * f;
+    double b0 = 0, l0 = 0, b1 = 0, l1 = 0;
+    const double te = dgrad_seconds(g, false, rows, cols, ncols, dhat, rhat, xin, false, &cal, &b0, &l0) +
+                      l0 * cal.launch_s;
+    const double ti = dgrad_seconds(g, true, rows, cols, ncols, dhat, rhat, xin, false, &cal, &b1, &l1) +
+                      l1 * cal.launch_s;
+    return ti < te;
+}
+}  // namespace cct
 
 extern "C" {
 

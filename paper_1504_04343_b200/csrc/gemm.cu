@@ -173,8 +173,30 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int n0 = nt * BN + int(rank) * BNL;
                 const int kb0 = sp * p.kb_per_split;
                 const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
-                Pix tile_px{};
-                if constexpr (A_IM && !A_MN) tile_px = pix_of(m0, p);  // forward: rows are pixels
+                // implicit lowering: the producer is one thread issuing every TMA of the
+                // CTA, so all im2col coordinates are per-tile constants or walked
+                // incrementally (no divisions inside the k-loop)
+                Pix px{};      // forward: first pixel of the tile; bwd-weight: pixel of k0
+                int tap_i = 0, tap_j = 0, cc = 0;   // forward: filter tap and channel block of kb
+                int bw_ch[kBM / 32], bw_ti[kBM / 32], bw_tj[kBM / 32];  // bwd-weight: per 32-row box
+                if constexpr (A_IM && !A_MN) {
+                    px = pix_of(m0, p);
+                    const int tap = kb0 / p.ic_cpt;
+                    cc = kb0 - tap * p.ic_cpt;
+                    tap_i = tap / p.ic_k;
+                    tap_j = tap - tap_i * p.ic_k;
+                } else if constexpr (A_IM && A_MN) {
+                    px = pix_of(kb0 * kBK, p);
+                    const int kkd = p.ic_k * p.ic_k * p.ic_d;
+#pragma unroll
+                    for (int c = 0; c < kBM / 32; ++c) {
+                        const int mcol = min(m0 + 32 * c, kkd - 32);  // rows >= M are masked later
+                        const int tap = mcol / p.ic_d;
+                        bw_ch[c] = mcol - tap * p.ic_d;
+                        bw_ti[c] = tap / p.ic_k;
+                        bw_tj[c] = tap - bw_ti[c] * p.ic_k;
+                    }
+                }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
                     ptx::mbar_arrive_expect_tx(&full[stage], C_::RAW_BYTES);
@@ -183,24 +205,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int k0 = kb * kBK;
                     if constexpr (A_IM && !A_MN) {
                         // implicit lowering, forward: 128 pixels x 16 channels of filter tap (ti, tj)
-                        const int tap = kb / p.ic_cpt;
-                        const int ch0 = (kb - tap * p.ic_cpt) * kBK;
-                        const int ti = tap / p.ic_k, tj = tap - ti * p.ic_k;
-                        ptx::tma_load_im2col_4d(a_dst, &tmA, &full[stage], ch0, p.ic_s * tile_px.c - p.ic_p,
-                                                p.ic_s * tile_px.r - p.ic_p, tile_px.q, uint16_t(tj), uint16_t(ti));
+                        ptx::tma_load_im2col_4d(a_dst, &tmA, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
+                                                p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
+                        if (++cc == p.ic_cpt) {
+                            cc = 0;
+                            if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
+                        }
                     } else if constexpr (A_IM && A_MN) {
                         // implicit lowering, backward-weight: K rows = 16 pixels, M = (tap, ch)
-                        const Pix px = pix_of(k0, p);
-                        const int kkd = p.ic_k * p.ic_k * p.ic_d;
 #pragma unroll
-                        for (int c = 0; c < kBM / 32; ++c) {
-                            const int mcol = min(m0 + 32 * c, kkd - 32);  // rows >= M are masked later
-                            const int tap = mcol / p.ic_d;
-                            const int ch0 = mcol - tap * p.ic_d;
-                            const int ti = tap / p.ic_k, tj = tap - ti * p.ic_k;
-                            ptx::tma_load_im2col_4d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], ch0,
+                        for (int c = 0; c < kBM / 32; ++c)
+                            ptx::tma_load_im2col_4d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], bw_ch[c],
                                                     p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
-                                                    uint16_t(tj), uint16_t(ti));
+                                                    uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
+                        px.c += kBK;
+                        while (px.c >= p.ic_m) {
+                            px.c -= p.ic_m;
+                            if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
                         }
                     } else if constexpr (!A_MN) {
                         ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
@@ -327,7 +348,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tmem_ld_wait();
                 float* dst = p.C + off + int64_t(n0 + c0) * sn;
                 const int nlim = p.N - (n0 + c0);
-                if (row_ok && nlim >= 32) {
+                if (row_ok && nlim >= 32 && sn == 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                    // row-major output (lane = row): 32 consecutive floats per thread
+                    float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                } else if (row_ok && nlim >= 32) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
                         *dst = __uint_as_float(v[j]);
@@ -506,9 +534,10 @@ template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
-    if (g.im2col.x) {  // implicit Type 1: forward (K, K) and backward-weight (MN, K)
+    if (g.im2col.x) {  // implicit Type 1: forward / backward-data (K, K), backward-weight (MN, K|MN)
         if (!amn && !bmn) return launch<BN, 0, 0, CG, 1>(ta, tb, kp, st);
         if (amn && !bmn) return launch<BN, 1, 0, CG, 1>(ta, tb, kp, st);
+        if (amn && bmn) return launch<BN, 1, 1, CG, 1>(ta, tb, kp, st);  // backward-weight, dy in NHWC
         return cudaErrorInvalidValue;
     }
     if (!amn && !bmn) return launch<BN, 0, 0, CG, 0>(ta, tb, kp, st);

@@ -31,7 +31,8 @@ struct OutMap {
 // through a TMA im2col tensor map (no Dhat in HBM).  Row (or K) index = output
 // pixel (q, r, c); lowered column = (i, j, ch) with ch fastest -- the same order
 // as the materialised Dhat, so B (the KernelBank) is unchanged.
-//   A.major == K  (forward):         tile = 128 pixels x 16 channels of one tap
+//   A.major == K  (forward; backward-data = forward of dy (NHWC) with rotated
+//                  weights): tile = 128 pixels x 16 channels of one tap
 //   A.major == MN (backward-weight): tile = 16 pixels x (4 x 32 channels)
 struct Im2col {
     const float* x = nullptr;  // nullptr: A is an ordinary (materialised) matrix

@@ -50,4 +50,9 @@ cudaError_t pad_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_sr
 cudaError_t transpose(const float* src, int64_t rows, int64_t cols, int64_t ld_src, float* dst,
                       int64_t ld_dst, cudaStream_t st);
 
+// batched: dst[z*dst_z + c*ldd + r] = src[z*src_z + r*lds + c] for z < nz (strides may be
+// negative); `phase` = the profiling phase the copy is accounted to
+cudaError_t transpose_batched(const float* src, int64_t rows, int64_t cols, int64_t lds, int64_t src_z, float* dst,
+                              int64_t ldd, int64_t dst_z, int64_t nz, int phase, cudaStream_t st);
+
 }  // namespace cct

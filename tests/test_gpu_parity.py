@@ -285,7 +285,7 @@ def test_cached_training_step_matches_separate_passes(cct, dev, orc, layer, t):
 @pytest.mark.parametrize("t", [1, 2, 3])
 def test_batch_chunking_under_workspace_limit(cct, dev, t):
     """A small workspace limit splits the batch into chunks (SPEC batching module):
-    fwd / bwd-data are bit-identical, bwd-weight agrees to the tolerance."""
+    every output agrees with the unchunked pass to fp32 rounding."""
     from paper_1504_04343_b200 import conv
     L = cct.lib()
     n, k, d, o, b, s, p = 27, 5, 32, 48, 12, 1, 2
@@ -306,10 +306,14 @@ def test_batch_chunking_under_workspace_limit(cct, dev, t):
         dx2, dw2 = conv.conv_bwd(dy, w, desc, t, x=x, cache=cache)
     finally:
         L.cct_set_workspace_limit(old)
-    assert torch.equal(ch[0], full[0]) and torch.equal(ch[1], full[1]) and torch.equal(y2, full[0])
-    assert torch.equal(dx2, full[1])
+    # chunks change the GEMM's N extent, hence possibly its tile width and the
+    # number of TMEM sub-accumulators: equal to fp32 rounding, not bit for bit
+    def close(a, ref):
+        return float(torch.linalg.norm(a - ref) / torch.linalg.norm(ref)) < 1e-5
+    assert close(ch[0], full[0]) and close(ch[1], full[1]) and close(y2, full[0])
+    assert close(dx2, full[1])
     for dwc in (ch[2], dw2):
-        assert float(torch.linalg.norm(dwc - full[2]) / torch.linalg.norm(full[2])) < 1e-5
+        assert close(dwc, full[2])
 
 
 @pytest.mark.parametrize("layer", [("conv2s", 27, 5, 96, 64, 1, 2), ("conv3", 13, 3, 256, 384, 1, 1),
@@ -344,3 +348,46 @@ def test_implicit_lowering_matches_materialised(cct, dev, orc, layer):
     assert torch.equal(dwi, dwm) and torch.equal(dwc, dwm)
     assert rel_l2(yi.cpu().numpy().ravel(), orc.conv_fwd(x_np, w_np, b, n, d, k, o, s, p)) <= TOL
     assert rel_l2(dwi.cpu().numpy().ravel(), orc.conv_bwd_weight(x_np, dy_np, b, n, d, k, o, s, p)) <= TOL
+
+
+@pytest.mark.parametrize("layer", [("conv2s", 27, 5, 96, 64, 1, 2), ("conv3", 13, 3, 256, 384, 1, 1),
+                                   ("pad0_d20", 12, 3, 20, 32, 1, 0), ("padk-1", 10, 3, 8, 16, 1, 2),
+                                   ("k1", 9, 1, 16, 16, 1, 0), ("d3", 11, 4, 3, 16, 1, 1),
+                                   ("longK", 9, 5, 8, 176, 1, 2), ("stride2", 15, 3, 32, 48, 2, 1)],
+                         ids=lambda l: l[0])
+def test_implicit_dgrad(cct, dev, orc, layer):
+    """Implicit stride-1 backward-data (dy -> NHWC, forward convolution with the rotated
+    kernel bank straight into dx; implicit mode 2 forces it) matches the oracle and the
+    materialised path; backward-weight with the NHWC dy as B operand too.  Stride 2 falls
+    back to the materialised form."""
+    from paper_1504_04343_b200 import conv
+    L = cct.lib()
+    _, n, k, d, o, s, p = layer
+    b = 3
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    x_np, w_np = orc.random_problem(91, b, n, d, k, o)
+    dy_np = orc.uniform(92, b * o * desc.m * desc.m)
+    x = T(x_np, dev, b, n, n, d)
+    w = T(w_np, dev, o, k, k, d)
+    dy = T(dy_np, dev, b, o, desc.m, desc.m)
+    old = L.cct_get_implicit_lowering()
+    try:
+        L.cct_set_implicit_lowering(2)
+        dxi, dwi = conv.conv_bwd_data(dy, w, desc, 1), conv.conv_bwd_weight(x, dy, desc, 1)
+        cache = conv.alloc_cache(desc, 1, dev)
+        conv.conv_fwd_cached(x, w, desc, 1, cache=cache)
+        dxc, dwc = conv.conv_bwd(dy, w, desc, 1, x=x, cache=cache)
+        L.cct_set_implicit_lowering(0)
+        dxm, dwm = conv.conv_bwd_data(dy, w, desc, 1), conv.conv_bwd_weight(x, dy, desc, 1)
+    finally:
+        L.cct_set_implicit_lowering(old)
+    assert torch.equal(dxc, dxi) and torch.equal(dwc, dwi)
+    ref_dx = orc.conv_bwd_data(dy_np, w_np, b, n, d, k, o, s, p)
+    ref_dw = orc.conv_bwd_weight(x_np, dy_np, b, n, d, k, o, s, p)
+    for got in (dxi, dxm):
+        assert rel_l2(got.cpu().numpy().ravel(), ref_dx) <= TOL
+    for got in (dwi, dwm):
+        assert rel_l2(got.cpu().numpy().ravel(), ref_dw) <= TOL
+    assert float(torch.linalg.norm(dxi - dxm) / torch.linalg.norm(dxm)) < 5e-5  # two ~1e-5 paths
+    if s != 1:
+        assert torch.equal(dxi, dxm)
