@@ -217,9 +217,15 @@ cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStr
     return CCT_OK;
 }
 
-int wgrad_splits(const Lowered& L) {
-    const int bn = choose_bn(L.ncols);
-    return choose_splits(L.cols, L.ncols, L.rows, num_sms(), bn);
+// backward-weight GEMM: dW^T (cols x ncols) = Dhat^T * dRhat, reduction over rows
+GemmProblem wgrad_problem(const Lowered& L, Operand a, Operand b) {
+    GemmProblem gp;
+    gp.M = L.cols;
+    gp.N = L.ncols;
+    gp.K = L.rows;
+    gp.A = a;
+    gp.B = b;
+    return gp;
 }
 
 // ---------------------------------------------------------------------------
@@ -310,17 +316,12 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
         const bool implicit = t1_implicit(g, 1, x);
         const float* dh = implicit ? nullptr : cache ? cache : dhat_of(g, 1, L, x, nullptr, ws, st, &e);
         CCT_TRY(e, "lower");
-        const int splits = wgrad_splits(L);
+        GemmProblem gp = wgrad_problem(L, {dh, L.ldc, Major::MN}, {dyn, g.o, Major::MN});
+        if (implicit) gp.im2col = im2col_of(g, x);
+        const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
         if (ws.base) {
-            GemmProblem gp;
-            gp.M = L.cols;
-            gp.N = L.ncols;
-            gp.K = L.rows;
-            gp.A = {dh, L.ldc, Major::MN};
-            gp.B = {dyn, g.o, Major::MN};
-            if (implicit) gp.im2col = im2col_of(g, x);
             gp.C.ptr = parts;
             gp.C.s_mr = 1;
             gp.C.s_n = L.cols;
@@ -373,17 +374,12 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
                                                                   : dhat_of(g, type, L, x, nullptr, ws, st, &e);
         CCT_TRY(e, "lower");
         const int64_t ldd = (dh == x) ? g.d : L.ldc;
-        const int splits = wgrad_splits(L);
+        GemmProblem gp = wgrad_problem(L, {dh, ldd, Major::MN}, {drt, L.ldr, Major::K});
+        if (implicit) gp.im2col = im2col_of(g, x);
+        const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
         if (ws.base) {
-            GemmProblem gp;
-            gp.M = L.cols;
-            gp.N = L.ncols;
-            gp.K = L.rows;
-            gp.A = {dh, ldd, Major::MN};
-            gp.B = {drt, L.ldr, Major::K};
-            if (implicit) gp.im2col = im2col_of(g, x);
             gp.C.ptr = parts;
             gp.C.s_mr = 1;
             gp.C.s_n = L.cols;
@@ -739,8 +735,7 @@ static cct_status gemm_common(int64_t M, int64_t N, int64_t K, const float* A, i
     gp.A = {B, ldb, Major::MN};
     gp.B = {A, lda, Major::K};
     gp.passes = passes;
-    const int bn = choose_bn(M);
-    int splits = split_k > 0 ? split_k : choose_splits(N, M, K, num_sms(), bn);
+    int splits = split_k > 0 ? split_k : plan_splits(gp);
     if (passes != 3) splits = 1;
     if (splits > 1) {
         const size_t need = size_t(splits) * size_t(M) * size_t(N) * 4;
@@ -759,7 +754,13 @@ static cct_status gemm_common(int64_t M, int64_t N, int64_t K, const float* A, i
 
 cct_status cct_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int split_k, size_t* bytes) {
     if (!bytes) return fail(CCT_ERR_CONFIG, "null size pointer");
-    const int splits = split_k > 0 ? split_k : choose_splits(N, M, K, num_sms(), choose_bn(M));
+    GemmProblem gp;  // same orientation as gemm_common
+    gp.M = N;
+    gp.N = M;
+    gp.K = K;
+    gp.A.major = Major::MN;
+    gp.B.major = Major::K;
+    const int splits = split_k > 0 ? split_k : plan_splits(gp);
     *bytes = splits > 1 ? size_t(splits) * size_t(M) * size_t(N) * 4 : 0;
     return CCT_OK;
 }

@@ -584,27 +584,32 @@ int choose_bn(int64_t N) {
 // kMaxChainK; longer reductions are split and the partials summed in fp32
 // round-to-nearest by the deterministic reduce kernel.  Short-K problems with
 // too few tiles to fill the machine are also split.
-int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn) {
-    const int64_t tiles = ((M + kBM - 1) / kBM) * ((N + bn - 1) / bn);
+int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn, int cg) {
+    const int64_t tiles = ((M + kBM * cg - 1) / (kBM * cg)) * ((N + bn - 1) / bn);
+    const int64_t slots = sms / cg;  // one CTA (pair) per SM (pair)
     const int64_t kb = (K + kBK - 1) / kBK;
     const int64_t s_min = std::max<int64_t>(1, (kb + kMaxChainKB - 1) / kMaxChainKB);  // accuracy floor
     if (kb < 64) return int(s_min);
     // Pick the split count in [s_min, 4 s_min] (>= 16 k-blocks per split) whose
-    // units fill the last wave best; the (pair-)units run on sms/2 clusters when
-    // pairs are used, so evaluate on 128-row tiles and the full SM count (both
-    // scale alike).  Ties keep the smaller split count.
+    // (pair-)units fill the last wave of the machine best; ties keep the smaller
+    // split count (less partial-sum traffic).
     int64_t best = s_min;
     double best_eff = 0.0;
     for (int64_t s = s_min; s <= 4 * s_min && kb / s >= 16; ++s) {
         const int64_t units = tiles * s;
-        const int64_t waves = (units + sms - 1) / sms;
-        const double eff = double(units) / double(waves * sms);
+        const int64_t waves = (units + slots - 1) / slots;
+        const double eff = double(units) / double(waves * slots);
         if (eff > best_eff + 0.02) {
             best_eff = eff;
             best = s;
         }
     }
     return int(best);
+}
+
+int plan_splits(const GemmProblem& g) {
+    const int bn = g.bn ? g.bn : choose_bn(g.N);
+    return choose_splits(g.M, g.N, g.K, num_sms(), bn, choose_cg(g, bn));
 }
 
 cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {

@@ -60,8 +60,11 @@ constexpr int kBK = 16;
 constexpr int kMaxChainKB = 256;
 
 int choose_bn(int64_t N);
-// number of k-blocks per split so that splits * tiles fill the machine
-int choose_splits(int64_t M, int64_t N, int64_t K, int num_sms, int bn);
+// split-K factor: at least the accuracy floor (chains <= kMaxChainKB k-blocks),
+// then the count whose (pair-)units fill the last wave best
+int choose_splits(int64_t M, int64_t N, int64_t K, int num_sms, int bn, int cg);
+// the same for a concrete problem (tile width and CTA-pair mode as run_gemm picks them)
+int plan_splits(const GemmProblem& g);
 
 cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream);
 
