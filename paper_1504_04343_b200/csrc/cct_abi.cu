@@ -351,17 +351,29 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
         const float* wv = weights_view(L, w, ws, st, &ldw, &e);
         CCT_TRY(e, "pad weights");
         const bool direct = (type == 3 && g.p == 0 && g.R == g.n && g.d % 4 == 0 && aligned16(dx));
-        float* dd = direct ? dx : ws.take(L.rows * L.ldc);
-        const int64_t ldd = direct ? g.d : L.ldc;
+        const bool slab = col2im_slab_layout(g, type);
+        const int64_t S = slab_stride(g);
+        const int64_t span = direct ? L.rows * g.d : slab ? g.b * g.m * g.k * S : L.rows * L.ldc;
+        float* dd = direct ? dx : ws.take(span);
+        const int64_t ldd = direct ? g.d : slab ? S : L.ldc;
         GemmProblem gp;
         gp.M = L.cols;
         gp.N = L.rows;
         gp.K = L.ncols;
         gp.A = {wv, ldw, Major::MN};
         gp.B = {drt, L.ldr, Major::MN};
-        gp.C.s_mr = 1;
-        gp.C.s_n = ldd;
-        cct_status s = gemm_capped(gp, dd, L.rows * ldd, ws, st, "gemm (bwd-data)");
+        if (slab) {  // column (i, j, ch) -> slab i; row (q, r, c) -> slab (q, r), run c
+            gp.C.mdiv = g.k * g.d;
+            gp.C.s_mq = S;
+            gp.C.s_mr = 1;
+            gp.C.ndiv = g.m;
+            gp.C.s_nq = g.k * S;
+            gp.C.s_n = g.k * g.d;
+        } else {
+            gp.C.s_mr = 1;
+            gp.C.s_n = ldd;
+        }
+        cct_status s = gemm_capped(gp, dd, span, ws, st, "gemm (bwd-data)");
         if (s != CCT_OK) return s;
         if (ws.base && !direct) CCT_TRY(col2im(g, type, dd, ldd, dx, st), "col2im");
         hi = std::max(hi, ws.off);

@@ -38,6 +38,8 @@ struct KParams {
     int passes;
     float* C;
     int64_t mdiv, s_mq, s_mr, s_n, s_split;
+    int ndiv;  // 0: column offset n * s_n; else (n / ndiv) * s_nq + (n % ndiv) * s_n
+    int64_t s_nq;
     // implicit (im2col) A: layer geometry
     int ic_d, ic_k, ic_s, ic_p, ic_m, ic_mm, ic_cpt;
 };
@@ -346,8 +348,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
                 }
                 ptx::tmem_ld_wait();
-                float* dst = p.C + off + int64_t(n0 + c0) * sn;
                 const int nlim = p.N - (n0 + c0);
+                if (p.ndiv) {
+                    // two-level column map (slab-major dDhat): walk (n / ndiv, n % ndiv)
+                    if (row_ok) {
+                        const int nq = (n0 + c0) / p.ndiv;
+                        int nr = (n0 + c0) - nq * p.ndiv;
+                        float* dst = p.C + off + int64_t(nq) * p.s_nq + int64_t(nr) * sn;
+                        const int64_t wrap = p.s_nq - int64_t(p.ndiv) * sn;
+                        if (nlim >= 32) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                *dst = __uint_as_float(v[j]);
+                                dst += sn;
+                                if (++nr == p.ndiv) { nr = 0; dst += wrap; }
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                if (j < nlim) *dst = __uint_as_float(v[j]);
+                                dst += sn;
+                                if (++nr == p.ndiv) { nr = 0; dst += wrap; }
+                            }
+                        }
+                    }
+                    continue;
+                }
+                float* dst = p.C + off + int64_t(n0 + c0) * sn;
                 if (row_ok && nlim >= 32 && sn == 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
                     // row-major output (lane = row): 32 consecutive floats per thread
                     float4* d4 = reinterpret_cast<float4*>(dst);
@@ -633,6 +660,8 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.s_mr = g.C.s_mr;
     kp.s_n = g.C.s_n;
     kp.s_split = g.C.s_split;
+    kp.ndiv = g.C.ndiv < (int64_t(1) << 31) ? int(g.C.ndiv) : 0;
+    kp.s_nq = g.C.s_nq;
 
     const int cg = choose_cg(g, bn);
     kp.num_m_tiles = int((g.M + kBM * cg - 1) / (kBM * cg));

@@ -19,12 +19,13 @@ struct Operand {
 };
 
 // Epilogue address map: element (row m, col n) of split s goes to
-//   ptr + (m / mdiv) * s_mq + (m % mdiv) * s_mr + n * s_n + s * s_split
+//   ptr + (m / mdiv) * s_mq + (m % mdiv) * s_mr + (n / ndiv) * s_nq + (n % ndiv) * s_n + s * s_split
 // (row = TMEM lane; s_mr == 1 gives fully coalesced stores).
 struct OutMap {
     float* ptr = nullptr;
     int64_t mdiv = INT64_MAX;
     int64_t s_mq = 0, s_mr = 1, s_n = 0, s_split = 0;
+    int64_t ndiv = INT64_MAX, s_nq = 0;
 };
 
 // Implicit Type 1 lowering: operand A is read straight from the NHWC input x

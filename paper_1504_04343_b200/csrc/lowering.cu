@@ -53,6 +53,11 @@ __device__ __forceinline__ void cp_async4(float* smem_dst, const float* gsrc) {
                  "l"(gsrc)
                  : "memory");
 }
+__device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst))),
+                 "l"(gsrc)
+                 : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 
 // One warp per lowered row (q, y, c).  The row is `nruns` runs of L source
@@ -344,22 +349,19 @@ __global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restr
     }
 }
 
-// col2im (Type 1): one CTA per input row (q, y).  The (r, i) pairs with
-// s*r + i == y + p contribute; for each, the k*d-float slice i of the m rows
-// (q, r, c) is staged in smem (async copies through a precomputed offset
-// table), then every dx element of the row sums its taps from smem using
-// per-element tap metadata built once.  Each dDhat element is read once.
-__global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t ld, float* __restrict__ dx, Geo g) {
-    extern __shared__ float sm[];
+// col2im (Type 1, small d): one CTA per input row (q, y).  dDhat arrives
+// slab-major (col2im_slab_layout): slab (q, r, i) = the m x k*d block of rows
+// (q, r, c) and filter row i, contiguous and 16-byte aligned (stride S floats),
+// as the backward-data GEMM epilogue writes it.  The (r, i) slabs with
+// s*r + i == y + p are staged with 16-byte async copies, then every dx element
+// of the row sums its taps from smem using per-element tap metadata built once.
+// Each dDhat element is read once.
+__global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t S, float* __restrict__ dx, Geo g) {
+    extern __shared__ __align__(16) float sm[];
     const int n = int(g.n), d = int(g.d), k = int(g.k), s = int(g.s), p = int(g.p), m = int(g.m);
-    const int kd = k * d, slab = m * kd;
+    const int kd = k * d;
     const int npair_max = (k + s - 1) / s;
-    int* stab = reinterpret_cast<int*>(sm + npair_max * slab);  // slab: staged float -> c*ld + rr
-    int* meta = stab + slab;                                     // n*d: tap run per output
-    for (int e = threadIdx.x; e < slab; e += blockDim.x) {
-        const int c = e / kd;
-        stab[e] = c * int(ld) + (e - c * kd);
-    }
+    int* meta = reinterpret_cast<int*>(sm + npair_max * S);  // n*d: tap run per output
     // per dx column element: slab offset of its first valid tap (c < m) and the
     // number of taps (j = j0 + t s, c = c0 - t, 0 <= c < m, j < k): branch-free sums
     for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
@@ -372,6 +374,7 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t ld, 
         meta[e] = off | (cnt << 24);                // off < 2^24 (slab <= 96 KiB)
     }
     const int64_t nqy = g.b * n;
+    const int S4 = int(S / 4);
     for (int64_t qy = blockIdx.x; qy < nqy; qy += gridDim.x) {
         const int yy = int(qy % n);
         const int64_t q = qy / n;
@@ -383,9 +386,9 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t ld, 
         __syncthreads();  // previous slabs consumed
         for (int a = 0; a < np; ++a) {
             const int r = rtop - a, i = py - s * r;
-            const float* src = dd + ((q * m + r) * int64_t(m)) * ld + int64_t(i) * kd;
-            float* dst = sm + a * slab;
-            for (int e = threadIdx.x; e < slab; e += blockDim.x) cp_async4(dst + e, src + stab[e]);
+            const float* src = dd + ((q * m + r) * int64_t(k) + i) * S;
+            float* dst = sm + a * S;
+            for (int e = threadIdx.x; e < S4; e += blockDim.x) cp_async16(dst + 4 * e, src + 4 * e);
         }
         cp_async_wait_all();
         __syncthreads();
@@ -396,7 +399,7 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t ld, 
             const int off = mt & 0xFFFFFF, cnt = mt >> 24;
             float acc = 0.f;
             for (int a = 0; a < np; ++a) {
-                const float* sl = sm + a * slab + off;
+                const float* sl = sm + a * S + off;
                 for (int t = 0; t < cnt; ++t) acc += sl[t * delta];
             }
             out[e] = acc;
@@ -525,26 +528,35 @@ cudaError_t expand(const Geo& g, int type, const float* dy, float* drt, int64_t 
     return cudaGetLastError();
 }
 
+bool col2im_slab_layout(const Geo& g, int type) {
+    if (type != 1 || g.d % 4 == 0 || g.d >= 256 || g.s >= 256) return false;
+    const int64_t S = slab_stride(g);
+    const int64_t npair = (g.k + g.s - 1) / g.s;
+    return (npair * S + g.n * g.d) * 4 <= 96 * 1024;
+}
+
+int64_t slab_stride(const Geo& g) { return rup4(g.m * g.k * g.d); }
+
 cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* dx, cudaStream_t st) {
     const int64_t rowsq = g.b * g.n;
     const int grid = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * 16));
     const RowMap rmi = rowmap_internal(g, type);
     PhaseScope ps(kPhaseCol2im, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + g.b * rmi.rpi * lowered_cols(g, type)));
-    const bool vec = g.d % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(dd) % 16 == 0) &&
-                     (reinterpret_cast<uintptr_t>(dx) % 16 == 0);
-    const size_t slab = size_t(g.m * g.k * g.d);
-    const size_t smem1 = (size_t((g.k + g.s - 1) / g.s) * slab + slab + size_t(g.n * g.d)) * 4;
-    if (type == 1 && !vec && g.d < 256 && g.s < 256 && smem1 <= 96 * 1024) {
+    if (col2im_slab_layout(g, type)) {  // ld = slab stride
+        if (ld != slab_stride(g) || reinterpret_cast<uintptr_t>(dd) % 16) return cudaErrorInvalidValue;
         static bool attr = false;
         if (!attr) {
             cudaFuncSetAttribute(col2im_t1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             attr = true;
         }
+        const size_t smem1 = size_t(((g.k + g.s - 1) / g.s) * ld + g.n * g.d) * 4;
         const int grid1 = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * 4));
         col2im_t1_smem_kernel<<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
         note_launch();
         return cudaGetLastError();
     }
+    const bool vec = g.d % 4 == 0 && ld % 4 == 0 && (reinterpret_cast<uintptr_t>(dd) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(dx) % 16 == 0);
     if (vec) col2im_kernel<4><<<grid, kThreads, 0, st>>>(dd, ld, dx, g, type);
     else col2im_kernel<1><<<grid, kThreads, 0, st>>>(dd, ld, dx, g, type);
     note_launch();

@@ -41,7 +41,13 @@ cudaError_t lift(const Geo& g, int type, const RowMap& rm, const float* rhat, in
                  float* y, cudaStream_t st);
 // dRhat^T[col*ldr + row], internal row order, zero where lift does not read
 cudaError_t expand(const Geo& g, int type, const float* dy, float* drt, int64_t ldr, cudaStream_t st);
-// dx from dDhat (internal order, row-major with ld); type 3 = crop of dXp
+// Small-channel Type 1 (d % 4 != 0, e.g. conv1): dDhat is produced slab-major --
+// slab (q, r, i) = rows (q, r, 0..m-1) x columns [i k d, (i+1) k d), contiguous,
+// slab stride slab_stride(g) floats -- so col2im stages whole slabs.
+bool col2im_slab_layout(const Geo& g, int type);
+int64_t slab_stride(const Geo& g);
+// dx from dDhat (internal order, row-major with ld -- or slab-major with ld = slab
+// stride when col2im_slab_layout); type 3 = crop of dXp
 cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* dx, cudaStream_t st);
 // dst[r*ld_dst + c] = src[r*ld_src + c] for c < cols, 0 for cols <= c < ld_dst
 cudaError_t pad_rows(const float* src, int64_t rows, int64_t cols, int64_t ld_src, float* dst,
