@@ -208,10 +208,14 @@ cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStr
     const int64_t kb = (gp.K + kBK - 1) / kBK;
     const int splits = int((kb + kMaxChainKB - 1) / kMaxChainKB);
     float* parts = splits > 1 ? ws.take(int64_t(splits) * span) : nullptr;
+    gp.splits = splits;
+    const size_t skb = gemm_workspace_bytes(gp);  // stream-K partial tiles
+    float* sk = skb ? ws.take(int64_t(skb / 4)) : nullptr;
     if (!ws.base) return CCT_OK;
+    gp.ws = sk;
+    gp.ws_bytes = skb;
     gp.C.ptr = splits > 1 ? parts : out;
     gp.C.s_split = span;
-    gp.splits = splits;
     CCT_TRY(run_gemm(gp, st), what);
     if (splits > 1) CCT_TRY(splitk_reduce(parts, span, splits, 1, span, span, out, span, st), "split-K reduce");
     return CCT_OK;

@@ -39,6 +39,12 @@ struct KParams {
     float* C;
     int64_t mdiv, s_mq, s_mr, s_n, s_split;
     int ndiv;  // 0: column offset n * s_n; else (n / ndiv) * s_nq + (n % ndiv) * s_n
+    // stream-K (sk_len > 0): CTA group g owns k-block iterations [g*sk_len, (g+1)*sk_len) of
+    // the flattened (tile, k-block) space; tiles cut between two groups are summed by
+    // whichever part finishes second, through sk_part / sk_cnt (see epilogue)
+    int sk_len;
+    float* sk_part;
+    int* sk_cnt;
     int64_t s_nq;
     // implicit (im2col) A: layer geometry
     int ic_d, ic_k, ic_s, ic_p, ic_m, ic_mm, ic_cpt;
@@ -112,6 +118,48 @@ __device__ __forceinline__ Pix pix_of(int idx, const KParams& p) {
     return x;
 }
 
+// One piece of work of a CTA group: output unit u (tile, m fastest, then n, then
+// split) over k-blocks [kb0, kb1).  kind 0: the whole unit; 1: leading part of a
+// stream-K tile (finished by the next group); 2: trailing part (begun by the
+// previous group).  Every warp role walks the same sequence.
+struct Work {
+    int u, kb0, kb1, kind;
+};
+struct WorkIter {
+    int next_u, it, end;
+    __device__ WorkIter(const KParams& p, int group) {
+        if (p.sk_len) {
+            it = group * p.sk_len;
+            end = min(it + p.sk_len, p.units * p.kb_total);
+            next_u = 0;
+        } else {
+            next_u = group;
+            it = end = 0;
+        }
+    }
+    __device__ bool next(const KParams& p, int ngroups, Work& w) {
+        if (p.sk_len) {
+            if (it >= end) return false;
+            w.u = it / p.kb_total;
+            const int lo = it - w.u * p.kb_total;
+            const int stop = min(end, (w.u + 1) * p.kb_total);
+            w.kb0 = lo;
+            w.kb1 = lo + (stop - it);
+            w.kind = (lo == 0 && w.kb1 == p.kb_total) ? 0 : (lo == 0 ? 1 : 2);
+            it = stop;
+            return true;
+        }
+        if (next_u >= p.units) return false;
+        w.u = next_u;
+        next_u += ngroups;
+        const int sp = w.u / (p.num_m_tiles * p.num_n_tiles);
+        w.kb0 = sp * p.kb_per_split;
+        w.kb1 = min(w.kb0 + p.kb_per_split, p.kb_total);
+        w.kind = 0;
+        return true;
+    }
+};
+
 template <int BN, int A_MN, int B_MN, int CG, int A_IM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -128,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tfull = empty + STAGES;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -166,15 +215,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            for (int u = group; u < p.units; u += ngroups) {
+            WorkIter wi(p, group);
+            Work w;
+            while (wi.next(p, ngroups, w)) {
+                const int u = w.u;
                 const int mt = u % p.num_m_tiles;
-                const int rest = u / p.num_m_tiles;
-                const int nt = rest % p.num_n_tiles;
-                const int sp = rest / p.num_n_tiles;
+                const int nt = (u / p.num_m_tiles) % p.num_n_tiles;
                 const int m0 = mt * (kBM * CG) + int(rank) * kBM;
                 const int n0 = nt * BN + int(rank) * BNL;
-                const int kb0 = sp * p.kb_per_split;
-                const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+                const int kb0 = w.kb0, kb1 = w.kb1;
                 // implicit lowering: the producer is one thread issuing every TMA of the
                 // CTA, so all im2col coordinates are per-tile constants or walked
                 // incrementally (no divisions inside the k-loop)
@@ -250,11 +299,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
-            for (int u = group; u < p.units; u += ngroups, ++local) {
-                const int rest = u / p.num_m_tiles;
-                const int sp = rest / p.num_n_tiles;
-                const int kb0 = sp * p.kb_per_split;
-                const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
+            WorkIter wi(p, group);
+            Work w;
+            for (; wi.next(p, ngroups, w); ++local) {
+                const int kb0 = w.kb0, kb1 = w.kb1;
                 const int acc = local & 1;
                 const uint32_t use = uint32_t(local >> 1);
                 ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
@@ -319,8 +367,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp >= 4 && warp < 8) {
         // ===================== epilogue (own TMEM lanes = own 128 rows) =====================
         const int q = warp & 3;
+        const int rit = q * 32 + lane;  // row within this CTA's 128-row tile
         int local = 0;
-        for (int u = group; u < p.units; u += ngroups, ++local) {
+        WorkIter wi(p, group);
+        Work w;
+        for (; wi.next(p, ngroups, w); ++local) {
+            const int u = w.u;
             const int mt = u % p.num_m_tiles;
             const int rest = u / p.num_m_tiles;
             const int nt = rest % p.num_n_tiles;
@@ -329,12 +381,57 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t use = uint32_t(local >> 1);
             ptx::mbar_wait(&tfull[acc], use & 1);
             ptx::tc_fence_after();
-            const int64_t row = int64_t(mt) * (kBM * CG) + int64_t(rank) * kBM + q * 32 + lane;
+            const int64_t row = int64_t(mt) * (kBM * CG) + int64_t(rank) * kBM + rit;
             const bool row_ok = row < p.M;
             int64_t off = 0;
             if (row_ok) off = (row / p.mdiv) * p.s_mq + (row % p.mdiv) * p.s_mr + int64_t(sp) * p.s_split;
             const int n0 = nt * BN;
-            const int64_t sn = p.s_n;
+            // final values of columns n0 + c0 .. +31 of this thread's row -> output map
+            auto store32 = [&](const uint32_t* v, int c0) {
+                const int64_t sn = p.s_n;
+                const int nlim = p.N - (n0 + c0);
+                if (!row_ok) return;
+                if (p.ndiv) {
+                    // two-level column map (slab-major dDhat): walk (n / ndiv, n % ndiv)
+                    const int nq = (n0 + c0) / p.ndiv;
+                    int nr = (n0 + c0) - nq * p.ndiv;
+                    float* dst = p.C + off + int64_t(nq) * p.s_nq + int64_t(nr) * sn;
+                    const int64_t wrap = p.s_nq - int64_t(p.ndiv) * sn;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (j < nlim) *dst = __uint_as_float(v[j]);
+                        dst += sn;
+                        if (++nr == p.ndiv) { nr = 0; dst += wrap; }
+                    }
+                    return;
+                }
+                float* dst = p.C + off + int64_t(n0 + c0) * sn;
+                if (nlim >= 32 && sn == 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+                    // row-major output (lane = row): 32 consecutive floats per thread
+                    float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                } else if (nlim >= 32) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        *dst = __uint_as_float(v[j]);
+                        dst += sn;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (j < nlim) *dst = __uint_as_float(v[j]);
+                        dst += sn;
+                    }
+                }
+            };
+            // stream-K part: this group's share of a tile cut at boundary `bnd` between
+            // groups bnd and bnd + 1 (part 0 = leading k-blocks, 1 = trailing)
+            const int bnd = (w.kind == 1) ? group : group - 1;
+            float* part = (w.kind == 0) ? nullptr
+                                        : p.sk_part + (int64_t((bnd * 2 + (w.kind - 1)) * CG + int(rank)) * BN) * kBM;
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t v[32];
@@ -348,52 +445,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
                 }
                 ptx::tmem_ld_wait();
-                const int nlim = p.N - (n0 + c0);
-                if (p.ndiv) {
-                    // two-level column map (slab-major dDhat): walk (n / ndiv, n % ndiv)
-                    if (row_ok) {
-                        const int nq = (n0 + c0) / p.ndiv;
-                        int nr = (n0 + c0) - nq * p.ndiv;
-                        float* dst = p.C + off + int64_t(nq) * p.s_nq + int64_t(nr) * sn;
-                        const int64_t wrap = p.s_nq - int64_t(p.ndiv) * sn;
-                        if (nlim >= 32) {
+                if (part) {
+                    // column-major partial tile: lanes (rows) coalesced
 #pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                *dst = __uint_as_float(v[j]);
-                                dst += sn;
-                                if (++nr == p.ndiv) { nr = 0; dst += wrap; }
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 32; ++j) {
-                                if (j < nlim) *dst = __uint_as_float(v[j]);
-                                dst += sn;
-                                if (++nr == p.ndiv) { nr = 0; dst += wrap; }
-                            }
-                        }
-                    }
-                    continue;
-                }
-                float* dst = p.C + off + int64_t(n0 + c0) * sn;
-                if (row_ok && nlim >= 32 && sn == 1 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-                    // row-major output (lane = row): 32 consecutive floats per thread
-                    float4* d4 = reinterpret_cast<float4*>(dst);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        d4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-                } else if (row_ok && nlim >= 32) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        *dst = __uint_as_float(v[j]);
-                        dst += sn;
-                    }
-                } else if (row_ok) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (j < nlim) *dst = __uint_as_float(v[j]);
-                        dst += sn;
-                    }
+                    for (int j = 0; j < 32; ++j) __stcg(part + (c0 + j) * kBM + rit, __uint_as_float(v[j]));
+                } else {
+                    store32(v, c0);
                 }
             }
             ptx::tc_fence_before();
@@ -402,18 +459,39 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if constexpr (CG == 1) ptx::mbar_arrive(&tempty[acc]);
                 else ptx::mbar_arrive_remote(tempty_leader + uint32_t(acc * 8));
             }
+            if (part) {
+                // second finisher of the two parts sums them (part 0 + part 1: the same
+                // result whichever group arrives last) and writes the tile
+                __threadfence();
+                ptx::named_bar_sync(1, 128);
+                if (rit == 0) *sk_flag = atomicAdd(p.sk_cnt + bnd * CG + int(rank), 1);
+                ptx::named_bar_sync(1, 128);
+                if (*sk_flag == 1) {
+                    __threadfence();
+                    const float* p0 = p.sk_part + (int64_t((bnd * 2) * CG + int(rank)) * BN) * kBM;
+                    const float* p1 = p0 + int64_t(CG) * BN * kBM;
+#pragma unroll 1
+                    for (int c0 = 0; c0 < BN; c0 += 32) {
+                        uint32_t v[32];
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            v[j] = __float_as_uint(__ldcg(p0 + (c0 + j) * kBM + rit) + __ldcg(p1 + (c0 + j) * kBM + rit));
+                        store32(v, c0);
+                    }
+                    if (rit == 0) p.sk_cnt[bnd * CG + int(rank)] = 0;  // ready for the next launch
+                }
+                ptx::named_bar_sync(1, 128);  // sk_flag reuse
+            }
         }
     } else if (warp >= 8) {
         // ===================== 3xTF32 transform (own tiles) =====================
         const int t = threadIdx.x - 256;
         int stage = 0;
         uint32_t phase = 0;
-        for (int u = group; u < p.units; u += ngroups) {
-            const int rest = u / p.num_m_tiles;
-            const int sp = rest / p.num_n_tiles;
-            const int kb0 = sp * p.kb_per_split;
-            const int kb1 = min(kb0 + p.kb_per_split, p.kb_total);
-            for (int kb = kb0; kb < kb1; ++kb) {
+        WorkIter wi(p, group);
+        Work w;
+        while (wi.next(p, ngroups, w)) {
+            for (int kb = w.kb0; kb < w.kb1; ++kb) {
                 ptx::mbar_wait(&full[stage], phase);
                 if (p.passes == 3) {
                     const uint32_t raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
@@ -537,7 +615,7 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& 
         attr_set = true;
     }
     const int sms = num_sms() / CG * CG;
-    const int grid = std::min(kp.units * CG, sms);
+    const int grid = kp.sk_len ? sms : std::min(kp.units * CG, sms);
     PhaseScope ps(kPhaseGemm, st, 2.0 * double(kp.M) * double(kp.N) * double(kp.K), 0);
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(unsigned(grid));
@@ -639,6 +717,42 @@ int plan_splits(const GemmProblem& g) {
     return choose_splits(g.M, g.N, g.K, num_sms(), bn, choose_cg(g, bn));
 }
 
+// Stream-K plan: used for an unsplit GEMM of at least one wave whose whole-tile
+// waves would leave >= 8% of the machine idle (e.g. 169 tiles on 74 CTA pairs).
+struct SkPlan {
+    int len = 0;             // k-block iterations per CTA group (0: data-parallel)
+    int64_t part_floats = 0;  // two partial tiles per group boundary
+    int64_t cnt_ints = 0;
+};
+
+SkPlan sk_plan(const GemmProblem& g) {
+    SkPlan sp;
+    static const int enabled = [] {
+        const char* e = getenv("CCT_STREAMK");
+        return e ? atoi(e) : 1;
+    }();
+    if (!enabled || g.splits > 1 || g.M <= 0 || g.N <= 0 || g.K <= 0) return sp;
+    const int bn = g.bn ? g.bn : choose_bn(g.N);
+    const int cg = choose_cg(g, bn);
+    const int64_t tiles = ((g.M + kBM * cg - 1) / (kBM * cg)) * ((g.N + bn - 1) / bn);
+    const int64_t slots = num_sms() / cg;
+    const int64_t kb = (g.K + kBK - 1) / kBK;
+    if (tiles < slots || kb < 4) return sp;
+    const int64_t waves = (tiles + slots - 1) / slots;
+    if (double(tiles) / double(waves * slots) >= 0.92) return sp;
+    const int64_t len = (tiles * kb + slots - 1) / slots;
+    if (len < kb || tiles * kb >= (int64_t(1) << 31)) return sp;  // each tile spans <= 2 groups
+    sp.len = int(len);
+    sp.part_floats = slots * 2 * cg * int64_t(bn) * kBM;
+    sp.cnt_ints = slots * cg;
+    return sp;
+}
+
+size_t gemm_workspace_bytes(const GemmProblem& g) {
+    const SkPlan sp = sk_plan(g);
+    return sp.len ? size_t(sp.part_floats) * 4 + size_t(sp.cnt_ints) * 4 + 256 : 0;
+}
+
 cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
     const int bn = g.bn ? g.bn : choose_bn(g.N);
@@ -666,6 +780,17 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     const int cg = choose_cg(g, bn);
     kp.num_m_tiles = int((g.M + kBM * cg - 1) / (kBM * cg));
     kp.units = kp.num_m_tiles * kp.num_n_tiles * kp.splits;
+    if (g.ws) {
+        const SkPlan sp = sk_plan(g);
+        if (sp.len && kp.splits == 1 && g.ws_bytes >= gemm_workspace_bytes(g)) {
+            char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(g.ws) + 255) & ~uintptr_t(255));
+            kp.sk_part = reinterpret_cast<float*>(base);
+            kp.sk_cnt = reinterpret_cast<int*>(base + sp.part_floats * 4);
+            cudaError_t e = cudaMemsetAsync(kp.sk_cnt, 0, size_t(sp.cnt_ints) * 4, stream);
+            if (e != cudaSuccess) return e;
+            kp.sk_len = sp.len;
+        }
+    }
     CUtensorMap ta, tb;
     if (g.im2col.x) {
         const Im2col& ic = g.im2col;

@@ -48,7 +48,14 @@ struct GemmProblem {
     int passes = 3;  // 3 = 3xTF32 (fp32-accurate), 1 = plain TF32 (diagnostic only)
     int bn = 0;      // 0 = choose
     Im2col im2col;   // implicit lowering of A (Type 1)
+    // scratch for stream-K partial tiles (gemm_workspace_bytes); without it the
+    // kernel runs data-parallel whole tiles
+    void* ws = nullptr;
+    size_t ws_bytes = 0;
 };
+
+// scratch run_gemm can use for this problem (0: none needed)
+size_t gemm_workspace_bytes(const GemmProblem& g);
 
 // Can this layer use the implicit (im2col) A operand?  fwd needs d % 16 == 0,
 // backward-weight d % 32 == 0 (one TMA box never straddles a filter tap).

@@ -35,6 +35,11 @@ __device__ __forceinline__ void sts128(uint32_t addr, float4 v) {
 }
 
 // ---- mbarrier ---------------------------------------------------------------
+// barrier among a subset of warps (id 1..15; `threads` a multiple of 32)
+__device__ __forceinline__ void named_bar_sync(int id, int threads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
 }
