@@ -391,14 +391,24 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
         CCT_TRY(e, "lower");
         const int64_t ldd = (dh == x) ? g.d : L.ldc;
         GemmProblem gp = wgrad_problem(L, {dh, ldd, Major::MN}, {drt, L.ldr, Major::K});
+        // narrow kernel banks (ncols < 128, e.g. conv1 o = 96) with a materialised Dhat:
+        // compute dW (ncols x cols) = dRhat^T * Dhat instead, so the wide lowered side
+        // is the tile width N
+        const bool swap = !implicit && L.ncols < 128 && L.cols >= 192;
+        if (swap) {
+            gp.M = L.ncols;
+            gp.N = L.cols;
+            gp.A = {drt, L.ldr, Major::K};
+            gp.B = {dh, ldd, Major::MN};
+        }
         if (implicit) gp.im2col = im2col_of(g, x);
         const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
         if (ws.base) {
             gp.C.ptr = parts;
-            gp.C.s_mr = 1;
-            gp.C.s_n = L.cols;
+            gp.C.s_mr = swap ? L.cols : 1;
+            gp.C.s_n = swap ? 1 : L.cols;
             gp.C.s_split = wsize;
             gp.splits = splits;
             CCT_TRY(run_gemm(gp, st), "gemm (bwd-weight)");

@@ -160,13 +160,21 @@ struct WorkIter {
     }
 };
 
-template <int BN, int A_MN, int B_MN, int CG, int A_IM>
+// A_TM: narrow tiles keep the A operand in TMEM (tcgen05.mma A-from-TMEM): the
+// transform warps read each A row once from smem and write its big / small parts
+// to a 4-slot TMEM ring, so the three MMAs of a K step read only B from shared
+// memory (for N <= 96 the A reads otherwise saturate the smem bus, ncu).
+template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const KParams p) {
     using C_ = Cfg<BN, CG>;
     constexpr int STAGES = C_::STAGES;
     constexpr int BNL = C_::BNL;
+    constexpr int kASlots = 4;                                        // TMEM ring of A tiles
+    constexpr uint32_t A_COL = uint32_t(2 * C_::NACC * BN);           // first A column
+    constexpr uint32_t TMEM_COLS = A_TM ? 512u : C_::TMEM_COLS;
+    static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots), "A_TM config");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align inside the shared window without leaving the shared address space
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         ptx::fence_barrier_init();
     }
-    if (warp == 2) ptx::tmem_alloc<C_::TMEM_COLS, CG>(tmem_slot);
+    if (warp == 2) ptx::tmem_alloc<TMEM_COLS, CG>(tmem_slot);
     ptx::tc_fence_before();
     if constexpr (CG == 2) ptx::cluster_sync();
     else __syncthreads();
@@ -299,6 +307,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
+            uint32_t gi = 0;  // k-blocks issued by this CTA (A_TM slot = gi % kASlots)
             WorkIter wi(p, group);
             Work w;
             for (; wi.next(p, ngroups, w); ++local) {
@@ -312,7 +321,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (CG == 1) ptx::mma_tf32(d, a, b, idesc, accumulate);
                     else ptx::mma_tf32_cg2(d, a, b, idesc, accumulate);
                 };
-                for (int kb = kb0; kb < kb1; ++kb) {
+                auto mma_ts = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t accumulate) {
+                    if constexpr (CG == 1) ptx::mma_tf32_ts(d, a, b, idesc, accumulate);
+                    else ptx::mma_tf32_ts_cg2(d, a, b, idesc, accumulate);
+                };
+                for (int kb = kb0; kb < kb1; ++kb, ++gi) {
                     // tdone implies the raw tiles of every CTA in the group landed
                     // (each transform warp waited on its own CTA's full barrier)
                     ptx::mbar_wait(&tdone[stage], phase);
@@ -321,7 +334,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_raw = a_raw + C_::A_BYTES;
                     const uint32_t a_sml = a_raw + C_::RAW_BYTES;
                     const uint32_t b_sml = b_raw + C_::RAW_BYTES;
-                    if constexpr (C_::NACC == 1) {
+                    if constexpr (A_TM) {
+                        // A big | small for this k-block in TMEM slot gi % kASlots (16 + 16 columns)
+                        const uint32_t a_big = tmem_base + A_COL + (gi % kASlots) * (2 * kBK);
+                        const uint32_t a_small = a_big + kBK;
+                        const uint32_t first = (kb > kb0) ? 1u : 0u;
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk)
+                            mma_ts(d_tmem + kk * BN, a_small + kk * 8, tile_desc<B_MN>(b_raw, kk), first);
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk)
+                            mma_ts(d_tmem + kk * BN, a_big + kk * 8, tile_desc<B_MN>(b_sml, kk), 1u);
+#pragma unroll
+                        for (int kk = 0; kk < 2; ++kk)
+                            mma_ts(d_tmem + kk * BN, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
+                    } else if constexpr (C_::NACC == 1) {
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk) {
                             const uint64_t ad = tile_desc<A_MN>(a_raw, kk);
@@ -488,13 +515,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int t = threadIdx.x - 256;
         int stage = 0;
         uint32_t phase = 0;
+        uint32_t gi = 0;
         WorkIter wi(p, group);
         Work w;
         while (wi.next(p, ngroups, w)) {
-            for (int kb = w.kb0; kb < w.kb1; ++kb) {
+            for (int kb = w.kb0; kb < w.kb1; ++kb, ++gi) {
                 ptx::mbar_wait(&full[stage], phase);
-                if (p.passes == 3) {
-                    const uint32_t raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
+                const uint32_t raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
+                if constexpr (A_TM) {
+                    // the MMAs of k-block gi - kASlots (same TMEM slot) must be complete
+                    if (gi >= kASlots) {
+                        const uint32_t g2 = gi - kASlots;
+                        ptx::mbar_wait(&empty[g2 % STAGES], (g2 / STAGES) & 1);
+                    }
+                    // row r of the K-major SWIZZLE_64B A tile: 16-byte chunk c at (c ^ (r/2 % 4))
+                    const int r = (warp & 3) * 32 + lane;
+                    uint32_t v[32];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const float4 x = ptx::lds128(raw + r * 64 + ((c ^ ((r >> 1) & 3)) << 4));
+                        const float4 sm = small_part(x);
+                        v[4 * c + 0] = __float_as_uint(x.x) & 0xFFFFE000u;
+                        v[4 * c + 1] = __float_as_uint(x.y) & 0xFFFFE000u;
+                        v[4 * c + 2] = __float_as_uint(x.z) & 0xFFFFE000u;
+                        v[4 * c + 3] = __float_as_uint(x.w) & 0xFFFFE000u;
+                        v[16 + 4 * c + 0] = __float_as_uint(sm.x);
+                        v[16 + 4 * c + 1] = __float_as_uint(sm.y);
+                        v[16 + 4 * c + 2] = __float_as_uint(sm.z);
+                        v[16 + 4 * c + 3] = __float_as_uint(sm.w);
+                    }
+                    ptx::tmem_st_32x32b_x32(tmem_base + (uint32_t((warp & 3) * 32) << 16) + A_COL +
+                                                (gi % kASlots) * (2 * kBK),
+                                            v);
+                    ptx::tmem_st_wait();
+                    // B small part in smem as usual
+                    constexpr int b0 = C_::A_BYTES / 16, b1 = C_::RAW_BYTES / 16;
+                    for (int i = b0 + t; i < b1; i += 32 * kTransformWarps) {
+                        const float4 x = ptx::lds128(raw + i * 16);
+                        ptx::sts128(raw + C_::RAW_BYTES + i * 16, small_part(x));
+                    }
+                    ptx::fence_proxy_async_smem();
+                    ptx::tc_fence_before();
+                } else if (p.passes == 3) {
                     constexpr int n4 = C_::RAW_BYTES / 16;
 #pragma unroll 4
                     for (int i = t; i < n4; i += 32 * kTransformWarps) {
@@ -518,7 +580,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     else __syncthreads();
     if (warp == 2) {
         ptx::tc_fence_after();
-        ptx::tmem_dealloc<C_::TMEM_COLS, CG>(tmem_base);
+        ptx::tmem_dealloc<TMEM_COLS, CG>(tmem_base);
     }
 }
 
@@ -604,10 +666,10 @@ bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major) {
     return true;
 }
 
-template <int BN, int A_MN, int B_MN, int CG, int A_IM>
+template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, cudaStream_t st) {
     using C_ = Cfg<BN, CG>;
-    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM>;
+    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM, A_TM>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
@@ -635,10 +697,24 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& 
     return cudaGetLastError();
 }
 
+bool a_in_tmem_enabled() {
+    static const int v = [] {  // $CCT_A_TMEM=0 keeps narrow tiles on the smem-A path (A/B)
+        const char* e = getenv("CCT_A_TMEM");
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
 template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
+    if constexpr (BN <= 96) {
+        if (!amn && g.passes == 3 && a_in_tmem_enabled()) {
+            if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 1>(ta, tb, kp, st);
+            return bmn ? launch<BN, 0, 1, CG, 0, 1>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 1>(ta, tb, kp, st);
+        }
+    }
     if (g.im2col.x) {  // implicit Type 1: forward / backward-data (K, K), backward-weight (MN, K|MN)
         if (!amn && !bmn) return launch<BN, 0, 0, CG, 1>(ta, tb, kp, st);
         if (amn && !bmn) return launch<BN, 1, 0, CG, 1>(ta, tb, kp, st);

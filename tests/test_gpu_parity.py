@@ -320,8 +320,8 @@ def test_batch_chunking_under_workspace_limit(cct, dev, t):
                                    ("s2p1", 15, 3, 32, 40, 2, 1), ("ragged", 14, 4, 64, 48, 3, 2)],
                          ids=lambda l: l[0])
 def test_implicit_lowering_matches_materialised(cct, dev, orc, layer):
-    """Implicit Type 1 (TMA im2col operands, no Dhat in HBM) == materialised Type 1,
-    bit for bit (same K order, same GEMM), and both match the oracle."""
+    """Implicit Type 1 (TMA im2col operands, no Dhat in HBM) == materialised Type 1:
+    forward bit for bit (same K order, same GEMM); both match the oracle."""
     from paper_1504_04343_b200 import conv
     L = cct.lib()
     _, n, k, d, o, s, p = layer
@@ -345,7 +345,10 @@ def test_implicit_lowering_matches_materialised(cct, dev, orc, layer):
     finally:
         L.cct_set_implicit_lowering(old)
     assert torch.equal(yi, ym) and torch.equal(yc, ym)
-    assert torch.equal(dwi, dwm) and torch.equal(dwc, dwm)
+    assert torch.equal(dwc, dwi)
+    # materialised bwd-weight of a narrow bank (o < 128) runs in the swapped
+    # orientation (dW = dRhat^T Dhat): same products, different rounding
+    assert float(torch.linalg.norm(dwi - dwm) / torch.linalg.norm(dwm)) < 2e-5
     assert rel_l2(yi.cpu().numpy().ravel(), orc.conv_fwd(x_np, w_np, b, n, d, k, o, s, p)) <= TOL
     assert rel_l2(dwi.cpu().numpy().ravel(), orc.conv_bwd_weight(x_np, dy_np, b, n, d, k, o, s, p)) <= TOL
 
