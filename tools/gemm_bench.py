@@ -58,11 +58,15 @@ def run(M, N, K, amaj, bmaj, passes, bn=0, reps=10, cmaj=0):
 
 
 def rate_table(reps=5):
-    """GEMM rate vs tile width N and reduction length K (cost-model calibration)."""
+    """Steady-state GEMM rate vs tile width N and reduction length K (cost-model
+    calibration): M large enough for >= 16 tiles per CTA pair, so pipeline fill and
+    the last wave are a small part of the time (the model adds those separately)."""
     out = {}
     for N in (64, 96, 128, 192, 256, 384, 1024):
         for K in (64, 256, 1024, 4096):
-            M = 65536 if N < 1024 else 16384
+            M = 524288 if N < 1024 else 131072
+            if K == 4096:
+                M //= 4
             ms, tf = run(M, N, K, 0, 0, 3, 0, reps, cmaj=1)
             out[f"{N},{K}"] = tf
             print(f"rate N={N:5d} K={K:5d}: {tf:6.1f} TF/s", flush=True)
