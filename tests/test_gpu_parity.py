@@ -216,6 +216,38 @@ def test_wgrad_full_batch_vs_fp64_gemm(cct, dev):
     assert err <= TOL, err
 
 
+@pytest.mark.parametrize("layer", [("conv3", 13, 3, 256, 384, 1, 1), ("conv5", 13, 3, 384, 256, 1, 1),
+                                   ("conv1", 227, 11, 3, 96, 4, 0)], ids=lambda l: l[0])
+def test_caffenet_b256_vs_fp64(cct, dev, layer):
+    """Full-batch (b = 256) training step of CaffeNet layers exactly as the bench runs it
+    (auto lowering: implicit Type 1 incl. implicit backward-data, stream-K GEMMs for the
+    ragged last wave, A-in-TMEM narrow tiles, slab-major col2im) against fp64 torch
+    convolutions on the GPU (checker only)."""
+    import torch.nn.functional as F
+    from paper_1504_04343_b200 import conv
+    _, n, k, d, o, s, p = layer
+    b = 256 if n < 100 else 32
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    t = cct.select_lowering(desc, 3)[0]
+    g = torch.Generator(device=dev).manual_seed(17)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    dy = torch.rand((b, o, desc.m, desc.m), generator=g, device=dev) * 2 - 1
+    cache = conv.alloc_cache(desc, t, dev)
+    y = conv.conv_fwd_cached(x, w, desc, t, cache=cache)
+    dx, dw = conv.conv_bwd(dy, w, desc, t, x=x, cache=cache)
+    xd = x.double().permute(0, 3, 1, 2).contiguous()
+    wd = w.double().permute(0, 3, 1, 2).contiguous()
+    dyd = dy.double()
+    ry = F.conv2d(xd, wd, stride=s, padding=p)
+    rdx = torch.nn.grad.conv2d_input(xd.shape, wd, dyd, stride=s, padding=p).permute(0, 2, 3, 1)
+    rdw = torch.nn.grad.conv2d_weight(xd, wd.shape, dyd, stride=s, padding=p).permute(0, 2, 3, 1)
+
+    def rel(a, r):
+        return float(torch.linalg.norm(a.double() - r) / torch.linalg.norm(r))
+    assert rel(y, ry) <= TOL and rel(dx, rdx) <= TOL and rel(dw, rdw) <= TOL, (rel(y, ry), rel(dx, rdx), rel(dw, rdw))
+
+
 # ------------------------------------------------------------- error behaviour
 def test_misaligned_pointer_is_config_error(cct, dev):
     from paper_1504_04343_b200 import conv
