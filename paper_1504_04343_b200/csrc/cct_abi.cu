@@ -19,6 +19,7 @@
 #include "gemm.cuh"
 #include "lowering.cuh"
 #include "reduce.cuh"
+#include "s2d.cuh"
 
 namespace cct {
 uint64_t launch_count();
@@ -143,10 +144,62 @@ bool implicit_enabled() {
     return g_implicit != 0;
 }
 
-// Type 1 with d % 32 == 0 runs forward and backward-weight on the input itself.
+// Type 1 with d % 16 == 0 runs forward and backward-weight on the input itself.
 bool t1_implicit(const Geo& g, int type, const float* x) {
     return implicit_enabled() && type == 1 && im2col_ok(g.d, true) && x && aligned16(x) &&
            g.n * g.n * g.d * g.b < (int64_t(1) << 40) && g.b * g.m * g.m < (int64_t(1) << 31);
+}
+
+// A strided Type 1 layer whose blocked depth s^2 d is a multiple of 16 runs in
+// space-to-depth form (s2d.cuh): the implicit stride-1 GEMMs on X' (CaffeNet
+// conv1: 3 x 3 taps of depth 48).  $CCT_S2D=0 keeps the materialised path.
+// Whether that form is used is the cost model's call per pass (prefer_s2d): the
+// entry points set the pass context (0 fwd, 1 bwd-data, 2 bwd-weight, 3 training
+// step: cct_conv_fwd_cached + cct_conv_bwd, whose lowered cache must agree).
+thread_local int t_pass = 3;
+struct PassCtx {
+    int old;
+    explicit PassCtx(int p) : old(t_pass) { t_pass = p; }
+    ~PassCtx() { t_pass = old; }
+};
+
+}  // namespace
+namespace cct {
+bool prefer_s2d(const cct_conv_desc* desc, int pass);  // cost_model.cpp
+}  // namespace cct
+namespace {
+
+bool t1_s2d(const Geo& g, int type) {
+    static const int env = [] {
+        const char* e = getenv("CCT_S2D");
+        return e ? atoi(e) : 1;
+    }();
+    if (!(env && implicit_enabled() && type == 1 && g.s > 1)) return false;
+    const Geo v = s2d_geo(g);
+    if (!(im2col_ok(v.d, false) && v.b * v.n * v.n * v.d < (int64_t(1) << 40) && v.b * v.n * v.n < (int64_t(1) << 31)))
+        return false;
+    if (env == 2) return true;  // $CCT_S2D=2: always (profiling)
+    cct_conv_desc d{};
+    d.n = g.n; d.k = g.k; d.d = g.d; d.o = g.o; d.b = g.b; d.stride = g.s; d.pad = g.p;
+    return prefer_s2d(&d, t_pass);
+}
+
+// planning runs (no workspace) still need non-null, aligned operand pointers so
+// they follow the same decisions as the real call
+const float* kPlanPtr = reinterpret_cast<const float*>(uintptr_t(256));
+template <class T>
+T* or_plan(T* p, const Ws& ws) {
+    return ws.base ? p : const_cast<T*>(reinterpret_cast<const T*>(kPlanPtr));
+}
+
+// floats per image of the forward's lowered cache (the blocked input X' in s2d form)
+int64_t cache_per_image(const Geo& g, int type) {
+    if (t1_s2d(g, type)) {
+        const Geo v = s2d_geo(g);
+        return v.n * v.n * v.d;
+    }
+    const RowMap rm = rowmap_internal(g, type);
+    return rm.rpi * rup4(lowered_cols(g, type));
 }
 
 }  // namespace
@@ -221,6 +274,21 @@ cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStr
     return CCT_OK;
 }
 
+// implicit backward-weight: A = im2col(x)^T (MN-major).  Its 32-channel boxes
+// need taps padded to dk = d rounded up to 32: M = k^2 dk, and rows (tap, ch >= d)
+// -- zeros read past the channel extent -- are not stored.
+void wgrad_im2col(GemmProblem& gp, const Geo& g, const float* x) {
+    gp.im2col = im2col_of(g, x);
+    const int64_t dk = im2col_dk(g.d, true);
+    gp.im2col.dk = dk;
+    if (dk != g.d) {
+        gp.M = g.k * g.k * dk;
+        gp.C.mdiv = dk;
+        gp.C.s_mq = g.d;
+        gp.C.mlim = g.d;
+    }
+}
+
 // backward-weight GEMM: dW^T (cols x ncols) = Dhat^T * dRhat, reduction over rows
 GemmProblem wgrad_problem(const Lowered& L, Operand a, Operand b) {
     GemmProblem gp;
@@ -238,6 +306,17 @@ GemmProblem wgrad_problem(const Lowered& L, Operand a, Operand b) {
 
 cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
                        cudaStream_t st) {
+    if (t1_s2d(g, type)) {
+        // blocked input (kept in the caller's lowered cache when given) and kernel bank
+        const Geo v = s2d_geo(g);
+        float* xs = cache ? cache : ws.take(v.b * v.n * v.n * v.d);
+        float* wsd = ws.take(v.o * v.k * v.k * v.d);
+        if (ws.base) {
+            CCT_TRY(s2d_input(g, x, xs, st), "space-to-depth (x)");
+            CCT_TRY(s2d_weights(g, w, wsd, st), "space-to-depth (w)");
+        }
+        return run_fwd_one(v, 1, or_plan(xs, ws), or_plan(wsd, ws), y, nullptr, ws, st);
+    }
     const Lowered L = lowered_of(g, type);
     cudaError_t e = cudaSuccess;
     int64_t ldw;
@@ -321,7 +400,7 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
         const float* dh = implicit ? nullptr : cache ? cache : dhat_of(g, 1, L, x, nullptr, ws, st, &e);
         CCT_TRY(e, "lower");
         GemmProblem gp = wgrad_problem(L, {dh, L.ldc, Major::MN}, {dyn, g.o, Major::MN});
-        if (implicit) gp.im2col = im2col_of(g, x);
+        if (implicit) wgrad_im2col(gp, g, x);
         const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
@@ -343,6 +422,33 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
 
 cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
                        float* dx, float* dw, Ws& ws, cudaStream_t st) {
+    if (t1_s2d(g, type)) {
+        // the stride-1 backward of the blocked layer, then the depth-to-space gathers
+        const Geo v = s2d_geo(g);
+        const float* xs = nullptr;
+        float *wsd = nullptr, *dxs = nullptr, *dws = nullptr;
+        if (dw) {
+            if (cache) {
+                xs = cache;
+            } else {
+                float* t = ws.take(v.b * v.n * v.n * v.d);
+                if (ws.base) CCT_TRY(s2d_input(g, x, t, st), "space-to-depth (x)");
+                xs = t;
+            }
+            dws = ws.take(v.o * v.k * v.k * v.d);
+        }
+        if (dx) {
+            wsd = ws.take(v.o * v.k * v.k * v.d);
+            dxs = ws.take(v.b * v.n * v.n * v.d);
+            if (ws.base) CCT_TRY(s2d_weights(g, w, wsd, st), "space-to-depth (w)");
+        }
+        cct_status s = run_bwd_one(v, 1, dw ? or_plan(xs, ws) : nullptr, nullptr, dy, dx ? or_plan(wsd, ws) : nullptr,
+                                   dx ? or_plan(dxs, ws) : nullptr, dw ? or_plan(dws, ws) : nullptr, ws, st);
+        if (s != CCT_OK || !ws.base) return s;
+        if (dx) CCT_TRY(d2s_input(g, dxs, dx, st), "depth-to-space (dx)");
+        if (dw) CCT_TRY(d2s_weights(g, dws, dw, st), "depth-to-space (dw)");
+        return CCT_OK;
+    }
     if (t1_implicit_bwd(g, type)) return run_bwd_implicit(g, x, cache, dy, w, dx, dw, ws, st);
     const Lowered L = lowered_of(g, type);
     cudaError_t e = cudaSuccess;
@@ -401,7 +507,7 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
             gp.A = {drt, L.ldr, Major::K};
             gp.B = {dh, ldd, Major::MN};
         }
-        if (implicit) gp.im2col = im2col_of(g, x);
+        if (implicit) wgrad_im2col(gp, g, x);
         const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
@@ -469,8 +575,7 @@ cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float
                    cudaStream_t st) {
     const int64_t cb = chunk_images(g, type, CCT_PASS_FWD);
     if (cb == g.b) return run_fwd_one(g, type, x, w, y, cache, ws, st);
-    const Lowered L = lowered_of(g, type);
-    const int64_t per_x = g.n * g.n * g.d, per_y = g.o * g.m * g.m, per_c = L.rm.rpi * L.ldc;
+    const int64_t per_x = g.n * g.n * g.d, per_y = g.o * g.m * g.m, per_c = cache_per_image(g, type);
     const size_t base = ws.off;
     size_t hi = base;
     for (int64_t q0 = 0; q0 < g.b; q0 += cb) {
@@ -491,8 +596,7 @@ cct_status run_bwd(const Geo& g, int type, const float* x, const float* cache, c
     const int pass = dx && dw ? CCT_PASS_BWD : dx ? CCT_PASS_BWD_DATA : CCT_PASS_BWD_WEIGHT;
     const int64_t cb = chunk_images(g, type, pass);
     if (cb == g.b) return run_bwd_one(g, type, x, cache, dy, w, dx, dw, ws, st);
-    const Lowered L = lowered_of(g, type);
-    const int64_t per_x = g.n * g.n * g.d, per_y = g.o * g.m * g.m, per_c = L.rm.rpi * L.ldc;
+    const int64_t per_x = g.n * g.n * g.d, per_y = g.o * g.m * g.m, per_c = cache_per_image(g, type);
     const int64_t nchunks = (g.b + cb - 1) / cb;
     const int64_t wsize = g.o * g.k * g.k * g.d;
     float* parts = dw ? ws.take(nchunks * wsize) : nullptr;  // per-chunk dW, reduced at the end
@@ -556,18 +660,26 @@ cct_status cct_workspace_size(const cct_conv_desc* desc, cct_lowering lowering, 
     if (!bytes) return fail(CCT_ERR_CONFIG, "null size pointer");
     const Geo g = geo_of(desc);
     const int type = resolve(desc, lowering, pass);
-    Ws ws(nullptr);
+    if (int(pass) < CCT_PASS_FWD || int(pass) > CCT_PASS_BWD) return fail(CCT_ERR_CONFIG, "unknown pass");
     // dummy, 16-byte aligned non-null pointers so zero-copy decisions match the real call
     const float* dummy = reinterpret_cast<const float*>(uintptr_t(256));
     float* dout = reinterpret_cast<float*>(uintptr_t(256));
-    switch (int(pass)) {
-    case CCT_PASS_FWD: s = run_fwd(g, type, dummy, dummy, nullptr, nullptr, ws, nullptr); break;
-    case CCT_PASS_BWD_DATA: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, dout, nullptr, ws, nullptr); break;
-    case CCT_PASS_BWD_WEIGHT: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, nullptr, dout, ws, nullptr); break;
-    case CCT_PASS_BWD: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, dout, dout, ws, nullptr); break;
-    default: return fail(CCT_ERR_CONFIG, "unknown pass");
+    // the size covers the pass both stand-alone and inside a training step (the
+    // two may pick different forms of a strided layer, t1_s2d)
+    size_t most = 0;
+    for (int ctx : {int(pass) == CCT_PASS_BWD ? 3 : int(pass), 3}) {
+        PassCtx pc(ctx);
+        Ws ws(nullptr);
+        switch (int(pass)) {
+        case CCT_PASS_FWD: s = run_fwd(g, type, dummy, dummy, nullptr, nullptr, ws, nullptr); break;
+        case CCT_PASS_BWD_DATA: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, dout, nullptr, ws, nullptr); break;
+        case CCT_PASS_BWD_WEIGHT: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, nullptr, dout, ws, nullptr); break;
+        default: s = run_bwd(g, type, dummy, nullptr, dummy, dummy, dout, dout, ws, nullptr); break;
+        }
+        if (s != CCT_OK) return s;
+        most = std::max(most, ws.off);
     }
-    *bytes = ws.off + 256;
+    *bytes = most + 256;
     return s;
 }
 
@@ -589,6 +701,7 @@ static cct_status run_pass(const cct_conv_desc* desc, cct_lowering lowering, cct
     const int type = resolve(desc, lowering, pass);
     Ws ws(wsp);
     cudaStream_t st = as_stream(stream);
+    PassCtx pc(int(pass));
     switch (pass) {
     case CCT_PASS_FWD: return run_fwd(g, type, a, b, out, nullptr, ws, st);
     case CCT_PASS_BWD_DATA: return run_bwd(g, type, nullptr, nullptr, a, b, out, nullptr, ws, st);
@@ -623,10 +736,11 @@ cct_status cct_lowered_cache_size(const cct_conv_desc* desc, cct_lowering loweri
     if (!bytes) return fail(CCT_ERR_CONFIG, "null size pointer");
     const Geo g = geo_of(desc);
     const int type = resolve_train(desc, lowering);
-    const Lowered L = lowered_of(g, type);
+    PassCtx pc(3);
     const float* aligned = reinterpret_cast<const float*>(uintptr_t(256));
-    *bytes = (dhat_is_input(g, type, aligned) || t1_implicit(g, type, aligned)) ? 0
-                                                                             : size_t(L.rows * L.ldc) * sizeof(float);
+    *bytes = (!t1_s2d(g, type) && (dhat_is_input(g, type, aligned) || t1_implicit(g, type, aligned)))
+                 ? 0
+                 : size_t(g.b * cache_per_image(g, type)) * sizeof(float);
     return CCT_OK;
 }
 
@@ -645,6 +759,7 @@ cct_status cct_conv_fwd_cached(const cct_conv_desc* desc, cct_lowering lowering,
     if (cache && cache_bytes < cneed) return fail(CCT_ERR_RESOURCE, "lowered cache too small for " + desc_str(desc));
     if (!wsp || ws_bytes < need) return fail(CCT_ERR_RESOURCE, "workspace too small for " + desc_str(desc));
     Ws ws(wsp);
+    PassCtx pc(3);
     return run_fwd(geo_of(desc), type, x, w, y, cneed ? cache : nullptr, ws, as_stream(stream));
 }
 
@@ -668,6 +783,7 @@ cct_status cct_conv_bwd(const cct_conv_desc* desc, cct_lowering lowering, const 
     // a cache is only meaningful when Dhat is not the input itself
     const float* c = (cache && !(x && dhat_is_input(g, type, x))) ? cache : nullptr;
     if (dw && !x && !c) return fail(CCT_ERR_CONFIG, "bwd-weight needs x for this lowering");
+    PassCtx pc(3);
     return run_bwd(g, type, x, c, dy, w, dx, dw, ws, as_stream(stream));
 }
 

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "cct.h"
 
@@ -124,9 +125,58 @@ double dgrad_seconds(const G& g, bool implicit, double rows, double cols, double
     return t;
 }
 
-// counts + model for one pass.  pass: 0 fwd, 1 bwd-data, 2 bwd-weight
-void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* secs, double* bytes) {
+// Strided Type 1 layers with s^2 d % 16 == 0 run in space-to-depth form
+// (s2d.cuh, cct_abi.cu t1_s2d): the stride-1 layer of side m + k' - 1, k' = ceil(k/s)
+// taps, depth s^2 d, plus the blocking / unblocking passes.
+bool s2d_possible(const G& g) {
+    const char* e = getenv("CCT_S2D");
+    return (!e || atoi(e) != 0) && cct_get_implicit_lowering() && g.s > 1 && std::fmod(g.s * g.s * g.d, 16) == 0;
+}
+G s2d_of(const G& g) {
+    G v = g;
+    v.k = std::ceil(g.k / g.s);
+    v.n = g.m + v.k - 1;
+    v.d = g.s * g.s * g.d;
+    v.s = 1;
+    v.p = 0;
+    v.N = v.n;
+    v.R = v.n;
+    return v;
+}
+
+void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* secs, double* bytes,
+              bool allow_s2d = true);
+
+// model seconds of a strided Type 1 pass with (true) / without the space-to-depth form
+double t1_form_seconds(const G& g, int pass, bool s2d, const cct_calibration* c) {
+    double secs = 0, bytes = 0;
+    one_pass(g, 1, pass, c, &secs, &bytes, s2d);
+    return secs;
+}
+
+// counts + model for one pass.  pass: 0 fwd, 1 bwd-data, 2 bwd-weight, 3 training step.
+// A strided Type 1 layer takes the faster of its direct and space-to-depth forms,
+// as the launcher does (cct::prefer_s2d).
+void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* secs, double* bytes,
+              bool allow_s2d) {
     const double f = 4.0;  // bytes per float
+    if (type == 1 && allow_s2d && s2d_possible(g)) {
+        double s0 = 0, b0 = 0, s1 = 0, b1 = 0;
+        one_pass(g, 1, pass, c, &s0, &b0, false);
+        const G v = s2d_of(g);
+        one_pass(v, 1, pass, c, &s1, &b1, false);
+        const double xin = g.b * g.n * g.n * g.d * f, xs = v.b * v.n * v.n * v.d * f;
+        // blocking of x (fwd, or wgrad without the forward's cache), unblocking of dx,
+        // and the two small kernel-bank gathers; the blocking kernels run at ~0.5 of
+        // the copy rate (one-thread-per-element gathers)
+        const double moved = (pass == 3 ? 2.0 : 1.0) * (xin + xs);
+        const double launches = pass == 0 ? 2 : pass == 3 ? 5 : 3;
+        s1 += moved / (0.5 * c->hbm_bytes_per_s) + launches * c->launch_s;
+        b1 += moved;
+        if (s1 < s0) { *secs = s1; *bytes = b1; }
+        else { *secs = s0; *bytes = b0; }
+        return;
+    }
     double rows, cols, ncols;
     if (type == 1) { rows = g.b * g.m * g.m; cols = g.k * g.k * g.d; ncols = g.o; }
     else if (type == 2) { rows = g.b * g.R * g.m; cols = g.k * g.d; ncols = g.k * g.o; }
@@ -134,9 +184,14 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     const double xin = g.b * g.n * g.n * g.d * f, yout = g.b * g.o * g.m * g.m * f;
     const double dhat = rows * rup(cols, 4) * f, rhat = rows * ncols * f;
     const bool t3_zero_copy = (type == 3 && g.p == 0 && g.R == g.n && std::fmod(g.d, 4) == 0);
-    // implicit Type 1 (TMA im2col operands, d % 32 == 0): no lowering, A read from x;
-    // backward-weight through im2col measured ~10% slower than from a materialised Dhat
-    const bool t1_implicit = (type == 1 && std::fmod(g.d, 32) == 0 && cct_get_implicit_lowering());
+    // implicit Type 1 (TMA im2col operands, d % 16 == 0): no lowering, A read from x;
+    // backward-weight through im2col measured ~10% slower than from a materialised Dhat,
+    // and its taps are padded to dk = d rounded up to 32 channels
+    const bool t1_implicit = (type == 1 && std::fmod(g.d, 16) == 0 && cct_get_implicit_lowering());
+    const double wg_cols = t1_implicit ? g.k * g.k * rup(g.d, 32) : cols;
+    // implicit backward-weight GEMM: MN-major im2col A; narrow banks (o <= 96) run
+    // without CTA pairs (measured 0.74 of the table rate, conv1 in s2d form)
+    const double wg_slow = t1_implicit ? (g.o <= 96 ? 1.35 : 1.1) : 1.0;
     double t = 0, by = 0, launches = 0;
     // measured class rates (sweep, profiles/r01): lift and expand gather, so they
     // run below the copy-like lower / col2im kernels
@@ -176,7 +231,7 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     } else if (pass == 2) {
         if (!t3_zero_copy && !t1_implicit) hbm(xin + dhat); // lower
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand
-        const double gt = gemm_seconds(cols, ncols, rows, c) * (t1_implicit ? 1.1 : 1.0);
+        const double gt = gemm_seconds(wg_cols, ncols, rows, c) * wg_slow;
         const double gb = a_in + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
@@ -191,7 +246,7 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         if (type != 1) hbm_at(rhat + yout, lift_bw);       // lift
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand (shared)
         t += dgrad(&by, &launches);                        // bwd-data
-        gt = gemm_seconds(cols, ncols, rows, c) * (t1_implicit ? 1.1 : 1.0);  // bwd-weight GEMM
+        gt = gemm_seconds(wg_cols, ncols, rows, c) * wg_slow;  // bwd-weight GEMM
         gb = a_in + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
@@ -204,6 +259,20 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
 }  // namespace
 
 namespace cct {
+// Used by the launcher (cct_abi.cu): run a strided Type 1 layer in space-to-depth
+// form when the model predicts that form faster for `pass` (0 fwd, 1 bwd-data,
+// 2 bwd-weight, 3 training step).  Decided at a fixed batch (256) so that batch
+// chunks and the lowered cache of a training step always agree.
+bool prefer_s2d(const cct_conv_desc* desc, int pass) {
+    G g = geo(desc);
+    if (!s2d_possible(g)) return false;
+    if (cct_get_implicit_lowering() == 2) return true;  // forced (tests)
+    g.b = 256;
+    cct_calibration cal;
+    cct_calibration_default(&cal);
+    return t1_form_seconds(g, pass, true, &cal) < t1_form_seconds(g, pass, false, &cal);
+}
+
 // Used by the launcher (cct_abi.cu): run Type 1 backward-data implicitly when
 // that form is possible and the model predicts it faster.
 bool prefer_implicit_dgrad(const cct_conv_desc* desc) {

@@ -46,7 +46,8 @@ struct KParams {
     float* sk_part;
     int* sk_cnt;
     int64_t s_nq;
-    // implicit (im2col) A: layer geometry
+    int64_t mlim;
+    // implicit (im2col) A: layer geometry (ic_d = channels per tap of the lowered index)
     int ic_d, ic_k, ic_s, ic_p, ic_m, ic_mm, ic_cpt;
 };
 
@@ -171,10 +172,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     using C_ = Cfg<BN, CG>;
     constexpr int STAGES = C_::STAGES;
     constexpr int BNL = C_::BNL;
-    constexpr int kASlots = 4;                                        // TMEM ring of A tiles
-    constexpr uint32_t A_COL = uint32_t(2 * C_::NACC * BN);           // first A column
+    // A_TM == 2: one accumulator per tile, the freed TMEM columns deepen the A ring
+    constexpr int NACC = (A_TM == 2) ? 1 : C_::NACC;
+    constexpr uint32_t A_COL = uint32_t(2 * NACC * BN);               // first A column
+    constexpr int kASlotsFit = int((512u - A_COL) / (2 * kBK));
+    constexpr int kASlots = A_TM ? (kASlotsFit < 12 ? (kASlotsFit < STAGES - 1 ? kASlotsFit : STAGES - 1)
+                                                    : (12 < STAGES - 1 ? 12 : STAGES - 1))
+                                 : 4;                                 // TMEM ring of A tiles
     constexpr uint32_t TMEM_COLS = A_TM ? 512u : C_::TMEM_COLS;
-    static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots), "A_TM config");
+    static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots && kASlots >= 4),
+                  "A_TM config");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align inside the shared window without leaving the shared address space
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -316,7 +323,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t use = uint32_t(local >> 1);
                 ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 ptx::tc_fence_after();
-                const uint32_t d_tmem = tmem_base + uint32_t(acc * C_::NACC * BN);
+                const uint32_t d_tmem = tmem_base + uint32_t(acc * NACC * BN);
                 auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
                     if constexpr (CG == 1) ptx::mma_tf32(d, a, b, idesc, accumulate);
                     else ptx::mma_tf32_cg2(d, a, b, idesc, accumulate);
@@ -341,14 +348,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t first = (kb > kb0) ? 1u : 0u;
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk)
-                            mma_ts(d_tmem + kk * BN, a_small + kk * 8, tile_desc<B_MN>(b_raw, kk), first);
+                            mma_ts(d_tmem + kk * (NACC - 1) * BN, a_small + kk * 8, tile_desc<B_MN>(b_raw, kk),
+                                   (NACC == 1 && kk) ? 1u : first);
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk)
-                            mma_ts(d_tmem + kk * BN, a_big + kk * 8, tile_desc<B_MN>(b_sml, kk), 1u);
+                            mma_ts(d_tmem + kk * (NACC - 1) * BN, a_big + kk * 8, tile_desc<B_MN>(b_sml, kk), 1u);
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk)
-                            mma_ts(d_tmem + kk * BN, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
-                    } else if constexpr (C_::NACC == 1) {
+                            mma_ts(d_tmem + kk * (NACC - 1) * BN, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
+                    } else if constexpr (NACC == 1) {
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk) {
                             const uint64_t ad = tile_desc<A_MN>(a_raw, kk);
@@ -409,9 +417,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_wait(&tfull[acc], use & 1);
             ptx::tc_fence_after();
             const int64_t row = int64_t(mt) * (kBM * CG) + int64_t(rank) * kBM + rit;
-            const bool row_ok = row < p.M;
+            bool row_ok = row < p.M;
             int64_t off = 0;
-            if (row_ok) off = (row / p.mdiv) * p.s_mq + (row % p.mdiv) * p.s_mr + int64_t(sp) * p.s_split;
+            if (row_ok) {
+                const int64_t rq = row / p.mdiv, rr = row - rq * p.mdiv;
+                row_ok = rr < p.mlim;
+                off = rq * p.s_mq + rr * p.s_mr + int64_t(sp) * p.s_split;
+            }
             const int n0 = nt * BN;
             // final values of columns n0 + c0 .. +31 of this thread's row -> output map
             auto store32 = [&](const uint32_t* v, int c0) {
@@ -462,9 +474,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 32) {
                 uint32_t v[32];
-                const uint32_t tcol = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * C_::NACC * BN + c0);
+                const uint32_t tcol = tmem_base + (uint32_t(q * 32) << 16) + uint32_t(acc * NACC * BN + c0);
                 ptx::tmem_ld_32x32b_x32(tcol, v);
-                if constexpr (C_::NACC == 2) {
+                if constexpr (NACC == 2) {
                     uint32_t v2[32];
                     ptx::tmem_ld_32x32b_x32(tcol + BN, v2);
                     ptx::tmem_ld_wait();
@@ -697,12 +709,14 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& 
     return cudaGetLastError();
 }
 
-bool a_in_tmem_enabled() {
-    static const int v = [] {  // $CCT_A_TMEM=0 keeps narrow tiles on the smem-A path (A/B)
+// $CCT_A_TMEM: 0 keeps narrow tiles on the smem-A path, 1 A in TMEM with two
+// sub-accumulators, 2 A in TMEM with one accumulator and a deeper A ring (A/B)
+int a_in_tmem_mode() {
+    static const int v = [] {
         const char* e = getenv("CCT_A_TMEM");
         return e ? atoi(e) : 1;
     }();
-    return v != 0;
+    return v;
 }
 
 template <int BN, int CG>
@@ -710,7 +724,12 @@ cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const C
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
     if constexpr (BN <= 96) {
-        if (!amn && g.passes == 3 && a_in_tmem_enabled()) {
+        const int atm = a_in_tmem_mode();
+        if (!amn && g.passes == 3 && atm == 2) {
+            if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 2>(ta, tb, kp, st);
+            return bmn ? launch<BN, 0, 1, CG, 0, 2>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 2>(ta, tb, kp, st);
+        }
+        if (!amn && g.passes == 3 && atm) {
             if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 1>(ta, tb, kp, st);
             return bmn ? launch<BN, 0, 1, CG, 0, 1>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 1>(ta, tb, kp, st);
         }
@@ -746,7 +765,8 @@ int choose_cg(const GemmProblem& g, int bn) {
 
 }  // namespace
 
-bool im2col_ok(int64_t d, bool mn_major) { return mn_major ? d % 32 == 0 : d % kBK == 0; }
+bool im2col_ok(int64_t d, bool) { return d % kBK == 0; }
+int64_t im2col_dk(int64_t d, bool mn_major) { return mn_major ? (d + 31) / 32 * 32 : d; }
 
 int choose_bn(int64_t N) {
     static const int cands[] = {256, 192, 128, 96, 64};
@@ -852,6 +872,7 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.s_split = g.C.s_split;
     kp.ndiv = g.C.ndiv < (int64_t(1) << 31) ? int(g.C.ndiv) : 0;
     kp.s_nq = g.C.s_nq;
+    kp.mlim = g.C.mlim;
 
     const int cg = choose_cg(g, bn);
     kp.num_m_tiles = int((g.M + kBM * cg - 1) / (kBM * cg));
@@ -870,15 +891,17 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     CUtensorMap ta, tb;
     if (g.im2col.x) {
         const Im2col& ic = g.im2col;
-        kp.ic_d = int(ic.d);
+        const bool amn = g.A.major == Major::MN;
+        const int64_t dk = ic.dk ? ic.dk : ic.d;
+        if (!im2col_ok(ic.d, amn) || dk < ic.d || dk % (amn ? 32 : kBK)) return cudaErrorInvalidValue;
+        kp.ic_d = int(dk);
         kp.ic_k = int(ic.k);
         kp.ic_s = int(ic.s);
         kp.ic_p = int(ic.p);
         kp.ic_m = int(ic.m);
         kp.ic_mm = int(ic.m * ic.m);
-        kp.ic_cpt = int(ic.d / kBK);
-        if (!im2col_ok(ic.d, g.A.major == Major::MN)) return cudaErrorInvalidValue;
-        if (!make_tmap_im2col(&ta, ic, g.A.major == Major::MN)) return cudaErrorInvalidValue;
+        kp.ic_cpt = int(dk / kBK);
+        if (!make_tmap_im2col(&ta, ic, amn)) return cudaErrorInvalidValue;
     } else if (!make_tmap(&ta, g.A, g.M, g.K, kBM)) {
         return cudaErrorInvalidValue;
     }

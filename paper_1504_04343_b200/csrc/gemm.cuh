@@ -26,6 +26,7 @@ struct OutMap {
     int64_t mdiv = INT64_MAX;
     int64_t s_mq = 0, s_mr = 1, s_n = 0, s_split = 0;
     int64_t ndiv = INT64_MAX, s_nq = 0;
+    int64_t mlim = INT64_MAX;  // rows with (m % mdiv) >= mlim are not stored (padded channels)
 };
 
 // Implicit Type 1 lowering: operand A is read straight from the NHWC input x
@@ -35,9 +36,14 @@ struct OutMap {
 //   A.major == K  (forward; backward-data = forward of dy (NHWC) with rotated
 //                  weights): tile = 128 pixels x 16 channels of one tap
 //   A.major == MN (backward-weight): tile = 16 pixels x (4 x 32 channels)
+// Channels per tap in the lowered index are dk (0: = d).  An MN-major A needs
+// whole 32-channel boxes per tap, so a layer with d % 32 != 0 uses dk = d rounded
+// up to 32: the boxes read past channel d-1 are zero-filled by TMA and the
+// epilogue skips those rows (OutMap::mlim).
 struct Im2col {
     const float* x = nullptr;  // nullptr: A is an ordinary (materialised) matrix
     int64_t b = 0, n = 0, d = 0, k = 0, s = 1, p = 0, m = 0;
+    int64_t dk = 0;
 };
 
 struct GemmProblem {
@@ -57,9 +63,11 @@ struct GemmProblem {
 // scratch run_gemm can use for this problem (0: none needed)
 size_t gemm_workspace_bytes(const GemmProblem& g);
 
-// Can this layer use the implicit (im2col) A operand?  fwd needs d % 16 == 0,
-// backward-weight d % 32 == 0 (one TMA box never straddles a filter tap).
+// Can this layer use the implicit (im2col) A operand?  d % 16 == 0 (one TMA box
+// never straddles a filter tap; backward-weight pads the tap to im2col_dk).
 bool im2col_ok(int64_t d, bool mn_major);
+// channels per tap of the lowered index for an im2col A operand
+int64_t im2col_dk(int64_t d, bool mn_major);
 
 // Tile constants shared by the launcher and the kernel.
 constexpr int kBM = 128;

@@ -349,7 +349,7 @@ def test_batch_chunking_under_workspace_limit(cct, dev, t):
 
 
 @pytest.mark.parametrize("layer", [("conv2s", 27, 5, 96, 64, 1, 2), ("conv3", 13, 3, 256, 384, 1, 1),
-                                   ("s2p1", 15, 3, 32, 40, 2, 1), ("ragged", 14, 4, 64, 48, 3, 2)],
+                                   ("d16", 11, 3, 16, 40, 1, 1), ("d48", 12, 5, 48, 64, 1, 2)],
                          ids=lambda l: l[0])
 def test_implicit_lowering_matches_materialised(cct, dev, orc, layer):
     """Implicit Type 1 (TMA im2col operands, no Dhat in HBM) == materialised Type 1:
@@ -388,13 +388,14 @@ def test_implicit_lowering_matches_materialised(cct, dev, orc, layer):
 @pytest.mark.parametrize("layer", [("conv2s", 27, 5, 96, 64, 1, 2), ("conv3", 13, 3, 256, 384, 1, 1),
                                    ("pad0_d20", 12, 3, 20, 32, 1, 0), ("padk-1", 10, 3, 8, 16, 1, 2),
                                    ("k1", 9, 1, 16, 16, 1, 0), ("d3", 11, 4, 3, 16, 1, 1),
-                                   ("longK", 9, 5, 8, 176, 1, 2), ("stride2", 15, 3, 32, 48, 2, 1)],
+                                   ("longK", 9, 5, 8, 176, 1, 2), ("stride2", 15, 3, 32, 48, 2, 1),
+                                   ("d48", 12, 5, 48, 64, 1, 2)],
                          ids=lambda l: l[0])
 def test_implicit_dgrad(cct, dev, orc, layer):
     """Implicit stride-1 backward-data (dy -> NHWC, forward convolution with the rotated
     kernel bank straight into dx; implicit mode 2 forces it) matches the oracle and the
-    materialised path; backward-weight with the NHWC dy as B operand too.  Stride 2 falls
-    back to the materialised form."""
+    materialised path; backward-weight with the NHWC dy as B operand too.  Stride 2 runs
+    as the stride-1 backward of its space-to-depth form."""
     from paper_1504_04343_b200 import conv
     L = cct.lib()
     _, n, k, d, o, s, p = layer
@@ -424,5 +425,53 @@ def test_implicit_dgrad(cct, dev, orc, layer):
     for got in (dwi, dwm):
         assert rel_l2(got.cpu().numpy().ravel(), ref_dw) <= TOL
     assert float(torch.linalg.norm(dxi - dxm) / torch.linalg.norm(dxm)) < 5e-5  # two ~1e-5 paths
-    if s != 1:
-        assert torch.equal(dxi, dxm)
+
+
+S2D_LAYERS = [("conv1", 227, 11, 3, 96, 4, 0), ("conv1s", 35, 11, 3, 96, 4, 0), ("s2p1", 15, 3, 32, 40, 2, 1),
+              ("ragged", 14, 4, 64, 48, 3, 2), ("s2d16", 23, 5, 4, 16, 2, 1), ("k_lt_s", 20, 3, 4, 8, 4, 1),
+              ("pad_gt", 17, 6, 16, 32, 2, 4), ("no_s2d", 19, 7, 12, 32, 3, 3)]
+
+
+@pytest.mark.parametrize("layer", S2D_LAYERS, ids=lambda l: l[0])
+def test_space_to_depth(cct, dev, orc, layer):
+    """Strided Type 1 layers run as the stride-1 convolution of the space-to-depth
+    blocked input (k' = ceil(k/s) taps of depth s^2 d; s2d.cuh): forward, backward-data,
+    backward-weight and the cached training step against the oracle, and against the
+    materialised path.  s^2 d % 16 != 0 (no_s2d) stays materialised.  Implicit mode 2
+    forces the blocked form; by default the cost model picks it per pass (prefer_s2d)."""
+    from paper_1504_04343_b200 import conv
+    L = cct.lib()
+    _, n, k, d, o, s, p = layer
+    b = 2
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    x_np, w_np = orc.random_problem(31, b, n, d, k, o)
+    dy_np = orc.uniform(32, b * o * desc.m * desc.m)
+    x = T(x_np, dev, b, n, n, d)
+    w = T(w_np, dev, o, k, k, d)
+    dy = T(dy_np, dev, b, o, desc.m, desc.m)
+    blocked = (s * s * d) % 16 == 0
+    old = L.cct_get_implicit_lowering()
+    try:
+        L.cct_set_implicit_lowering(2)  # forces the blocked form (else the cost model picks per pass)
+        ks, ns = -(-k // s), desc.m + -(-k // s) - 1
+        assert cct.lowered_cache_size(desc, 1) == (b * ns * ns * s * s * d * 4 if blocked else
+                                                    b * desc.m * desc.m * ((k * k * d + 3) // 4 * 4) * 4)
+        y, dx, dw = (conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_data(dy, w, desc, 1),
+                     conv.conv_bwd_weight(x, dy, desc, 1))
+        cache = conv.alloc_cache(desc, 1, dev)
+        yc = conv.conv_fwd_cached(x, w, desc, 1, cache=cache)
+        dxc, dwc = conv.conv_bwd(dy, w, desc, 1, x=x, cache=cache)
+        L.cct_set_implicit_lowering(0)
+        ym, dxm, dwm = (conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_data(dy, w, desc, 1),
+                        conv.conv_bwd_weight(x, dy, desc, 1))
+    finally:
+        L.cct_set_implicit_lowering(old)
+    assert torch.equal(yc, y) and torch.equal(dxc, dx) and torch.equal(dwc, dw)
+    refs = (orc.conv_fwd(x_np, w_np, b, n, d, k, o, s, p), orc.conv_bwd_data(dy_np, w_np, b, n, d, k, o, s, p),
+            orc.conv_bwd_weight(x_np, dy_np, b, n, d, k, o, s, p))
+    for got, ref in zip((y, dx, dw), refs):
+        assert rel_l2(got.cpu().numpy().ravel(), ref) <= TOL
+    for got, ref in zip((ym, dxm, dwm), refs):
+        assert rel_l2(got.cpu().numpy().ravel(), ref) <= TOL
+    if not blocked:
+        assert torch.equal(y, ym) and torch.equal(dx, dxm)

@@ -26,6 +26,9 @@ SHAPES = {
     "wgrad_like": (2400, 256, 4096),
     "square": (8192, 8192, 2048),
     "narrow96": (65536, 96, 4096),
+    "narrow64": (65536, 64, 4096),
+    "conv1fwd": (774400, 96, 432),
+    "conv1dgrad": (831744, 48, 864),
     "mid192": (65536, 192, 4096),
 }
 
