@@ -313,12 +313,17 @@ def run_ours(a):
     gemm_ms = pms[1] / a.steps
     alg_per_rank = st.flops_per_step()
     achieved = alg_per_rank / (gemm_ms * 1e-3) / 1e12 if gemm_ms > 0 else None
-    peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 2.0 / 3.0
+    # The GEMMs run at max SM clock inside this step (clocks below), so the ceiling is
+    # the burst tensor rate: measured dense bf16 / 2 (TF32) / 3 (three products).  The
+    # sustained figure (power-capped 4 s matmul at ~1.3 GHz) is kept for reference.
+    peak = peaks.get("bf16_tflops") / 2.0 / 3.0
+    peak_sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 2.0 / 3.0
     roofline = {
         "bound": "tensor", "kernel": "gemm3xtf32_kernel (tcgen05 kind::tf32, 3 products per K step)",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": (achieved / peak) if achieved else None,
-        "peak_source": f"{peak_src} bf16_tflops_sustained / 2 (TF32 rate) / 3 (3xTF32 products)",
+        "peak_source": f"{peak_src} bf16_tflops (burst) / 2 (TF32 rate) / 3 (3xTF32 products)",
+        "peak_sustained": peak_sus,
         "tf32_cublas_tflops_measured": tf32_meas,
         "frac_of_burst_ceiling": (achieved / (tf32_meas / 3.0)) if (achieved and tf32_meas) else None,
         "step_frac": (flops_step / world / (ms_max * 1e-3) / 1e12) / peak,

@@ -240,6 +240,9 @@ CCT_API void cct_profile_read(double* ms, double* flops, double* bytes, uint64_t
 /* ---- misc ------------------------------------------------------------- */
 CCT_API const char* cct_last_error(void);
 CCT_API int cct_abi_version(void);
+/* name of the current CUDA device and its SM count (0 and "none" without a
+ * device): the machine descriptor of convbench records */
+CCT_API int cct_device_info(char* name, size_t len, int* sms);
 /* number of CUDA kernels this library launched on the calling host thread
  * since the last reset (the bench's gpu_launches evidence) */
 CCT_API uint64_t cct_launch_count(void);

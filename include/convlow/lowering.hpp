@@ -45,6 +45,10 @@ std::pair<OutputBatch, PhaseTimings> convolve_lowered(const DataBatch& batch, co
                                                       LoweringStrategy strategy, std::size_t gemm_threads,
                                                       ConvGeometry geom = {});
 
+// Extension of direct_convolve_batch (tensor.hpp) to stride / pad: the exact
+// fp64 device oracle of the generalised layer (checker for convbench verify).
+OutputBatch direct_convolve_batch(const DataBatch& batch, const KernelBank& bank, ConvGeometry geom);
+
 // Backward passes (north_star).  dy has the OutputBatch layout of the forward
 // output; the results have the layouts of the forward inputs.
 DataBatch convolve_backward_data(const OutputBatch& dy, const KernelBank& bank, std::size_t n,

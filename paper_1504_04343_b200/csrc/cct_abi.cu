@@ -629,6 +629,17 @@ cct_status check_ptrs(std::initializer_list<const void*> ps) {
 extern "C" {
 
 int cct_abi_version(void) { return CCT_ABI_VERSION; }
+
+int cct_device_info(char* name, size_t len, int* sms) {
+    int dev = 0, n = 0;
+    cudaDeviceProp prop;
+    const bool ok = cudaGetDeviceCount(&n) == cudaSuccess && n > 0 && cudaGetDevice(&dev) == cudaSuccess &&
+                    cudaGetDeviceProperties(&prop, dev) == cudaSuccess;
+    if (!ok) cudaGetLastError();  // clear the sticky "no device" error
+    if (name && len) snprintf(name, len, "%s", ok ? prop.name : "none");
+    if (sms) *sms = ok ? prop.multiProcessorCount : 0;
+    return ok ? n : 0;
+}
 void cct_set_workspace_limit(size_t bytes) { g_ws_limit = bytes; }
 void cct_set_implicit_lowering(int mode) { g_implicit = std::max(0, std::min(2, mode)); }
 int cct_get_implicit_lowering(void) { return implicit_enabled() ? g_implicit : 0; }

@@ -684,4 +684,85 @@ SplitPlan proportional_split(const std::vector<DeviceProfile>& devices, std::siz
     return plan;
 }
 
+double simulate_makespan(const LayerConfig& layer, const SplitPlan& plan, const std::vector<DeviceProfile>& devices,
+                         LoweringStrategy strategy) {
+    if (plan.fractions.size() != devices.size())
+        throw config_error("split plan has " + std::to_string(plan.fractions.size()) + " fractions for " +
+                           std::to_string(devices.size()) + " devices");
+    LayerConfig one = layer;
+    one.b = 1;
+    one.validate();
+    const double per_image = double(estimate(strategy, one, CostWeights{0, 0, false}).gemm_flops);
+    double span = 0;
+    for (size_t i = 0; i < devices.size(); ++i) {
+        if (!(devices[i].flops > 0)) throw config_error("device '" + devices[i].name + "' needs flops > 0");
+        const double f = plan.fractions[i];
+        if (f <= 0) continue;  // a device without work finishes at 0
+        span = std::max(span, devices[i].fixed_overhead + f * double(layer.b) * per_image / devices[i].flops);
+    }
+    return span;
+}
+
+namespace {
+SplitPlan two_way(double p, std::size_t b) {
+    SplitPlan s;
+    s.fractions = {1.0 - p, p};
+    const auto c1 = std::size_t(std::llround(p * double(b)));
+    s.counts = {b - std::min(b, c1), std::min(b, c1)};
+    return s;
+}
+}  // namespace
+
+SplitPlan optimal_split_sweep(const LayerConfig& layer, const std::vector<DeviceProfile>& devices,
+                              std::size_t granularity, LoweringStrategy strategy) {
+    if (devices.size() != 2)
+        throw config_error("optimal_split_sweep supports exactly 2 devices (SPEC.md:393), got " +
+                           std::to_string(devices.size()));
+    if (granularity < 10) throw config_error("granularity must be >= 10");
+    SplitPlan best = two_way(0.0, layer.b);
+    double best_t = simulate_makespan(layer, best, devices, strategy);
+    for (std::size_t i = 1; i <= granularity; ++i) {
+        SplitPlan s = two_way(double(i) / double(granularity), layer.b);
+        const double t = simulate_makespan(layer, s, devices, strategy);
+        if (t < best_t) {  // strict: ties keep the smaller fraction
+            best_t = t;
+            best = s;
+        }
+    }
+    return best;
+}
+
+double heuristic_gap(const LayerConfig& layer, const std::vector<DeviceProfile>& devices, std::size_t granularity,
+                     LoweringStrategy strategy) {
+    const SplitPlan prop = proportional_split(devices, layer.b);
+    const double tp = simulate_makespan(layer, prop, devices, strategy);
+    const double ts = simulate_makespan(layer, optimal_split_sweep(layer, devices, granularity, strategy), devices,
+                                        strategy);
+    const double opt = std::min(tp, ts);
+    return opt > 0 ? tp / opt : 1.0;
+}
+
+OutputBatch direct_convolve_batch(const DataBatch& batch, const KernelBank& bank, ConvGeometry geom) {
+    const Tensor3& first = batch[0];
+    if (bank.depth() != first.depth() || bank.k() > first.rows() + 2 * geom.pad)
+        throw config_error("kernel bank " + bank_shape_str(bank) + " incompatible with data tensor " +
+                           tensor_shape_str(first));
+    LayerConfig L;
+    L.n = first.rows();
+    L.k = bank.k();
+    L.d = first.depth();
+    L.o = bank.o();
+    L.b = batch.b();
+    L = layer_with(L, geom);
+    cct_conv_desc d = make_desc(L);
+    float* dx = upload_batch(batch, kX);
+    float* dw = upload(bank.values(), kW);
+    OutputBatch out(L.b, L.o, L.m());
+    auto* dy = static_cast<float*>(ctx().get(kY, out.size() * sizeof(float)));
+    check(cct_direct_conv_fwd_exact(&d, dx, dw, dy, ctx().stream), "direct_convolve_batch");
+    download(out.values(), dy);
+    ctx().sync();
+    return out;
+}
+
 }  // namespace convlow
