@@ -142,6 +142,32 @@ CCT_API cct_status cct_conv_bwd(const cct_conv_desc* desc, cct_lowering lowering
                                 const float* cache, const float* dy, const float* w, float* dx, float* dw,
                                 void* ws, size_t ws_bytes, void* stream);
 
+/* Layer extension (the reference SPEC puts groups out of
+ * scope): grouped convolution as in bvlc_reference_caffenet
+ * (group = 2 on conv2/4/5) and the bias + ReLU epilogue
+ * around the layer.  desc->d and desc->o are the TOTAL channel counts; w is
+ * (o, k, k, d / groups), output channel j reads input-channel group
+ * j / (o / groups); y = relu ? max(conv + bias, 0) : conv + bias (bias may be
+ * NULL).  The lowering type (AUTO: the cost model's choice for one group) is
+ * applied per group.  Implicit Type 1 groups run straight on x / y (TMA im2col
+ * over a channel view, strided epilogue with the bias / ReLU fused); other forms
+ * gather each group into scratch.  NULL ext = { 1, NULL, 0 }. */
+typedef struct {
+    int64_t groups;
+    const float* bias; /* (o) device pointer or NULL */
+    int relu;          /* 0 or 1 */
+} cct_conv_ext;
+
+CCT_API cct_status cct_workspace_size_ex(const cct_conv_desc* desc, cct_lowering lowering, const cct_conv_ext* ext,
+                                         cct_pass pass, size_t* bytes);
+CCT_API cct_status cct_conv_fwd_ex(const cct_conv_desc* desc, cct_lowering lowering, const cct_conv_ext* ext,
+                                   const float* x, const float* w, float* y, void* ws, size_t ws_bytes, void* stream);
+/* dy: gradient of the layer output y (post-activation; y is needed when relu).
+ * Any of dx, dw, db (bias gradient, (o)) may be NULL.  Deterministic. */
+CCT_API cct_status cct_conv_bwd_ex(const cct_conv_desc* desc, cct_lowering lowering, const cct_conv_ext* ext,
+                                   const float* x, const float* y, const float* dy, const float* w, float* dx,
+                                   float* dw, float* db, void* ws, size_t ws_bytes, void* stream);
+
 /* Phase-level API for PhaseTimings and the bit-exact lowering parity.
  * lower: dhat gets the data-side matrix with row stride ld
  * (floats, >= cols).  Shapes: cct_lowered_shape().  The kernel side never

@@ -230,6 +230,43 @@ class Reference:
         return out
 
 
+def grouped_fwd(orc, x, w, b, n, d, k, o, s, p, groups, bias=None, relu=False):
+    """Grouped convolution + bias + ReLU (the layer extension) on
+    the oracle: group j convolves input channels [j d/G, (j+1) d/G) with kernels
+    [j o/G, (j+1) o/G) -- Caffe's `group` semantics (bvlc_reference_caffenet,
+    PAPER.md:343, 401) -- then y = act(conv + bias).  Returns (b, o, m, m) float32."""
+    dg, og = d // groups, o // groups
+    m = (n + 2 * p - k) // s + 1
+    xs = np.asarray(x, np.float32).reshape(b, n, n, d)
+    ws = np.asarray(w, np.float32).reshape(o, k, k, dg)
+    parts = [orc.conv_fwd(_f32(xs[..., j * dg:(j + 1) * dg]).ravel(), _f32(ws[j * og:(j + 1) * og]).ravel(),
+                          b, n, dg, k, og, s, p).reshape(b, og, m, m) for j in range(groups)]
+    y = np.concatenate(parts, axis=1)
+    if bias is not None:
+        y = y + np.asarray(bias, np.float32)[None, :, None, None]
+    return np.maximum(y, 0).astype(np.float32) if relu else y.astype(np.float32)
+
+
+def grouped_bwd(orc, dz, x, w, b, n, d, k, o, s, p, groups):
+    """(dx, dw, db) of the grouped convolution for dz = the gradient at the conv output
+    (the ReLU mask already applied).  dx (b, n, n, d), dw (o, k, k, d/G), db (o), fp64 db."""
+    dg, og = d // groups, o // groups
+    m = (n + 2 * p - k) // s + 1
+    dzs = np.asarray(dz, np.float32).reshape(b, o, m, m)
+    xs = np.asarray(x, np.float32).reshape(b, n, n, d)
+    ws = np.asarray(w, np.float32).reshape(o, k, k, dg)
+    dx = np.empty((b, n, n, d), np.float32)
+    dw = np.empty((o, k, k, dg), np.float32)
+    for j in range(groups):
+        dzj = _f32(dzs[:, j * og:(j + 1) * og]).ravel()
+        dx[..., j * dg:(j + 1) * dg] = orc.conv_bwd_data(dzj, _f32(ws[j * og:(j + 1) * og]).ravel(),
+                                                         b, n, dg, k, og, s, p).reshape(b, n, n, dg)
+        dw[j * og:(j + 1) * og] = orc.conv_bwd_weight(_f32(xs[..., j * dg:(j + 1) * dg]).ravel(), dzj,
+                                                      b, n, dg, k, og, s, p).reshape(og, k, k, dg)
+    db = dzs.astype(np.float64).sum(axis=(0, 2, 3))
+    return dx, dw, db
+
+
 def rel_l2(a, b) -> float:
     a = np.asarray(a, np.float64).ravel()
     b = np.asarray(b, np.float64).ravel()

@@ -43,6 +43,11 @@ class ResourceError(CctError):
     """Maps CCT_ERR_RESOURCE / CCT_ERR_CUDA (convlow::resource_error, common.hpp:22-24)."""
 
 
+class ConvExt(C.Structure):
+    """cct_conv_ext: channel groups and the bias / ReLU epilogue (include/cct.h)."""
+    _fields_ = [("groups", C.c_int64), ("bias", C.c_void_p), ("relu", C.c_int)]
+
+
 class _Desc(C.Structure):
     _fields_ = [(f, C.c_int64) for f in ("n", "k", "d", "o", "b", "stride", "pad", "m", "R")]
 
@@ -91,6 +96,9 @@ def lib() -> C.CDLL:
         "cct_conv_fwd_cached": [D, C.c_int, VP, VP, VP, VP, SZ, VP, SZ, VP],
         "cct_conv_bwd": [D, C.c_int, VP, VP, VP, VP, VP, VP, VP, SZ, VP],
         "cct_estimate": [D, C.c_int, P(Calibration), C.c_int, P(CostEstimate)],
+        "cct_workspace_size_ex": [D, C.c_int, P(ConvExt), C.c_int, P(SZ)],
+        "cct_conv_fwd_ex": [D, C.c_int, P(ConvExt), VP, VP, VP, VP, SZ, VP],
+        "cct_conv_bwd_ex": [D, C.c_int, P(ConvExt), VP, VP, VP, VP, VP, VP, VP, VP, SZ, VP],
     }
     for name, args in sigs.items():
         fn = getattr(L, name)

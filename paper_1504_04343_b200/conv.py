@@ -13,10 +13,10 @@ import ctypes as C
 import torch
 
 from . import (LOWER_AUTO, PASS_BWD, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_FWD, ROWS_INTERNAL, ROWS_SPEC,
-               ConfigError, ConvDesc, check, lib, lowered_cache_size, workspace_size)
+               ConfigError, ConvDesc, ConvExt, check, lib, lowered_cache_size, workspace_size)
 
 __all__ = ["Workspace", "conv_fwd", "conv_bwd_data", "conv_bwd_weight", "convolve_lowered", "lower",
-           "conv_fwd_cached", "conv_bwd", "alloc_cache",
+           "conv_fwd_cached", "conv_bwd", "alloc_cache", "conv_fwd_ex", "conv_bwd_ex",
            "lower_khat", "lift", "lowered_shape", "multiply", "multiply_passes"]
 
 
@@ -195,3 +195,44 @@ def multiply_passes(a, b, passes: int, stream=None):
     check(lib().cct_gemm_passes(M, N, K, _ptr(ap), ap.shape[1], _ptr(bp), bp.shape[1], _ptr(c), N, passes,
                                 _stream(stream)))
     return c
+
+
+# ---------------------------------------------------------------- layer extension
+def _ext(groups: int, bias, relu: bool) -> ConvExt:
+    return ConvExt(int(groups), bias.data_ptr() if bias is not None else None, 1 if relu else 0)
+
+
+def _ws_ex(desc: ConvDesc, lowering: int, ext: ConvExt, pass_: int) -> int:
+    out = C.c_size_t()
+    check(lib().cct_workspace_size_ex(C.byref(desc.c()), lowering, C.byref(ext), pass_, C.byref(out)))
+    return out.value
+
+
+def conv_fwd_ex(x, w, desc: ConvDesc, lowering: int = LOWER_AUTO, groups: int = 1, bias=None, relu: bool = False,
+                out=None, ws=None, stream=None):
+    """Grouped convolution + bias + ReLU (cct_conv_fwd_ex): x (b,n,n,d), w (o,k,k,d/groups),
+    bias (o) or None -> y (b,o,m,m) = act(conv + bias)."""
+    _need_cuda_f32(x, w, *([bias] if bias is not None else []))
+    m = desc.m
+    y = out if out is not None else torch.empty((desc.b, desc.o, m, m), dtype=torch.float32, device=x.device)
+    ext = _ext(groups, bias, relu)
+    buf = _ws(ws, x.device).get(_ws_ex(desc, lowering, ext, PASS_FWD))
+    check(lib().cct_conv_fwd_ex(C.byref(desc.c()), lowering, C.byref(ext), _ptr(x), _ptr(w), _ptr(y), _ptr(buf),
+                                buf.numel(), _stream(stream)))
+    return y
+
+
+def conv_bwd_ex(dy, w, desc: ConvDesc, lowering: int = LOWER_AUTO, groups: int = 1, relu: bool = False, x=None,
+                y=None, need_dx: bool = True, need_dw: bool = True, need_db: bool = False, ws=None, stream=None):
+    """Backward of conv_fwd_ex: dy is the gradient of the layer output y (post-ReLU; y is needed
+    when relu).  Returns (dx, dw, db), None for the gradients not requested."""
+    dev = dy.device
+    dx = torch.empty((desc.b, desc.n, desc.n, desc.d), dtype=torch.float32, device=dev) if need_dx else None
+    dw = torch.empty((desc.o, desc.k, desc.k, desc.d // groups), dtype=torch.float32, device=dev) if need_dw else None
+    db = torch.empty((desc.o,), dtype=torch.float32, device=dev) if need_db else None
+    ext = _ext(groups, None, relu)
+    pass_ = PASS_BWD if (need_dx and need_dw) else PASS_BWD_DATA if need_dx else PASS_BWD_WEIGHT
+    buf = _ws(ws, dev).get(_ws_ex(desc, lowering, ext, pass_))
+    check(lib().cct_conv_bwd_ex(C.byref(desc.c()), lowering, C.byref(ext), _ptr(x), _ptr(y), _ptr(dy), _ptr(w),
+                                _ptr(dx), _ptr(dw), _ptr(db), _ptr(buf), buf.numel(), _stream(stream)))
+    return dx, dw, db

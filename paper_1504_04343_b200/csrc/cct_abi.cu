@@ -20,6 +20,7 @@
 #include "lowering.cuh"
 #include "reduce.cuh"
 #include "s2d.cuh"
+#include "epilogue.cuh"
 
 namespace cct {
 uint64_t launch_count();
@@ -257,9 +258,16 @@ const float* dhat_of(const Geo& g, int type, const Lowered& L, const float* x, f
 // longer than the accumulation-chain cap (kMaxChainKB k-blocks) are split and
 // reduced in fp32 round-to-nearest (deterministic order).  In planning mode
 // (ws.base == nullptr) only the workspace is reserved.
-cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStream_t st, const char* what) {
+cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStream_t st, const char* what,
+                       bool* fused = nullptr) {
     const int64_t kb = (gp.K + kBK - 1) / kBK;
     const int splits = int((kb + kMaxChainKB - 1) / kMaxChainKB);
+    // a fused epilogue (bias / ReLU) applies to final stores only: not to split partials
+    if (fused) *fused = splits == 1;
+    if (splits > 1) {
+        gp.C.bias = nullptr;
+        gp.C.relu = 0;
+    }
     float* parts = splits > 1 ? ws.take(int64_t(splits) * span) : nullptr;
     gp.splits = splits;
     const size_t skb = gemm_workspace_bytes(gp);  // stream-K partial tiles
@@ -304,8 +312,23 @@ GemmProblem wgrad_problem(const Lowered& L, Operand a, Operand b) {
 // the three passes; ws.base == nullptr plans sizes only
 // ---------------------------------------------------------------------------
 
+// Extension options of a forward pass (cct_conv_fwd_ex): a channel group read
+// straight from a wider x (pixel stride xcs) and written into a wider y (image
+// stride ycs) -- implicit Type 1 only -- and the fused bias / ReLU epilogue
+// (applied by the GEMM when it writes y unsplit; `fused` reports whether it did).
+struct FwdOpts {
+    int64_t xcs = 0, ycs = 0;
+    const float* bias = nullptr;
+    int relu = 0;
+    bool* fused = nullptr;
+};
+
 cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
-                       cudaStream_t st) {
+                       cudaStream_t st, const FwdOpts& opts = FwdOpts{}) {
+    if (opts.fused) *opts.fused = false;
+    const bool strided = (opts.xcs && opts.xcs != g.d) || (opts.ycs && opts.ycs != g.o * g.m * g.m);
+    if (strided && !(type == 1 && t1_implicit(g, type, x) && !t1_s2d(g, type)))
+        return fail(CCT_ERR_UNSUPPORTED, "channel-group views need the implicit Type 1 path");
     if (t1_s2d(g, type)) {
         // blocked input (kept in the caller's lowered cache when given) and kernel bank
         const Geo v = s2d_geo(g);
@@ -332,18 +355,23 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
     gp.K = L.cols;
     gp.A = {dh, ldd, Major::K};
     gp.B = {wv, ldw, Major::K};
-    if (implicit) gp.im2col = im2col_of(g, x);
+    if (implicit) {
+        gp.im2col = im2col_of(g, x);
+        gp.im2col.cs = opts.xcs;
+    }
     float* rht = nullptr;
     float* out;
     int64_t span;
     if (type == 1) {
-        // lift_t1 is a reshape: write NCHW straight from the epilogue
+        // lift_t1 is a reshape: write NCHW straight from the epilogue (+ bias / ReLU)
         out = y;
-        span = g.b * g.o * g.m * g.m;
         gp.C.mdiv = g.m * g.m;
-        gp.C.s_mq = g.o * g.m * g.m;
+        gp.C.s_mq = opts.ycs ? opts.ycs : g.o * g.m * g.m;
         gp.C.s_mr = 1;
         gp.C.s_n = g.m * g.m;
+        gp.C.bias = opts.bias;
+        gp.C.relu = opts.relu;
+        span = (g.b - 1) * gp.C.s_mq + g.o * g.m * g.m;
     } else {
         rht = ws.take(L.ncols * L.ldr);
         out = rht;
@@ -351,7 +379,7 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
         gp.C.s_mr = 1;
         gp.C.s_n = L.ldr;
     }
-    cct_status s = gemm_capped(gp, out, span, ws, st, "gemm (fwd)");
+    cct_status s = gemm_capped(gp, out, span, ws, st, "gemm (fwd)", type == 1 ? opts.fused : nullptr);
     if (s != CCT_OK || !ws.base) return s;
     if (type != 1) CCT_TRY(lift(g, type, L.rm, rht, 1, L.ldr, y, st), "lift");
     return CCT_OK;
@@ -572,21 +600,28 @@ int64_t chunk_images(const Geo& g, int type, int pass) {
 }
 
 cct_status run_fwd(const Geo& g, int type, const float* x, const float* w, float* y, float* cache, Ws& ws,
-                   cudaStream_t st) {
+                   cudaStream_t st, const FwdOpts& opts = FwdOpts{}) {
     const int64_t cb = chunk_images(g, type, CCT_PASS_FWD);
-    if (cb == g.b) return run_fwd_one(g, type, x, w, y, cache, ws, st);
-    const int64_t per_x = g.n * g.n * g.d, per_y = g.o * g.m * g.m, per_c = cache_per_image(g, type);
+    if (cb == g.b) return run_fwd_one(g, type, x, w, y, cache, ws, st, opts);
+    const int64_t per_x = g.n * g.n * (opts.xcs ? opts.xcs : g.d), per_y = opts.ycs ? opts.ycs : g.o * g.m * g.m;
+    const int64_t per_c = cache_per_image(g, type);
     const size_t base = ws.off;
     size_t hi = base;
+    bool all_fused = true;
     for (int64_t q0 = 0; q0 < g.b; q0 += cb) {
         const Geo gc = with_batch(g, std::min(cb, g.b - q0));
         ws.off = base;
+        bool f = false;
+        FwdOpts oc = opts;
+        oc.fused = &f;
         cct_status s = run_fwd_one(gc, type, x + q0 * per_x, w, y ? y + q0 * per_y : nullptr,
-                                   cache ? cache + q0 * per_c : nullptr, ws, st);
+                                   cache ? cache + q0 * per_c : nullptr, ws, st, oc);
         if (s != CCT_OK) return s;
+        all_fused = all_fused && f;
         hi = std::max(hi, ws.off);
         if (!ws.base) break;  // planning: one chunk is representative
     }
+    if (opts.fused) *opts.fused = all_fused;
     ws.off = hi;
     return CCT_OK;
 }
@@ -615,6 +650,128 @@ cct_status run_bwd(const Geo& g, int type, const float* x, const float* cache, c
     }
     ws.off = hi;
     if (dw && ws.base) CCT_TRY(splitk_reduce(parts, wsize, int(nchunks), 1, wsize, wsize, dw, wsize, st), "chunk reduce");
+    return CCT_OK;
+}
+
+// ---------------------------------------------------------------------------
+// layer extension (cct_conv_*_ex): channel groups and the bias / ReLU epilogue
+// (SURVEY 8(f) item 3).  Group j of G convolves input channels [j d/G, (j+1) d/G)
+// with kernels [j o/G, (j+1) o/G) (KernelBank (o, k, k, d/G)).  Implicit Type 1
+// reads a group's channels straight from x and writes straight into y (TMA
+// im2col over a channel view, strided epilogue, fused bias / ReLU); the other
+// forms gather the group into contiguous scratch and scatter the result back.
+// ---------------------------------------------------------------------------
+struct Ext {
+    int64_t groups = 1;
+    const float* bias = nullptr;
+    int relu = 0;
+};
+
+Geo group_geo(const Geo& g, int64_t G) {
+    Geo v = g;
+    v.d = g.d / G;
+    v.o = g.o / G;
+    return v;
+}
+
+// the direct (no gather / scatter) grouped forward: implicit Type 1, one chain
+bool group_direct(const Geo& gg, int type) {
+    return type == 1 && t1_implicit(gg, type, kPlanPtr) && !t1_s2d(gg, type) &&
+           gg.k * gg.k * gg.d <= int64_t(kMaxChainKB) * kBK;
+}
+
+cct_status run_fwd_ex(const Geo& g, int type, const Ext& e, const float* x, const float* w, float* y, Ws& ws,
+                      cudaStream_t st) {
+    const int64_t G = e.groups, mm = g.m * g.m;
+    const Geo gg = group_geo(g, G);
+    const int64_t dg = gg.d, og = gg.o, wsz = og * g.k * g.k * dg;
+    if (G == 1 || group_direct(gg, type)) {
+        const size_t mark = ws.off;
+        size_t hi = mark;
+        for (int64_t j = 0; j < G; ++j) {
+            ws.off = mark;
+            bool fused = false;
+            FwdOpts o;
+            o.xcs = G > 1 ? g.d : 0;
+            o.ycs = G > 1 ? g.o * mm : 0;
+            o.bias = e.bias ? e.bias + j * og : nullptr;
+            o.relu = e.relu;
+            o.fused = &fused;
+            cct_status s = run_fwd(G > 1 ? gg : g, type, x + j * dg, w + j * wsz, y + j * og * mm, nullptr, ws, st, o);
+            if (s != CCT_OK) return s;
+            hi = std::max(hi, ws.off);
+            if (ws.base && !fused && (e.bias || e.relu))
+                CCT_TRY(bias_act(y + j * og * mm, o.bias, e.relu, g.b, og, mm, g.o, st), "bias / ReLU");
+            if (!ws.base) break;  // planning: every group needs the same scratch
+        }
+        ws.off = hi;
+        return CCT_OK;
+    }
+    float* xg = ws.take(g.b * g.n * g.n * dg);
+    float* yg = ws.take(g.b * og * mm);
+    const size_t mark = ws.off;
+    size_t hi = mark;
+    for (int64_t j = 0; j < G; ++j) {
+        ws.off = mark;
+        if (ws.base) CCT_TRY(copy2d(xg, dg, x + j * dg, g.d, dg, g.b * g.n * g.n, st), "gather channel group");
+        cct_status s = run_fwd(gg, type, or_plan(xg, ws), w + j * wsz, or_plan(yg, ws), nullptr, ws, st);
+        if (s != CCT_OK) return s;
+        hi = std::max(hi, ws.off);
+        if (!ws.base) break;
+        CCT_TRY(copy2d(y + j * og * mm, g.o * mm, yg, og * mm, og * mm, g.b, st), "scatter channel group");
+    }
+    ws.off = hi;
+    if (ws.base) CCT_TRY(bias_act(y, e.bias, e.relu, g.b, g.o, mm, g.o, st), "bias / ReLU");
+    return CCT_OK;
+}
+
+// dy is the gradient of the layer output (after the ReLU); y that output
+cct_status run_bwd_ex(const Geo& g, int type, const Ext& e, const float* x, const float* y, const float* dy,
+                      const float* w, float* dx, float* dw, float* db, Ws& ws, cudaStream_t st) {
+    const int64_t G = e.groups, mm = g.m * g.m;
+    const float* dz = dy;
+    if (e.relu || db) {
+        float* z = e.relu ? ws.take(g.b * g.o * mm) : nullptr;
+        float* partial = db ? ws.take(g.b * g.o) : nullptr;
+        if (ws.base) CCT_TRY(relu_bias_bwd(dy, y, z, db, partial, e.relu, g.b, g.o, mm, st), "ReLU / bias backward");
+        if (e.relu) dz = or_plan(z, ws);
+    }
+    if (!dx && !dw) return CCT_OK;
+    if (G == 1) return run_bwd(g, type, x, nullptr, dz, w, dx, dw, ws, st);
+    const Geo gg = group_geo(g, G);
+    const int64_t dg = gg.d, og = gg.o, wsz = og * g.k * g.k * dg;
+    float* zg = ws.take(g.b * og * mm);
+    float* xg = dw ? ws.take(g.b * g.n * g.n * dg) : nullptr;
+    float* dxg = dx ? ws.take(g.b * g.n * g.n * dg) : nullptr;
+    const size_t mark = ws.off;
+    size_t hi = mark;
+    for (int64_t j = 0; j < G; ++j) {
+        ws.off = mark;
+        if (ws.base) {
+            CCT_TRY(copy2d(zg, og * mm, dz + j * og * mm, g.o * mm, og * mm, g.b, st), "gather dy group");
+            if (dw) CCT_TRY(copy2d(xg, dg, x + j * dg, g.d, dg, g.b * g.n * g.n, st), "gather x group");
+        }
+        cct_status s = run_bwd(gg, type, dw ? or_plan(xg, ws) : nullptr, nullptr, or_plan(zg, ws), w + j * wsz,
+                               dx ? or_plan(dxg, ws) : nullptr, dw ? dw + j * wsz : nullptr, ws, st);
+        if (s != CCT_OK) return s;
+        hi = std::max(hi, ws.off);
+        if (!ws.base) break;
+        if (dx) CCT_TRY(copy2d(dx + j * dg, g.d, dxg, dg, dg, g.b * g.n * g.n, st), "scatter dx group");
+    }
+    ws.off = hi;
+    return CCT_OK;
+}
+
+cct_status check_ext(const cct_conv_desc* d, const cct_conv_ext* x, Ext* e) {
+    if (x) {
+        e->groups = x->groups;
+        e->bias = x->bias;
+        e->relu = x->relu;
+    }
+    if (e->groups < 1 || d->d % e->groups || d->o % e->groups)
+        return fail(CCT_ERR_CONFIG, "groups must be >= 1 and divide d and o " + desc_str(d));
+    if (e->relu != 0 && e->relu != 1) return fail(CCT_ERR_CONFIG, "relu must be 0 or 1");
+    if (e->bias && !aligned16(e->bias)) return fail(CCT_ERR_CONFIG, "bias must be 16-byte aligned");
     return CCT_OK;
 }
 
@@ -796,6 +953,88 @@ cct_status cct_conv_bwd(const cct_conv_desc* desc, cct_lowering lowering, const 
     if (dw && !x && !c) return fail(CCT_ERR_CONFIG, "bwd-weight needs x for this lowering");
     PassCtx pc(3);
     return run_bwd(g, type, x, c, dy, w, dx, dw, ws, as_stream(stream));
+}
+
+// ---- layer extension: groups, bias, ReLU ------------------
+
+static int resolve_ex(const cct_conv_desc* desc, const Ext& e, cct_lowering l, cct_pass pass) {
+    cct_conv_desc gd = *desc;  // the lowering choice is the group's (each group is one such layer)
+    gd.d /= e.groups;
+    gd.o /= e.groups;
+    return resolve(&gd, l, pass);
+}
+
+static cct_status plan_ex(const cct_conv_desc* desc, const Ext& e, int type, cct_pass pass, size_t* bytes) {
+    const Geo g = geo_of(desc);
+    const float* dummy = kPlanPtr;
+    float* dout = const_cast<float*>(kPlanPtr);
+    size_t most = 0;
+    for (int ctx : {int(pass) == CCT_PASS_BWD ? 3 : int(pass), 3}) {
+        PassCtx pc(ctx);
+        Ws ws(nullptr);
+        cct_status s;
+        if (pass == CCT_PASS_FWD) s = run_fwd_ex(g, type, e, dummy, dummy, dout, ws, nullptr);
+        else s = run_bwd_ex(g, type, e, dummy, dummy, dummy, dummy, pass != CCT_PASS_BWD_WEIGHT ? dout : nullptr,
+                            pass != CCT_PASS_BWD_DATA ? dout : nullptr, dout, ws, nullptr);
+        if (s != CCT_OK) return s;
+        most = std::max(most, ws.off);
+    }
+    *bytes = most + 256;
+    return CCT_OK;
+}
+
+cct_status cct_workspace_size_ex(const cct_conv_desc* desc, cct_lowering lowering, const cct_conv_ext* ext,
+                                 cct_pass pass, size_t* bytes) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    Ext e;
+    if ((s = check_ext(desc, ext, &e)) != CCT_OK) return s;
+    if (!bytes) return fail(CCT_ERR_CONFIG, "null size pointer");
+    if (int(pass) < CCT_PASS_FWD || int(pass) > CCT_PASS_BWD) return fail(CCT_ERR_CONFIG, "unknown pass");
+    return plan_ex(desc, e, resolve_ex(desc, e, lowering, pass), pass, bytes);
+}
+
+cct_status cct_conv_fwd_ex(const cct_conv_desc* desc, cct_lowering lowering, const cct_conv_ext* ext, const float* x,
+                           const float* w, float* y, void* wsp, size_t ws_bytes, void* stream) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    Ext e;
+    if ((s = check_ext(desc, ext, &e)) != CCT_OK) return s;
+    if ((s = check_ptrs({x, w, y})) != CCT_OK) return s;
+    if (!aligned16(x) || !aligned16(w) || !aligned16(y))
+        return fail(CCT_ERR_CONFIG, "tensor pointers must be 16-byte aligned");
+    const int type = resolve_ex(desc, e, lowering, CCT_PASS_FWD);
+    size_t need = 0;
+    if ((s = plan_ex(desc, e, type, CCT_PASS_FWD, &need)) != CCT_OK) return s;
+    if (!wsp || ws_bytes < need) return fail(CCT_ERR_RESOURCE, "workspace too small for " + desc_str(desc));
+    Ws ws(wsp);
+    PassCtx pc(CCT_PASS_FWD);
+    return run_fwd_ex(geo_of(desc), type, e, x, w, y, ws, as_stream(stream));
+}
+
+cct_status cct_conv_bwd_ex(const cct_conv_desc* desc, cct_lowering lowering, const cct_conv_ext* ext, const float* x,
+                           const float* y, const float* dy, const float* w, float* dx, float* dw, float* db,
+                           void* wsp, size_t ws_bytes, void* stream) {
+    cct_status s = check_desc(desc);
+    if (s != CCT_OK) return s;
+    Ext e;
+    if ((s = check_ext(desc, ext, &e)) != CCT_OK) return s;
+    if (!dy || (!dx && !dw && !db)) return fail(CCT_ERR_CONFIG, "cct_conv_bwd_ex needs dy and one of dx, dw, db");
+    if (dx && !w) return fail(CCT_ERR_CONFIG, "bwd-data needs w");
+    if (dw && !x) return fail(CCT_ERR_CONFIG, "bwd-weight needs x");
+    if (e.relu && !y) return fail(CCT_ERR_CONFIG, "the ReLU backward needs the layer output y");
+    for (const void* p : {static_cast<const void*>(x), static_cast<const void*>(y), static_cast<const void*>(dy),
+                          static_cast<const void*>(w), static_cast<const void*>(dx), static_cast<const void*>(dw),
+                          static_cast<const void*>(db)})
+        if (p && !aligned16(p)) return fail(CCT_ERR_CONFIG, "tensor pointers must be 16-byte aligned");
+    const cct_pass pass = dx && dw ? CCT_PASS_BWD : dx ? CCT_PASS_BWD_DATA : CCT_PASS_BWD_WEIGHT;
+    const int type = resolve_ex(desc, e, lowering, pass);
+    size_t need = 0;
+    if ((s = plan_ex(desc, e, type, pass, &need)) != CCT_OK) return s;
+    if (!wsp || ws_bytes < need) return fail(CCT_ERR_RESOURCE, "workspace too small for " + desc_str(desc));
+    Ws ws(wsp);
+    PassCtx pc(int(pass));
+    return run_bwd_ex(geo_of(desc), type, e, x, y, dy, w, dx, dw, db, ws, as_stream(stream));
 }
 
 // ---- phase-level API ---------------------------------------------------------

@@ -47,6 +47,8 @@ struct KParams {
     int* sk_cnt;
     int64_t s_nq;
     int64_t mlim;
+    const float* bias;  // fused epilogue: v = act(v + bias[n])
+    int relu;
     // implicit (im2col) A: layer geometry (ic_d = channels per tap of the lowered index)
     int ic_d, ic_k, ic_s, ic_p, ic_m, ic_mm, ic_cpt;
 };
@@ -426,10 +428,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             const int n0 = nt * BN;
             // final values of columns n0 + c0 .. +31 of this thread's row -> output map
-            auto store32 = [&](const uint32_t* v, int c0) {
+            auto store32 = [&](uint32_t* v, int c0) {
                 const int64_t sn = p.s_n;
                 const int nlim = p.N - (n0 + c0);
                 if (!row_ok) return;
+                if (p.bias || p.relu) {  // fused bias + ReLU (conv layer epilogue)
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        float f = __uint_as_float(v[j]);
+                        if (p.bias && j < nlim) f += __ldg(p.bias + n0 + c0 + j);
+                        if (p.relu) f = fmaxf(f, 0.f);
+                        v[j] = __float_as_uint(f);
+                    }
+                }
                 if (p.ndiv) {
                     // two-level column map (slab-major dDhat): walk (n / ndiv, n % ndiv)
                     const int nq = (n0 + c0) / p.ndiv;
@@ -658,8 +669,9 @@ PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
 bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major) {
     auto enc = encode_im2col_fn();
     if (!enc) return false;
+    const int64_t cs = ic.cs ? ic.cs : ic.d;  // channel group of a wider tensor: extent d, stride cs
     cuuint64_t dims[4] = {cuuint64_t(ic.d), cuuint64_t(ic.n), cuuint64_t(ic.n), cuuint64_t(ic.b)};
-    cuuint64_t strides[3] = {cuuint64_t(ic.d) * 4, cuuint64_t(ic.n * ic.d) * 4, cuuint64_t(ic.n * ic.n * ic.d) * 4};
+    cuuint64_t strides[3] = {cuuint64_t(cs) * 4, cuuint64_t(ic.n * cs) * 4, cuuint64_t(ic.n * ic.n * cs) * 4};
     int lower[2] = {int(-ic.p), int(-ic.p)};
     int upper[2] = {int(ic.p - (ic.k - 1)), int(ic.p - (ic.k - 1))};
     cuuint32_t estr[4] = {1, cuuint32_t(ic.s), cuuint32_t(ic.s), 1};
@@ -674,7 +686,7 @@ bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major) {
     // the second descriptor word is cleared (same workaround as CUTLASS).
     int drv = 0;
     cudaDriverGetVersion(&drv);
-    if (drv <= 13010 && ic.b * ic.n * ic.n * ic.d * 4 < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
+    if (drv <= 13010 && ic.b * ic.n * ic.n * cs * 4 < 131072) reinterpret_cast<uint64_t*>(map)[1] &= ~(1ull << 21);
     return true;
 }
 
@@ -873,6 +885,8 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.ndiv = g.C.ndiv < (int64_t(1) << 31) ? int(g.C.ndiv) : 0;
     kp.s_nq = g.C.s_nq;
     kp.mlim = g.C.mlim;
+    kp.bias = g.C.bias;
+    kp.relu = g.C.relu;
 
     const int cg = choose_cg(g, bn);
     kp.num_m_tiles = int((g.M + kBM * cg - 1) / (kBM * cg));

@@ -27,6 +27,9 @@ struct OutMap {
     int64_t s_mq = 0, s_mr = 1, s_n = 0, s_split = 0;
     int64_t ndiv = INT64_MAX, s_nq = 0;
     int64_t mlim = INT64_MAX;  // rows with (m % mdiv) >= mlim are not stored (padded channels)
+    // fused epilogue (final stores only): v = act(v + bias[n]), act = ReLU when relu != 0
+    const float* bias = nullptr;
+    int relu = 0;
 };
 
 // Implicit Type 1 lowering: operand A is read straight from the NHWC input x
@@ -44,6 +47,7 @@ struct Im2col {
     const float* x = nullptr;  // nullptr: A is an ordinary (materialised) matrix
     int64_t b = 0, n = 0, d = 0, k = 0, s = 1, p = 0, m = 0;
     int64_t dk = 0;
+    int64_t cs = 0;  // channel stride of a pixel in x (0: = d); > d reads one channel group
 };
 
 struct GemmProblem {
