@@ -23,7 +23,8 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libcct.so")
+# $CCT_LIB_DIR selects another in-tree build of libcct.so (A/B profiling of kernel variants)
+LIB_PATH = os.path.join(os.environ.get("CCT_LIB_DIR", os.path.join(_HERE, "_lib")), "libcct.so")
 
 LOWER_AUTO, LOWER_T1, LOWER_T2, LOWER_T3 = 0, 1, 2, 3
 PASS_FWD, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_BWD = 0, 1, 2, 3

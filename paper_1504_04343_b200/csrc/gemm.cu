@@ -54,7 +54,15 @@ struct KParams {
 };
 
 // warps 0-3 control (TMA, MMA, TMEM alloc, spare), 4-7 epilogue, 8.. transform
-constexpr int kTransformWarps = 4;
+#ifndef KTGROUPS
+#define KTGROUPS 2
+#endif
+// Transform warps run as kTGroups groups of 4 that take alternate k-blocks, so the
+// per-stage latency chain (ld.shared -> split -> st.shared / tcgen05.st -> proxy
+// fence -> barrier arrive) of one group overlaps the next group's (measured: one
+// group of 4 bounded narrow tiles at ~820 clocks per k-block).
+constexpr int kTGroups = KTGROUPS;
+constexpr int kTransformWarps = 4 * kTGroups;
 constexpr int kThreads = 256 + 32 * kTransformWarps;
 
 __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
@@ -208,7 +216,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::prefetch_tmap(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(&full[s], 1);
-            ptx::mbar_init(&tdone[s], kTransformWarps * CG);  // transform warps of every CTA in the group
+            ptx::mbar_init(&tdone[s], 4 * CG);  // one transform group of every CTA in the group
             ptx::mbar_init(&empty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
@@ -535,7 +543,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
     } else if (warp >= 8) {
         // ===================== 3xTF32 transform (own tiles) =====================
-        const int t = threadIdx.x - 256;
+        const int tg = (warp - 8) >> 2;                   // transform group: k-blocks gi % kTGroups == tg
+        const int t = threadIdx.x - 256 - tg * 128;
         int stage = 0;
         uint32_t phase = 0;
         uint32_t gi = 0;
@@ -543,6 +552,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         Work w;
         while (wi.next(p, ngroups, w)) {
             for (int kb = w.kb0; kb < w.kb1; ++kb, ++gi) {
+                if (int(gi % kTGroups) != tg) {
+                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    continue;
+                }
                 ptx::mbar_wait(&full[stage], phase);
                 const uint32_t raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
                 if constexpr (A_TM) {
@@ -573,7 +586,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::tmem_st_wait();
                     // B small part in smem as usual
                     constexpr int b0 = C_::A_BYTES / 16, b1 = C_::RAW_BYTES / 16;
-                    for (int i = b0 + t; i < b1; i += 32 * kTransformWarps) {
+                    for (int i = b0 + t; i < b1; i += 128) {
                         const float4 x = ptx::lds128(raw + i * 16);
                         ptx::sts128(raw + C_::RAW_BYTES + i * 16, small_part(x));
                     }
@@ -582,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 } else if (p.passes == 3) {
                     constexpr int n4 = C_::RAW_BYTES / 16;
 #pragma unroll 4
-                    for (int i = t; i < n4; i += 32 * kTransformWarps) {
+                    for (int i = t; i < n4; i += 128) {
                         const float4 v = ptx::lds128(raw + i * 16);
                         ptx::sts128(raw + C_::RAW_BYTES + i * 16, small_part(v));
                     }

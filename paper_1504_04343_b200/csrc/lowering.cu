@@ -9,6 +9,7 @@
 
 #include "common.cuh"
 #include "lowering.cuh"
+#include "ptx.cuh"
 
 namespace cct {
 
@@ -59,6 +60,7 @@ __device__ __forceinline__ void cp_async16(float* smem_dst, const float* gsrc) {
                  : "memory");
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 
 // One warp per lowered row (q, y, c).  The row is `nruns` runs of L source
 // floats that are contiguous in x (T1: k runs of k*d; T2: 1 run of k*d; T3: 1
@@ -353,15 +355,19 @@ __global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restr
 // slab-major (col2im_slab_layout): slab (q, r, i) = the m x k*d block of rows
 // (q, r, c) and filter row i, contiguous and 16-byte aligned (stride S floats),
 // as the backward-data GEMM epilogue writes it.  The (r, i) slabs with
-// s*r + i == y + p are staged with 16-byte async copies, then every dx element
-// of the row sums its taps from smem using per-element tap metadata built once.
-// Each dDhat element is read once.
+// s*r + i == y + p are staged by bulk (TMA engine) copies completing on an
+// mbarrier, then every dx element of the row sums its taps from smem using
+// per-element tap metadata built once (NP: compile-time bound on the slab and tap
+// counts, ceil(k / s), so the sums unroll into predicated adds).  Each dDhat
+// element is read once.
+template <int NP>
 __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t S, float* __restrict__ dx, Geo g) {
     extern __shared__ __align__(16) float sm[];
+    __shared__ __align__(8) uint64_t full[2];
     const int n = int(g.n), d = int(g.d), k = int(g.k), s = int(g.s), p = int(g.p), m = int(g.m);
     const int kd = k * d;
     const int npair_max = (k + s - 1) / s;
-    int* meta = reinterpret_cast<int*>(sm + npair_max * S);  // n*d: tap run per output
+    int* meta = reinterpret_cast<int*>(sm + 2 * npair_max * S);  // n*d: tap run per output
     // per dx column element: slab offset of its first valid tap (c < m) and the
     // number of taps (j = j0 + t s, c = c0 - t, 0 <= c < m, j < k): branch-free sums
     for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
@@ -373,34 +379,70 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t S, f
         const int off = (cnt > 0) ? c * kd + j * d + ch : 0;
         meta[e] = off | (cnt << 24);                // off < 2^24 (slab <= 96 KiB)
     }
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&full[0], 1);
+        ptx::mbar_init(&full[1], 1);
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
     const int64_t nqy = g.b * n;
-    const int S4 = int(S / 4);
-    for (int64_t qy = blockIdx.x; qy < nqy; qy += gridDim.x) {
-        const int yy = int(qy % n);
-        const int64_t q = qy / n;
-        const int py = yy + p;
-        // pairs (r, i), ascending i: r from min(m-1, py/s) down while i = py - s r < k
+    const uint32_t slab_bytes = uint32_t(S) * 4u;
+    // slabs (r, i) of dx row qy, ascending i: r from min(m-1, py/s) down while i = py - s r < k
+    auto pairs = [&](int64_t row, int* rtop_out) {
+        const int py = int(row % n) + p;
         const int rtop = min(m - 1, py / s);
         int np = 0;
         while (np < npair_max && rtop - np >= 0 && py - s * (rtop - np) < k) ++np;
-        __syncthreads();  // previous slabs consumed
+        *rtop_out = rtop;
+        return np;
+    };
+    // double-buffered: the slabs of the CTA's next row load while this row is summed
+    auto issue = [&](int64_t row, int buf) {
+        int rtop;
+        const int np = pairs(row, &rtop);
+        if (np == 0) return;
+        const int py = int(row % n) + p;
+        const int64_t q = row / n;
+        ptx::mbar_arrive_expect_tx(&full[buf], uint32_t(np) * slab_bytes);
         for (int a = 0; a < np; ++a) {
             const int r = rtop - a, i = py - s * r;
-            const float* src = dd + ((q * m + r) * int64_t(k) + i) * S;
-            float* dst = sm + a * S;
-            for (int e = threadIdx.x; e < S4; e += blockDim.x) cp_async16(dst + 4 * e, src + 4 * e);
+            ptx::bulk_load(sm + (buf * npair_max + a) * S, dd + ((q * m + r) * int64_t(k) + i) * S, slab_bytes,
+                           &full[buf]);
         }
-        cp_async_wait_all();
-        __syncthreads();
+    };
+    uint32_t phase[2] = {0, 0};
+    if (threadIdx.x == 0 && blockIdx.x < nqy) issue(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t qy = blockIdx.x; qy < nqy; qy += gridDim.x, ++it) {
+        const int buf = it & 1;
+        __syncthreads();  // every thread is done with the other buffer (previous row)
+        if (threadIdx.x == 0 && qy + gridDim.x < nqy) issue(qy + gridDim.x, buf ^ 1);
+        int rtop;
+        const int np = pairs(qy, &rtop);
+        if (np > 0) {
+            ptx::mbar_wait(&full[buf], phase[buf]);
+            phase[buf] ^= 1;
+        }
+        const float* slabs = sm + buf * npair_max * S;
         float* out = dx + qy * int64_t(n) * d;
         const int delta = s * d - kd;  // slab step from tap t to t + 1
         for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
             const int mt = meta[e];
             const int off = mt & 0xFFFFFF, cnt = mt >> 24;
             float acc = 0.f;
-            for (int a = 0; a < np; ++a) {
-                const float* sl = sm + a * S + off;
-                for (int t = 0; t < cnt; ++t) acc += sl[t * delta];
+            if constexpr (NP > 0) {
+#pragma unroll
+                for (int a = 0; a < NP; ++a) {
+                    const float* sl = slabs + a * S + off;
+#pragma unroll
+                    for (int t = 0; t < NP; ++t)
+                        if (a < np && t < cnt) acc += sl[t * delta];
+                }
+            } else {
+                for (int a = 0; a < np; ++a) {
+                    const float* sl = slabs + a * S + off;
+                    for (int t = 0; t < cnt; ++t) acc += sl[t * delta];
+                }
             }
             out[e] = acc;
         }
@@ -532,7 +574,7 @@ bool col2im_slab_layout(const Geo& g, int type) {
     if (type != 1 || g.d % 4 == 0 || g.d >= 256 || g.s >= 256) return false;
     const int64_t S = slab_stride(g);
     const int64_t npair = (g.k + g.s - 1) / g.s;
-    return (npair * S + g.n * g.d) * 4 <= 96 * 1024;
+    return (2 * npair * S + g.n * g.d) * 4 <= 96 * 1024;  // double-buffered slabs
 }
 
 int64_t slab_stride(const Geo& g) { return rup4(g.m * g.k * g.d); }
@@ -546,12 +588,14 @@ cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* d
         if (ld != slab_stride(g) || reinterpret_cast<uintptr_t>(dd) % 16) return cudaErrorInvalidValue;
         static bool attr = false;
         if (!attr) {
-            cudaFuncSetAttribute(col2im_t1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(col2im_t1_smem_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            cudaFuncSetAttribute(col2im_t1_smem_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
             attr = true;
         }
-        const size_t smem1 = size_t(((g.k + g.s - 1) / g.s) * ld + g.n * g.d) * 4;
+        const size_t smem1 = size_t(2 * ((g.k + g.s - 1) / g.s) * ld + g.n * g.d) * 4;
         const int grid1 = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * 4));
-        col2im_t1_smem_kernel<<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
+        if ((g.k + g.s - 1) / g.s <= 3) col2im_t1_smem_kernel<3><<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
+        else col2im_t1_smem_kernel<0><<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
         note_launch();
         return cudaGetLastError();
     }
