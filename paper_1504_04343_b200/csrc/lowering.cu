@@ -481,31 +481,36 @@ __global__ void transpose_kernel(const float* __restrict__ src, int64_t rows, in
 // Batched transpose: for z < nz, dst[z*dst_z + c*ldd + r] = src[z*src_z + r*lds + c]
 // (rows x cols -> cols x rows).  32 x 32 tiles through padded smem; 256 threads,
 // each moving 4 elements per tile, so reads and writes are both 128-byte rows.
-__global__ void transpose_batched_kernel(const float* __restrict__ src, int rows, int cols, int64_t lds,
-                                         int64_t src_z, float* __restrict__ dst, int64_t ldd, int64_t dst_z,
-                                         int nz) {
-    __shared__ float tile[32][33];
-    const int tr = (rows + 31) >> 5, tc = (cols + 31) >> 5;
+template <int TR>
+__global__ void __launch_bounds__(256) transpose_batched_kernel(const float* __restrict__ src, int rows, int cols,
+                                                                int64_t lds, int64_t src_z, float* __restrict__ dst,
+                                                                int64_t ldd, int64_t dst_z, int nz) {
+    // TR x 32 tiles: each thread keeps TR / 8 loads in flight (latency-bound at TR = 32)
+    __shared__ float tile[TR][33];
+    const int tr = (rows + TR - 1) / TR, tc = (cols + 31) >> 5;
     const int64_t per_z = int64_t(tr) * tc;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     for (int64_t t = blockIdx.x; t < per_z * nz; t += gridDim.x) {
         const int z = int(t / per_z);
         const int rem = int(t - int64_t(z) * per_z);
-        const int r0 = (rem / tc) << 5, c0 = (rem % tc) << 5;
+        const int r0 = (rem / tc) * TR, c0 = (rem % tc) << 5;
         const float* s = src + int64_t(z) * src_z;
         float* d = dst + int64_t(z) * dst_z;
         const int c = c0 + tx;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < TR / 8; ++i) {
             const int r = r0 + ty + 8 * i;
-            tile[ty + 8 * i][tx] = (r < rows && c < cols) ? __ldg(s + int64_t(r) * lds + c) : 0.f;
+            tile[ty + 8 * i][tx] = (r < rows && c < cols) ? __ldcs(s + int64_t(r) * lds + c) : 0.f;
         }
         __syncthreads();
-        const int r = r0 + tx;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int cc = c0 + ty + 8 * i;
-            if (r < rows && cc < cols) d[int64_t(cc) * ldd + r] = tile[tx][ty + 8 * i];
+        for (int h = 0; h < TR / 32; ++h) {
+            const int r = r0 + 32 * h + tx;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int cc = c0 + ty + 8 * i;
+                if (r < rows && cc < cols) d[int64_t(cc) * ldd + r] = tile[32 * h + tx][ty + 8 * i];
+            }
         }
         __syncthreads();
     }
@@ -630,9 +635,17 @@ cudaError_t transpose_batched(const float* src, int64_t rows, int64_t cols, int6
     if (rows >= (int64_t(1) << 31) || cols >= (int64_t(1) << 31) || nz >= (int64_t(1) << 31))
         return cudaErrorInvalidConfiguration;
     PhaseScope ps(Phase(phase), st, 0, 8.0 * double(rows * cols * nz));
-    const int64_t tiles = cdiv(rows, 32) * cdiv(cols, 32) * nz;
-    const int grid = int(std::min<int64_t>(tiles, int64_t(num_sms()) * 8));
-    transpose_batched_kernel<<<grid, 256, 0, st>>>(src, int(rows), int(cols), lds, src_z, dst, ldd, dst_z, int(nz));
+    if (rows >= 128) {
+        const int64_t tiles = cdiv(rows, 128) * cdiv(cols, 32) * nz;
+        const int grid = int(std::min<int64_t>(tiles, int64_t(num_sms()) * 8));
+        transpose_batched_kernel<128><<<grid, 256, 0, st>>>(src, int(rows), int(cols), lds, src_z, dst, ldd, dst_z,
+                                                            int(nz));
+    } else {
+        const int64_t tiles = cdiv(rows, 32) * cdiv(cols, 32) * nz;
+        const int grid = int(std::min<int64_t>(tiles, int64_t(num_sms()) * 8));
+        transpose_batched_kernel<32><<<grid, 256, 0, st>>>(src, int(rows), int(cols), lds, src_z, dst, ldd, dst_z,
+                                                           int(nz));
+    }
     note_launch();
     return cudaGetLastError();
 }

@@ -11,7 +11,7 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
-        if "cct" not in d["Kernel Name"] and "--all" not in sys.argv:
+        if "cct" not in d["Kernel Name"] and "unnamed>" not in d["Kernel Name"] and "--all" not in sys.argv:
             continue
         key = (int(d["ID"]), d["Kernel Name"].split("(")[0].replace("void ", "").replace("cct::<unnamed>::", ""))
         agg.setdefault(key, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
