@@ -255,7 +255,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 Pix px{};      // forward: first pixel of the tile; bwd-weight: pixel of k0
                 int tap_i = 0, tap_j = 0, cc = 0;   // forward: filter tap and channel block of kb
                 int bw_ch[kBM / 32], bw_ti[kBM / 32], bw_tj[kBM / 32];  // bwd-weight: per 32-row box
-                if constexpr (A_IM && !A_MN) {
+                if constexpr (A_IM == 2) {  // B = im2col: the tile's pixels are its N index
+                    px = pix_of(n0, p);
+                    const int tap = kb0 / p.ic_cpt;
+                    cc = kb0 - tap * p.ic_cpt;
+                    tap_i = tap / p.ic_k;
+                    tap_j = tap - tap_i * p.ic_k;
+                } else if constexpr (A_IM && !A_MN) {
                     px = pix_of(m0, p);
                     const int tap = kb0 / p.ic_cpt;
                     cc = kb0 - tap * p.ic_cpt;
@@ -279,7 +285,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint8_t* a_dst = smem + stage * C_::STAGE_BYTES;
                     uint8_t* b_dst = a_dst + C_::A_BYTES;
                     const int k0 = kb * kBK;
-                    if constexpr (A_IM && !A_MN) {
+                    if constexpr (A_IM == 2) {
+                        // A: ordinary K-major tile (kernel bank rows); B: BNL pixels x 16 channels of tap (ti, tj)
+                        ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+                        ptx::tma_load_im2col_4d(b_dst, &tmB, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
+                                                p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
+                        if (++cc == p.ic_cpt) {
+                            cc = 0;
+                            if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
+                        }
+                    } else if constexpr (A_IM && !A_MN) {
                         // implicit lowering, forward: 128 pixels x 16 channels of filter tap (ti, tj)
                         ptx::tma_load_im2col_4d(a_dst, &tmA, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
                                                 p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
@@ -306,7 +321,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                         for (int c = 0; c < kBM / 32; ++c)
                             ptx::tma_load_2d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], m0 + 32 * c, k0);
                     }
-                    if constexpr (!B_MN) {
+                    if constexpr (A_IM == 2) {
+                        // B issued above (im2col)
+                    } else if constexpr (!B_MN) {
                         ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
                     } else {
 #pragma unroll
@@ -679,7 +696,7 @@ PFN_cuTensorMapEncodeIm2col_v12000 encode_im2col_fn() {
 
 // NHWC input as a 4D (c, w, h, n) im2col map: bounding box lower corner -p,
 // upper corner p - (k - 1), traversal stride s (output pixels along W, H, N).
-bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major) {
+bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major, int box_pixels = kBM) {
     auto enc = encode_im2col_fn();
     if (!enc) return false;
     const int64_t cs = ic.cs ? ic.cs : ic.d;  // channel group of a wider tensor: extent d, stride cs
@@ -689,7 +706,7 @@ bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major) {
     int upper[2] = {int(ic.p - (ic.k - 1)), int(ic.p - (ic.k - 1))};
     cuuint32_t estr[4] = {1, cuuint32_t(ic.s), cuuint32_t(ic.s), 1};
     const cuuint32_t chans = mn_major ? 32 : kBK;
-    const cuuint32_t pixels = mn_major ? kBK : kBM;
+    const cuuint32_t pixels = mn_major ? kBK : cuuint32_t(box_pixels);
     CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<float*>(ic.x), dims, strides, lower, upper,
                      chans, pixels, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                      mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_64B,
@@ -749,7 +766,7 @@ cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const C
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
     if constexpr (BN <= 96) {
-        const int atm = a_in_tmem_mode();
+        const int atm = g.im2col.operand == 1 ? 0 : a_in_tmem_mode();
         if (!amn && g.passes == 3 && atm == 2) {
             if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 2>(ta, tb, kp, st);
             return bmn ? launch<BN, 0, 1, CG, 0, 2>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 2>(ta, tb, kp, st);
@@ -758,6 +775,10 @@ cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const C
             if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 1>(ta, tb, kp, st);
             return bmn ? launch<BN, 0, 1, CG, 0, 1>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 1>(ta, tb, kp, st);
         }
+    }
+    if (g.im2col.x && g.im2col.operand == 1) {  // B = im2col (swapped implicit GEMM), K-major A and B
+        if (amn || bmn) return cudaErrorInvalidValue;
+        return launch<BN, 0, 0, CG, 2>(ta, tb, kp, st);
     }
     if (g.im2col.x) {  // implicit Type 1: forward / backward-data (K, K), backward-weight (MN, K|MN)
         if (!amn && !bmn) return launch<BN, 0, 0, CG, 1>(ta, tb, kp, st);
@@ -916,6 +937,7 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
         }
     }
     CUtensorMap ta, tb;
+    const bool b_im = g.im2col.x && g.im2col.operand == 1;
     if (g.im2col.x) {
         const Im2col& ic = g.im2col;
         const bool amn = g.A.major == Major::MN;
@@ -928,11 +950,17 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
         kp.ic_m = int(ic.m);
         kp.ic_mm = int(ic.m * ic.m);
         kp.ic_cpt = int(dk / kBK);
-        if (!make_tmap_im2col(&ta, ic, amn)) return cudaErrorInvalidValue;
+        if (b_im) {
+            if (amn || g.B.major == Major::MN || !make_tmap_im2col(&tb, ic, false, bn / cg) ||
+                !make_tmap(&ta, g.A, g.M, g.K, kBM))
+                return cudaErrorInvalidValue;
+        } else if (!make_tmap_im2col(&ta, ic, amn)) {
+            return cudaErrorInvalidValue;
+        }
     } else if (!make_tmap(&ta, g.A, g.M, g.K, kBM)) {
         return cudaErrorInvalidValue;
     }
-    if (!make_tmap(&tb, g.B, g.N, g.K, bn / cg)) return cudaErrorInvalidValue;
+    if (!b_im && !make_tmap(&tb, g.B, g.N, g.K, bn / cg)) return cudaErrorInvalidValue;
     if (cg == 2) {
         switch (bn) {
         case 256: return dispatch_layout<256, 2>(g, ta, tb, kp, stream);

@@ -48,6 +48,7 @@ struct Im2col {
     int64_t b = 0, n = 0, d = 0, k = 0, s = 1, p = 0, m = 0;
     int64_t dk = 0;
     int64_t cs = 0;  // channel stride of a pixel in x (0: = d); > d reads one channel group
+    int operand = 0; // 0: A = im2col(x) (M = pixels); 1: B = im2col(x) (N = pixels, K-major; swapped GEMM)
 };
 
 struct GemmProblem {
