@@ -114,13 +114,16 @@ CCT_API void cct_set_workspace_limit(size_t bytes);
 CCT_API size_t cct_get_workspace_limit(void);
 
 /* Implicit Type 1 lowering (the paper's "fusion").
- * mode 1 (default; $CCT_IMPLICIT): for Type 1 layers with d % 32 == 0 the
+ * mode 1 (default; $CCT_IMPLICIT): for Type 1 layers with d % 16 == 0 the
  *   forward and backward-weight GEMMs read their lowered operand straight from
- *   x through TMA im2col tiles -- Dhat never exists in HBM (bit-identical to
- *   the materialised path).  At stride 1 with o % 16 == 0, backward-data runs
- *   as the forward convolution of dy (transposed to NHWC) with the rotated
- *   kernel bank, written straight to dx (no dDhat, no col2im), whenever the
- *   cost model predicts that faster.
+ *   x through TMA im2col tiles -- Dhat never exists in HBM (the forward is
+ *   bit-identical to the materialised path).  At stride 1 with o % 16 == 0,
+ *   backward-data runs as the forward convolution of dy (transposed to NHWC)
+ *   with the rotated kernel bank, written straight to dx (no dDhat, no col2im;
+ *   swapped, pixels as the wide tile side, when d < 128), whenever the cost
+ *   model predicts that faster.  A strided layer with s^2 d % 16 == 0 may run
+ *   as the stride-1 convolution of its space-to-depth blocked input (cost
+ *   model, per pass); the lowered cache then holds the blocked input.
  * mode 2: every implicit form whenever possible (tests).
  * mode 0: everything materialised. */
 CCT_API void cct_set_implicit_lowering(int mode);
