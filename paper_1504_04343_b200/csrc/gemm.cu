@@ -72,17 +72,20 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
 // Per-CTA tile geometry.  CG = 1: one CTA computes 128 x BN.  CG = 2 (CTA
 // pair, tcgen05 cta_group::2): the pair computes 256 x BN; each CTA holds its
 // 128 rows of A and BN/2 rows of B in smem and its 128 rows of D in TMEM.
-template <int BN, int CG>
+template <int BN, int CG, int TRO = 0>
 struct Cfg {
     static constexpr int BNL = BN / CG;  // B rows loaded by this CTA
     static constexpr uint32_t A_BYTES = kBM * kBK * 4;
     static constexpr uint32_t B_BYTES = BNL * kBK * 4;
     static constexpr uint32_t RAW_BYTES = A_BYTES + B_BYTES;
     static constexpr uint32_t STAGE_BYTES = 2 * RAW_BYTES;  // raw | small
+    // transposing epilogue (TRO): one 32 x 33 fp32 staging block per epilogue warp
+    static constexpr uint32_t EPI_BYTES = TRO ? 4 * 32 * 33 * 4 + 4 * 32 * 16 : 0;
     // as many ring stages as fit next to the barriers (227 KB opt-in smem per CTA)
-    static constexpr int STAGES = ((225 * 1024) / STAGE_BYTES) > 12 ? 12 : ((225 * 1024) / STAGE_BYTES);
+    static constexpr int BUDGET = 225 * 1024 - int(EPI_BYTES);
+    static constexpr int STAGES = (BUDGET / int(STAGE_BYTES)) > 12 ? 12 : (BUDGET / int(STAGE_BYTES));
     static constexpr uint32_t BAR_BYTES = (3 * STAGES + 4) * 8 + 16;
-    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 1024;
+    static constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + EPI_BYTES + 1024;
     // Narrow tiles keep two sub-accumulators per tile (even / odd 8-wide K steps):
     // consecutive MMAs then target different TMEM regions and overlap instead of
     // serialising on one accumulator (measured: N=96 MMAs were latency-bound).
@@ -175,11 +178,15 @@ struct WorkIter {
 // transform warps read each A row once from smem and write its big / small parts
 // to a 4-slot TMEM ring, so the three MMAs of a K step read only B from shared
 // memory (for N <= 96 the A reads otherwise saturate the smem bus, ncu).
-template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0>
+// TRO: transposing epilogue -- each warp stages its 32 rows x 32 columns chunk in
+// smem and writes it back column by column, so an output whose ROWS are contiguous
+// along the tile's N index (NCHW y of a swapped GEMM: rows = channels, columns =
+// pixels) is stored as 128-byte row segments instead of 4-byte scatters.
+template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0, int TRO = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const KParams p) {
-    using C_ = Cfg<BN, CG>;
+    using C_ = Cfg<BN, CG, TRO>;
     constexpr int STAGES = C_::STAGES;
     constexpr int BNL = C_::BNL;
     // A_TM == 2: one accumulator per tile, the freed TMEM columns deepen the A ring
@@ -202,6 +209,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
+    float* epi = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + ((C_::BAR_BYTES + 15) & ~15u));
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -502,6 +510,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             };
+            // TRO: columns n0 + c0 + lane of rows (this warp's 32) through the staging block
+            // (row offsets / validity / bias: this tile's per-lane values, published once per
+            // tile in a per-warp table and read back as smem broadcasts)
+            if constexpr (TRO) {
+                int64_t* roff = reinterpret_cast<int64_t*>(epi + 4 * 32 * 33) + q * 32;
+                float* rb = reinterpret_cast<float*>(epi + 4 * 32 * 33 + 4 * 32 * 2) + q * 64;
+                roff[lane] = row_ok ? off : int64_t(-1);
+                rb[lane] = (p.bias && row_ok) ? __ldg(p.bias + row) : 0.f;
+                __syncwarp();
+            }
+            auto store32_t = [&](const uint32_t* v, int c0) {
+                float* buf = epi + q * 32 * 33;
+                const int64_t* roff = reinterpret_cast<const int64_t*>(epi + 4 * 32 * 33) + q * 32;
+                const float* rb = reinterpret_cast<const float*>(epi + 4 * 32 * 33 + 4 * 32 * 2) + q * 64;
+#pragma unroll
+                for (int j = 0; j < 32; ++j) buf[lane * 33 + j] = __uint_as_float(v[j]);
+                __syncwarp();
+                const int col = n0 + c0 + lane;
+                int64_t coff = -1;
+                if (col < p.N) {
+                    if (p.ndiv) {
+                        const int cq = col / p.ndiv;
+                        coff = int64_t(cq) * p.s_nq + int64_t(col - cq * p.ndiv) * p.s_n;
+                    } else {
+                        coff = int64_t(col) * p.s_n;
+                    }
+                }
+#pragma unroll 8
+                for (int r = 0; r < 32; ++r) {
+                    const int64_t ro = roff[r];
+                    float f = buf[r * 33 + lane] + rb[r];
+                    if (p.relu) f = fmaxf(f, 0.f);
+                    if (ro >= 0 && coff >= 0) p.C[ro + coff] = f;
+                }
+                __syncwarp();
+            };
             // stream-K part: this group's share of a tile cut at boundary `bnd` between
             // groups bnd and bnd + 1 (part 0 = leading k-blocks, 1 = trailing)
             const int bnd = (w.kind == 1) ? group : group - 1;
@@ -524,6 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // column-major partial tile: lanes (rows) coalesced
 #pragma unroll
                     for (int j = 0; j < 32; ++j) __stcg(part + (c0 + j) * kBM + rit, __uint_as_float(v[j]));
+                } else if constexpr (TRO) {
+                    store32_t(v, c0);
                 } else {
                     store32(v, c0);
                 }
@@ -551,7 +597,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int j = 0; j < 32; ++j)
                             v[j] = __float_as_uint(__ldcg(p0 + (c0 + j) * kBM + rit) + __ldcg(p1 + (c0 + j) * kBM + rit));
-                        store32(v, c0);
+                        if constexpr (TRO) store32_t(v, c0);
+                        else store32(v, c0);
                     }
                     if (rit == 0) p.sk_cnt[bnd * CG + int(rank)] = 0;  // ready for the next launch
                 }
@@ -720,10 +767,10 @@ bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major, int box
     return true;
 }
 
-template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0>
+template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0, int TRO = 0>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, cudaStream_t st) {
-    using C_ = Cfg<BN, CG>;
-    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM, A_TM>;
+    using C_ = Cfg<BN, CG, TRO>;
+    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM, A_TM, TRO>;
     static bool attr_set = false;
     if (!attr_set) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
@@ -765,6 +812,14 @@ template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
+    if (g.C.transposed) {  // swapped forward of a narrow bank: y rows = channels
+        if constexpr (CG == 1 && BN >= 192) {
+            if (amn || bmn) return cudaErrorInvalidValue;
+            if (g.im2col.x && g.im2col.operand == 1) return launch<BN, 0, 0, 1, 2, 0, 1>(ta, tb, kp, st);
+            if (!g.im2col.x) return launch<BN, 0, 0, 1, 0, 0, 1>(ta, tb, kp, st);
+        }
+        return cudaErrorInvalidValue;
+    }
     if constexpr (BN <= 96) {
         const int atm = g.im2col.operand == 1 ? 0 : a_in_tmem_mode();
         if (!amn && g.passes == 3 && atm == 2) {
@@ -854,8 +909,16 @@ int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn, int cg) {
     return int(best);
 }
 
+// tile width of a problem: the caller's, else the least-padding candidate (>= 192 for
+// the transposing epilogue)
+int tile_n(const GemmProblem& g) {
+    if (g.bn) return g.bn;
+    if (g.C.transposed) return ((g.N + 191) / 192) * 192 < ((g.N + 255) / 256) * 256 ? 192 : 256;
+    return choose_bn(g.N);
+}
+
 int plan_splits(const GemmProblem& g) {
-    const int bn = g.bn ? g.bn : choose_bn(g.N);
+    const int bn = tile_n(g);
     return choose_splits(g.M, g.N, g.K, num_sms(), bn, choose_cg(g, bn));
 }
 
@@ -874,7 +937,7 @@ SkPlan sk_plan(const GemmProblem& g) {
         return e ? atoi(e) : 1;
     }();
     if (!enabled || g.splits > 1 || g.M <= 0 || g.N <= 0 || g.K <= 0) return sp;
-    const int bn = g.bn ? g.bn : choose_bn(g.N);
+    const int bn = tile_n(g);
     const int cg = choose_cg(g, bn);
     const int64_t tiles = ((g.M + kBM * cg - 1) / (kBM * cg)) * ((g.N + bn - 1) / bn);
     const int64_t slots = num_sms() / cg;
@@ -897,7 +960,7 @@ size_t gemm_workspace_bytes(const GemmProblem& g) {
 
 cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     if (g.M <= 0 || g.N <= 0 || g.K <= 0) return cudaErrorInvalidValue;
-    const int bn = g.bn ? g.bn : choose_bn(g.N);
+    const int bn = tile_n(g);
     KParams kp{};
     kp.M = int(g.M);
     kp.N = int(g.N);

@@ -30,6 +30,10 @@ struct OutMap {
     // fused epilogue (final stores only): v = act(v + bias[n]), act = ReLU when relu != 0
     const float* bias = nullptr;
     int relu = 0;
+    // transposing epilogue: rows of the output are contiguous along n (e.g. NCHW y of a
+    // swapped GEMM, rows = channels); the bias is then indexed by the ROW.  Needs K-major
+    // A and B, no CTA pairs, BN >= 192 (run_gemm forces those)
+    int transposed = 0;
 };
 
 // Implicit Type 1 lowering: operand A is read straight from the NHWC input x

@@ -295,7 +295,9 @@ def test_phase_timings(cct, dev):
 @pytest.mark.parametrize("layer", CAFFENET[:3], ids=[l[0] for l in CAFFENET[:3]])
 def test_cached_training_step_matches_separate_passes(cct, dev, orc, layer, t):
     """cct_conv_fwd_cached + cct_conv_bwd (Dhat lowered once, dy expanded once)
-    give the same tensors as the three separate entry points, bit for bit."""
+    give the same tensors as the three separate entry points, bit for bit -- except the
+    stand-alone forward of a strided Type 1 layer, which the cost model may run in
+    space-to-depth form (a different K order: equal to fp32 rounding)."""
     from paper_1504_04343_b200 import conv
     _, n, k, d, o, s, p = layer
     b = 3
@@ -307,7 +309,11 @@ def test_cached_training_step_matches_separate_passes(cct, dev, orc, layer, t):
     cache = conv.alloc_cache(desc, t, dev)
     y = conv.conv_fwd_cached(x, w, desc, t, cache=cache)
     dx, dw = conv.conv_bwd(dy, w, desc, t, x=x, cache=cache)
-    assert torch.equal(y, conv.conv_fwd(x, w, desc, t))
+    yf = conv.conv_fwd(x, w, desc, t)
+    if s > 1 and t == 1:
+        assert float(torch.linalg.norm(yf - y) / torch.linalg.norm(y)) < 1e-5
+    else:
+        assert torch.equal(y, yf)
     assert torch.equal(dx, conv.conv_bwd_data(dy, w, desc, t))
     assert torch.equal(dw, conv.conv_bwd_weight(x, dy, desc, t))
     _, dw2 = conv.conv_bwd(dy, w, desc, t, x=None if cache is not None else x, cache=cache, want_dx=False)
@@ -475,3 +481,44 @@ def test_space_to_depth(cct, dev, orc, layer):
         assert rel_l2(got.cpu().numpy().ravel(), ref) <= TOL
     if not blocked:
         assert torch.equal(y, ym) and torch.equal(dx, dxm)
+
+
+SWAP_SCRIPT = r"""
+import os, sys, json
+import numpy as np, torch
+sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.environ["ROOT"], "oracle"))
+import paper_1504_04343_b200 as cct
+from paper_1504_04343_b200 import conv
+from oracle_py import Oracle, rel_l2, grouped_fwd
+orc = Oracle(); dev = torch.device("cuda")
+out = {}
+for name, (n, k, d, o, s, p, G, mode) in {"conv1": (227, 11, 3, 96, 4, 0, 1, 1), "conv1_s2d": (227, 11, 3, 96, 4, 0, 1, 2),
+                                           "implicit": (13, 3, 32, 48, 1, 1, 1, 1),
+                                           "grouped_bias": (13, 3, 64, 64, 1, 1, 2, 1)}.items():
+    b = 2
+    cct.lib().cct_set_implicit_lowering(mode)
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    x = orc.uniform(5, b * n * n * d); w = orc.uniform(6, o * k * k * (d // G)); bias = orc.uniform(7, o)
+    xt = torch.from_numpy(x).to(dev).view(b, n, n, d); wt = torch.from_numpy(w).to(dev).view(o, k, k, d // G)
+    bt = torch.from_numpy(bias).to(dev)
+    y = conv.conv_fwd_ex(xt, wt, desc, 1, groups=G, bias=bt, relu=True)
+    ref = grouped_fwd(orc, x, w, b, n, d, k, o, s, p, G, bias, relu=True)
+    out[name] = rel_l2(y.cpu().numpy().ravel(), ref.ravel())
+print(json.dumps(out))
+"""
+
+
+def test_swapped_forward_opt_in(cct, dev):
+    """$CCT_FWD_SWAP=1: narrow banks (o < 128) run the forward swapped -- channels on the
+    128-row side, pixels 256 wide (materialised Dhat or TMA-im2col B operand), NCHW rows
+    through the transposing epilogue with a per-row bias + ReLU.  Off by default (slower
+    on conv1); kept correct here."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CCT_FWD_SWAP="1", ROOT=root)
+    r = subprocess.run([sys.executable, "-c", SWAP_SCRIPT], capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    errs = json.loads(r.stdout.strip().splitlines()[-1])
+    assert len(errs) == 4 and max(errs.values()) <= TOL, errs
