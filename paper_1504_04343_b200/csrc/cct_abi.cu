@@ -231,6 +231,17 @@ bool t1_implicit_bwd(const Geo& g, int type) {
     return prefer_implicit_dgrad(&d);
 }
 
+// Implicit backward-weight of a narrow bank (o < 128) runs swapped: dW rows = the o
+// channels, columns = (tap, channel) -- B is the MN-major TMA im2col of x -- instead of
+// an o-wide tile.  $CCT_WGRAD_SWAP=0 disables it (A/B).
+bool wgrad_swapped(const Geo& g) {
+    static const int env = [] {
+        const char* e = getenv("CCT_WGRAD_SWAP");
+        return e ? atoi(e) : 1;
+    }();
+    return env != 0 && g.o < 128 && g.k * g.k * im2col_dk(g.d, true) >= 192;
+}
+
 // Implicit backward-data with a narrow kernel depth (d < 128) runs swapped, the
 // pixels as the GEMM's N side (B = TMA im2col of dy): a 128-row tile with d useful
 // rows beats a d-wide tile (measured narrow-tile rate ~ 0.58 of the 256-wide one at
@@ -485,14 +496,32 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
         const float* dh = implicit ? nullptr : cache ? cache : dhat_of(g, 1, L, x, nullptr, ws, st, &e);
         CCT_TRY(e, "lower");
         GemmProblem gp = wgrad_problem(L, {dh, L.ldc, Major::MN}, {dyn, g.o, Major::MN});
-        if (implicit) wgrad_im2col(gp, g, x);
+        const bool swapped = implicit && wgrad_swapped(g);
+        if (swapped) {
+            // narrow bank (o < 128): dW (o x k^2 d) = dy^T * im2col(x) -- channels on the 128-row
+            // side, the (tap, channel) columns 192 / 256 wide (B = MN-major TMA im2col, taps
+            // padded to dk; padded columns are not stored)
+            const int64_t dk = im2col_dk(g.d, true);
+            gp.M = g.o;
+            gp.N = kk * dk;
+            gp.A = {dyn, g.o, Major::MN};
+            gp.B = {nullptr, 0, Major::MN};
+            gp.im2col = im2col_of(g, x);
+            gp.im2col.dk = dk;
+            gp.im2col.operand = 2;
+            gp.C.ndiv = dk;
+            gp.C.s_nq = g.d;
+            gp.C.nmlim = g.d;
+        } else if (implicit) {
+            wgrad_im2col(gp, g, x);
+        }
         const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
         if (ws.base) {
             gp.C.ptr = parts;
-            gp.C.s_mr = 1;
-            gp.C.s_n = L.cols;
+            gp.C.s_mr = swapped ? L.cols : 1;
+            gp.C.s_n = swapped ? 1 : L.cols;
             gp.C.s_split = wsize;
             gp.splits = splits;
             CCT_TRY(run_gemm(gp, st), "gemm (bwd-weight)");

@@ -194,6 +194,14 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     // implicit backward-weight GEMM: MN-major im2col A; narrow banks (o <= 96) run
     // without CTA pairs (measured 0.74 of the table rate, conv1 in s2d form)
     const double wg_slow = t1_implicit ? (g.o <= 96 ? 1.35 : 1.1) : 1.0;
+    // ... except that with the implicit backward (dy in NHWC) a narrow bank runs swapped
+    // (cct_abi.cu wgrad_swapped): o rows of a 128-row tile, the (tap, channel) columns wide
+    const bool wg_swap = t1_implicit && g.o < 128 && implicit_dgrad_possible(g) && wg_cols >= 192;
+    auto wgrad_gemm = [&]() {
+        // (measured on conv1 in blocked form: 1.46x the table rate -- CTA-pair-less, and the
+        // producer issues 4 + 6 TMA boxes per k-block)
+        return wg_swap ? gemm_seconds(g.o, wg_cols, rows, c) * 1.46 : gemm_seconds(wg_cols, ncols, rows, c) * wg_slow;
+    };
     double t = 0, by = 0, launches = 0;
     // measured class rates (sweep, profiles/r01): lift and expand gather, so they
     // run below the copy-like lower / col2im kernels
@@ -233,7 +241,7 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     } else if (pass == 2) {
         if (!t3_zero_copy && !t1_implicit) hbm(xin + dhat); // lower
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand
-        const double gt = gemm_seconds(wg_cols, ncols, rows, c) * wg_slow;
+        const double gt = wgrad_gemm();
         const double gb = a_in + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;
@@ -248,7 +256,7 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         if (type != 1) hbm_at(rhat + yout, lift_bw);       // lift
         hbm_at(yout + rhat, type == 1 ? c->hbm_bytes_per_s * 0.45 : expand_bw);  // expand (shared)
         t += dgrad(&by, &launches);                        // bwd-data
-        gt = gemm_seconds(wg_cols, ncols, rows, c) * wg_slow;  // bwd-weight GEMM
+        gt = wgrad_gemm();  // bwd-weight GEMM
         gb = a_in + rhat;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         by += gb;

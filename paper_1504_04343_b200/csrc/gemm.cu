@@ -47,6 +47,7 @@ struct KParams {
     int* sk_cnt;
     int64_t s_nq;
     int64_t mlim;
+    int nmlim;  // with ndiv: columns with (n % ndiv) >= nmlim are not stored
     const float* bias;  // fused epilogue: v = act(v + bias[n])
     int relu;
     // implicit (im2col) A: layer geometry (ic_d = channels per tap of the lowered index)
@@ -262,20 +263,33 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // incrementally (no divisions inside the k-loop)
                 Pix px{};      // forward: first pixel of the tile; bwd-weight: pixel of k0
                 int tap_i = 0, tap_j = 0, cc = 0;   // forward: filter tap and channel block of kb
-                int bw_ch[kBM / 32], bw_ti[kBM / 32], bw_tj[kBM / 32];  // bwd-weight: per 32-row box
+                // bwd-weight: per 32-channel box (A rows, or B rows when B is the MN-major im2col)
+                constexpr int NBW = (A_IM == 3) ? (BNL / 32 > 0 ? BNL / 32 : 1) : kBM / 32;
+                int bw_ch[NBW], bw_ti[NBW], bw_tj[NBW];
                 if constexpr (A_IM == 2) {  // B = im2col: the tile's pixels are its N index
                     px = pix_of(n0, p);
                     const int tap = kb0 / p.ic_cpt;
                     cc = kb0 - tap * p.ic_cpt;
                     tap_i = tap / p.ic_k;
                     tap_j = tap - tap_i * p.ic_k;
-                } else if constexpr (A_IM && !A_MN) {
+                } else if constexpr (A_IM == 3) {  // B = MN-major im2col: N = (tap, channel), K = pixels
+                    px = pix_of(kb0 * kBK, p);
+                    const int kkd = p.ic_k * p.ic_k * p.ic_d;
+#pragma unroll
+                    for (int c = 0; c < NBW; ++c) {
+                        const int ncol = min(n0 + 32 * c, kkd - 32);  // columns >= N are masked later
+                        const int tap = ncol / p.ic_d;
+                        bw_ch[c] = ncol - tap * p.ic_d;
+                        bw_ti[c] = tap / p.ic_k;
+                        bw_tj[c] = tap - bw_ti[c] * p.ic_k;
+                    }
+                } else if constexpr (A_IM == 1 && !A_MN) {
                     px = pix_of(m0, p);
                     const int tap = kb0 / p.ic_cpt;
                     cc = kb0 - tap * p.ic_cpt;
                     tap_i = tap / p.ic_k;
                     tap_j = tap - tap_i * p.ic_k;
-                } else if constexpr (A_IM && A_MN) {
+                } else if constexpr (A_IM == 1 && A_MN) {
                     px = pix_of(kb0 * kBK, p);
                     const int kkd = p.ic_k * p.ic_k * p.ic_d;
 #pragma unroll
@@ -302,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             cc = 0;
                             if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
                         }
-                    } else if constexpr (A_IM && !A_MN) {
+                    } else if constexpr (A_IM == 1 && !A_MN) {
                         // implicit lowering, forward: 128 pixels x 16 channels of filter tap (ti, tj)
                         ptx::tma_load_im2col_4d(a_dst, &tmA, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
                                                 p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
@@ -310,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             cc = 0;
                             if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
                         }
-                    } else if constexpr (A_IM && A_MN) {
+                    } else if constexpr (A_IM == 1 && A_MN) {
                         // implicit lowering, backward-weight: K rows = 16 pixels, M = (tap, ch)
 #pragma unroll
                         for (int c = 0; c < kBM / 32; ++c)
@@ -331,6 +345,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if constexpr (A_IM == 2) {
                         // B issued above (im2col)
+                    } else if constexpr (A_IM == 3) {
+                        // swapped backward-weight: B = 16 pixels x (BNL/32 x 32 channels of a tap)
+#pragma unroll
+                        for (int c = 0; c < NBW; ++c)
+                            ptx::tma_load_im2col_4d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage], bw_ch[c],
+                                                    p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
+                                                    uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
+                        px.c += kBK;
+                        while (px.c >= p.ic_m) {
+                            px.c -= p.ic_m;
+                            if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
+                        }
                     } else if constexpr (!B_MN) {
                         ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
                     } else {
@@ -482,7 +508,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int64_t wrap = p.s_nq - int64_t(p.ndiv) * sn;
 #pragma unroll
                     for (int j = 0; j < 32; ++j) {
-                        if (j < nlim) *dst = __uint_as_float(v[j]);
+                        if (j < nlim && nr < p.nmlim) *dst = __uint_as_float(v[j]);
                         dst += sn;
                         if (++nr == p.ndiv) { nr = 0; dst += wrap; }
                     }
@@ -821,7 +847,7 @@ cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const C
         return cudaErrorInvalidValue;
     }
     if constexpr (BN <= 96) {
-        const int atm = g.im2col.operand == 1 ? 0 : a_in_tmem_mode();
+        const int atm = g.im2col.operand >= 1 ? 0 : a_in_tmem_mode();
         if (!amn && g.passes == 3 && atm == 2) {
             if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 2>(ta, tb, kp, st);
             return bmn ? launch<BN, 0, 1, CG, 0, 2>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 2>(ta, tb, kp, st);
@@ -830,6 +856,10 @@ cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const C
             if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 1>(ta, tb, kp, st);
             return bmn ? launch<BN, 0, 1, CG, 0, 1>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 1>(ta, tb, kp, st);
         }
+    }
+    if (g.im2col.x && g.im2col.operand == 2) {  // B = MN-major im2col (swapped backward-weight)
+        if (!bmn) return cudaErrorInvalidValue;
+        return amn ? launch<BN, 1, 1, CG, 3>(ta, tb, kp, st) : launch<BN, 0, 1, CG, 3>(ta, tb, kp, st);
     }
     if (g.im2col.x && g.im2col.operand == 1) {  // B = im2col (swapped implicit GEMM), K-major A and B
         if (amn || bmn) return cudaErrorInvalidValue;
@@ -982,6 +1012,7 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.ndiv = g.C.ndiv < (int64_t(1) << 31) ? int(g.C.ndiv) : 0;
     kp.s_nq = g.C.s_nq;
     kp.mlim = g.C.mlim;
+    kp.nmlim = g.C.nmlim < (int64_t(1) << 31) ? int(g.C.nmlim) : INT32_MAX;
     kp.bias = g.C.bias;
     kp.relu = g.C.relu;
 
@@ -1000,12 +1031,13 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
         }
     }
     CUtensorMap ta, tb;
-    const bool b_im = g.im2col.x && g.im2col.operand == 1;
+    const bool b_im = g.im2col.x && g.im2col.operand >= 1;
     if (g.im2col.x) {
         const Im2col& ic = g.im2col;
         const bool amn = g.A.major == Major::MN;
+        const bool imn = (ic.operand == 2) || (ic.operand == 0 && amn);  // the im2col operand is MN-major
         const int64_t dk = ic.dk ? ic.dk : ic.d;
-        if (!im2col_ok(ic.d, amn) || dk < ic.d || dk % (amn ? 32 : kBK)) return cudaErrorInvalidValue;
+        if (!im2col_ok(ic.d, imn) || dk < ic.d || dk % (imn ? 32 : kBK)) return cudaErrorInvalidValue;
         kp.ic_d = int(dk);
         kp.ic_k = int(ic.k);
         kp.ic_s = int(ic.s);
@@ -1013,7 +1045,11 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
         kp.ic_m = int(ic.m);
         kp.ic_mm = int(ic.m * ic.m);
         kp.ic_cpt = int(dk / kBK);
-        if (b_im) {
+        if (b_im && ic.operand == 2) {
+            if (g.B.major != Major::MN || (bn / cg) % 32 || !make_tmap_im2col(&tb, ic, true) ||
+                !make_tmap(&ta, g.A, g.M, g.K, kBM))
+                return cudaErrorInvalidValue;
+        } else if (b_im) {
             if (amn || g.B.major == Major::MN || !make_tmap_im2col(&tb, ic, false, bn / cg) ||
                 !make_tmap(&ta, g.A, g.M, g.K, kBM))
                 return cudaErrorInvalidValue;

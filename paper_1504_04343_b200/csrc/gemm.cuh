@@ -27,6 +27,7 @@ struct OutMap {
     int64_t s_mq = 0, s_mr = 1, s_n = 0, s_split = 0;
     int64_t ndiv = INT64_MAX, s_nq = 0;
     int64_t mlim = INT64_MAX;  // rows with (m % mdiv) >= mlim are not stored (padded channels)
+    int64_t nmlim = INT64_MAX; // columns with (n % ndiv) >= nmlim are not stored (two-level map only)
     // fused epilogue (final stores only): v = act(v + bias[n]), act = ReLU when relu != 0
     const float* bias = nullptr;
     int relu = 0;
@@ -52,7 +53,10 @@ struct Im2col {
     int64_t b = 0, n = 0, d = 0, k = 0, s = 1, p = 0, m = 0;
     int64_t dk = 0;
     int64_t cs = 0;  // channel stride of a pixel in x (0: = d); > d reads one channel group
-    int operand = 0; // 0: A = im2col(x) (M = pixels); 1: B = im2col(x) (N = pixels, K-major; swapped GEMM)
+    // 0: A = im2col(x) (M = pixels, or MN-major for backward-weight); 1: B = im2col(x) (N =
+    // pixels, K-major: swapped forward / backward-data); 2: B = MN-major im2col(x) (N = (tap,
+    // channel), K = pixels: swapped backward-weight of a narrow bank)
+    int operand = 0;
 };
 
 struct GemmProblem {

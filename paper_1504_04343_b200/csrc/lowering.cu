@@ -635,17 +635,18 @@ cudaError_t transpose_batched(const float* src, int64_t rows, int64_t cols, int6
     if (rows >= (int64_t(1) << 31) || cols >= (int64_t(1) << 31) || nz >= (int64_t(1) << 31))
         return cudaErrorInvalidConfiguration;
     PhaseScope ps(Phase(phase), st, 0, 8.0 * double(rows * cols * nz));
-    if (rows >= 128) {
-        const int64_t tiles = cdiv(rows, 128) * cdiv(cols, 32) * nz;
+    // tile height: the largest of 128 / 96 / 64 / 32 rows not above `rows` (more loads in flight)
+    auto go = [&](auto tr) {
+        constexpr int TR = decltype(tr)::value;
+        const int64_t tiles = cdiv(rows, TR) * cdiv(cols, 32) * nz;
         const int grid = int(std::min<int64_t>(tiles, int64_t(num_sms()) * 8));
-        transpose_batched_kernel<128><<<grid, 256, 0, st>>>(src, int(rows), int(cols), lds, src_z, dst, ldd, dst_z,
-                                                            int(nz));
-    } else {
-        const int64_t tiles = cdiv(rows, 32) * cdiv(cols, 32) * nz;
-        const int grid = int(std::min<int64_t>(tiles, int64_t(num_sms()) * 8));
-        transpose_batched_kernel<32><<<grid, 256, 0, st>>>(src, int(rows), int(cols), lds, src_z, dst, ldd, dst_z,
+        transpose_batched_kernel<TR><<<grid, 256, 0, st>>>(src, int(rows), int(cols), lds, src_z, dst, ldd, dst_z,
                                                            int(nz));
-    }
+    };
+    if (rows >= 128) go(std::integral_constant<int, 128>{});
+    else if (rows >= 96) go(std::integral_constant<int, 96>{});
+    else if (rows >= 64) go(std::integral_constant<int, 64>{});
+    else go(std::integral_constant<int, 32>{});
     note_launch();
     return cudaGetLastError();
 }

@@ -48,25 +48,31 @@ __global__ void s2d_input_kernel(const float* __restrict__ x, float* __restrict_
     }
 }
 
-// one block per dx row (q, r): dx[q][r][c][ch] = dX'[q][u][v][a s d + (E - v s d)],
-// E = (c + p) d + ch, u = (r + p) / s, a = (r + p) % s, v = E / (s d); 0 where no
-// blocked position covers the pixel
+// one block per dX' row (q, u): the row (n' s^2 d contiguous floats) is staged in smem,
+// then the s dx rows r = s u + a - p it covers are written coalesced:
+// dx[q][r][c][ch] = dX'[q][u][v][a s d + (E - v s d)], E = (c + p) d + ch, v = E / (s d)
+// (0 where v >= n').  The last block also zeroes dx rows past s n' - p (no blocked row).
 __global__ void d2s_input_kernel(const float* __restrict__ dxs, float* __restrict__ dx, int64_t b, int n, int d,
                                  int s, int p, int ns) {
-    const int sd = s * d, ds = s * sd;
-    const int row_len = n * d;
-    for (int64_t row = blockIdx.x; row < b * n; row += gridDim.x) {
-        const int64_t q = row / n;
-        const int r = int(row - q * n);
-        const int u = (r + p) / s, a = (r + p) - u * s;
-        float* dst = dx + row * row_len;
-        const float* src = dxs + (q * ns + u) * int64_t(ns) * ds + a * sd;
-        for (int e = threadIdx.x; e < row_len; e += blockDim.x) {
-            const int E = e + p * d;
-            const int v = E / sd;
-            float val = 0.f;
-            if (u < ns && v < ns) val = __ldg(src + int64_t(v) * ds + (E - v * sd));
-            dst[e] = val;
+    extern __shared__ float row_sm[];  // n' s^2 d
+    const int sd = s * d, ds = s * sd, nd = n * d;
+    const int row_len = ns * ds;
+    for (int64_t row = blockIdx.x; row < b * ns; row += gridDim.x) {
+        const int64_t q = row / ns;
+        const int u = int(row - q * ns);
+        __syncthreads();
+        const float* src = dxs + row * row_len;
+        for (int e = threadIdx.x; e < row_len; e += blockDim.x) row_sm[e] = __ldg(src + e);
+        __syncthreads();
+        const int r_end = (u == ns - 1) ? n : min(n, s * u - p + s);
+        for (int r = max(0, s * u - p); r < r_end; ++r) {
+            const int a = r + p - s * u;  // >= s: past the blocked rows -> zero
+            float* out = dx + (q * n + r) * int64_t(nd);
+            for (int e = threadIdx.x; e < nd; e += blockDim.x) {
+                const int E = e + p * d;
+                const int v = E / sd;
+                out[e] = (a < s && v < ns) ? row_sm[v * ds + a * sd + (E - v * sd)] : 0.f;
+            }
         }
     }
 }
@@ -103,15 +109,15 @@ __global__ void d2s_weights_kernel(const float* __restrict__ dws, float* __restr
     }
 }
 
-int rows_grid(int64_t rows) { return int(std::min<int64_t>(rows, int64_t(num_sms()) * 16)); }
+int rows_grid(int64_t rows) { return int(std::min<int64_t>(rows, int64_t(num_sms()) * 8)); }
 
 }  // namespace
 
 cudaError_t s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st) {
     const Geo v = s2d_geo(g);
     PhaseScope ps(kPhaseLower, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + g.b * v.n * v.n * v.d));
-    s2d_input_kernel<<<rows_grid(g.b * v.n), kThreads, 0, st>>>(x, xs, g.b, int(g.n), int(g.d), int(g.s), int(g.p),
-                                                                 int(v.n));
+    s2d_input_kernel<<<int(std::min<int64_t>(g.b * v.n, int64_t(num_sms()) * 16)), kThreads, 0, st>>>(
+        x, xs, g.b, int(g.n), int(g.d), int(g.s), int(g.p), int(v.n));
     note_launch();
     return cudaGetLastError();
 }
@@ -119,8 +125,10 @@ cudaError_t s2d_input(const Geo& g, const float* x, float* xs, cudaStream_t st) 
 cudaError_t d2s_input(const Geo& g, const float* dxs, float* dx, cudaStream_t st) {
     const Geo v = s2d_geo(g);
     PhaseScope ps(kPhaseCol2im, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + g.b * v.n * v.n * v.d));
-    d2s_input_kernel<<<rows_grid(g.b * g.n), kThreads, 0, st>>>(dxs, dx, g.b, int(g.n), int(g.d), int(g.s), int(g.p),
-                                                                 int(v.n));
+    const size_t sm = size_t(v.n * v.d) * 4;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(d2s_input_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm));
+    d2s_input_kernel<<<rows_grid(g.b * v.n), kThreads, sm, st>>>(dxs, dx, g.b, int(g.n), int(g.d), int(g.s), int(g.p),
+                                                                  int(v.n));
     note_launch();
     return cudaGetLastError();
 }
