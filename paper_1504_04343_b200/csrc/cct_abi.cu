@@ -9,6 +9,7 @@
 //   BWD_DATA: M=cols(Dhat) N=rows K=ncols  A=W (MN-major) B=dRhat^T (MN-major) C -> dDhat, col2im
 //   BWD_WEIGHT: M=cols N=ncols K=rows   A=Dhat (MN-major) B=dRhat^T (K-major) C -> dW (split-K)
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <sstream>
@@ -136,13 +137,15 @@ const float* weights_view(const Lowered& L, const float* w, Ws& ws, cudaStream_t
 
 // Implicit Type 1 lowering (TMA im2col A operand) -- on by default; the
 // materialised path stays available for parity tests and small-channel layers.
-int g_implicit = -1;
+// process-wide knobs (atomics: the ABI may be called from several host threads)
+std::atomic<int> g_implicit{-1};
 bool implicit_enabled() {
-    if (g_implicit < 0) {
+    if (g_implicit.load() < 0) {
         const char* e = getenv("CCT_IMPLICIT");
-        g_implicit = e ? std::max(0, std::min(2, atoi(e))) : 1;
+        int expected = -1;
+        g_implicit.compare_exchange_strong(expected, e ? std::max(0, std::min(2, atoi(e))) : 1);
     }
-    return g_implicit != 0;
+    return g_implicit.load() != 0;
 }
 
 // Type 1 with d % 16 == 0 runs forward and backward-weight on the input itself.
@@ -647,14 +650,15 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
 // reuse the same scratch region in stream order.  Backward-weight partials of
 // the chunks are summed in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
-size_t g_ws_limit = 0;
+std::atomic<size_t> g_ws_limit{0};
 
 size_t ws_limit() {
-    if (!g_ws_limit) {
+    if (!g_ws_limit.load()) {
         const char* e = getenv("CCT_WORKSPACE_LIMIT");
-        g_ws_limit = e ? size_t(strtoull(e, nullptr, 10)) : (size_t(16) << 30);
+        size_t expected = 0;
+        g_ws_limit.compare_exchange_strong(expected, e ? size_t(strtoull(e, nullptr, 10)) : (size_t(16) << 30));
     }
-    return g_ws_limit;
+    return g_ws_limit.load();
 }
 
 Geo with_batch(Geo g, int64_t b) {
@@ -885,7 +889,7 @@ int cct_device_info(char* name, size_t len, int* sms) {
 }
 void cct_set_workspace_limit(size_t bytes) { g_ws_limit = bytes; }
 void cct_set_implicit_lowering(int mode) { g_implicit = std::max(0, std::min(2, mode)); }
-int cct_get_implicit_lowering(void) { return implicit_enabled() ? g_implicit : 0; }
+int cct_get_implicit_lowering(void) { return implicit_enabled() ? g_implicit.load() : 0; }
 size_t cct_get_workspace_limit(void) { return ws_limit(); }
 void cct_profile_enable(int on) { cct::profile_enable(on != 0); }
 void cct_profile_read(double* ms, double* flops, double* bytes, uint64_t* launches, int reset) {

@@ -797,11 +797,11 @@ template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0, int TRO = 
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, cudaStream_t st) {
     using C_ = Cfg<BN, CG, TRO>;
     auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM, A_TM, TRO>;
-    static bool attr_set = false;
-    if (!attr_set) {
+    // per call (idempotent, ~1 us): the attribute is per device, and callers may switch devices
+    // or threads; a process-wide "done" flag would miss the second GPU
+    {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C_::SMEM_BYTES);
         if (e != cudaSuccess) return e;
-        attr_set = true;
     }
     const int sms = num_sms() / CG * CG;
     const int grid = kp.sk_len ? sms : std::min(kp.units * CG, sms);

@@ -529,11 +529,7 @@ cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, floa
     const size_t smem1 = size_t(g.k * (g.n + 2 * g.p) * g.d) * 4 + size_t(cols) * 4 + size_t((g.n + 2 * g.p) * g.d) * 4;
     if (type == 1 && !vec && ld % 4 == 0 && reinterpret_cast<uintptr_t>(dhat) % 16 == 0 && smem1 <= 96 * 1024 &&
         rm.ny == g.m && rm.nc == g.m) {
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(lower_t1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            attr = true;
-        }
+        cudaFuncSetAttribute(lower_t1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);  // per device
         const int64_t nqr = g.b * g.m;
         const int grid1 = int(std::min<int64_t>(nqr, int64_t(num_sms()) * 4));
         lower_t1_smem_kernel<<<grid1, 512, smem1, st>>>(x, dhat, g, rm, ld, int(cols));
@@ -591,12 +587,8 @@ cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* d
     PhaseScope ps(kPhaseCol2im, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + g.b * rmi.rpi * lowered_cols(g, type)));
     if (col2im_slab_layout(g, type)) {  // ld = slab stride
         if (ld != slab_stride(g) || reinterpret_cast<uintptr_t>(dd) % 16) return cudaErrorInvalidValue;
-        static bool attr = false;
-        if (!attr) {
-            cudaFuncSetAttribute(col2im_t1_smem_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            cudaFuncSetAttribute(col2im_t1_smem_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-            attr = true;
-        }
+        cudaFuncSetAttribute(col2im_t1_smem_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(col2im_t1_smem_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         const size_t smem1 = size_t(2 * ((g.k + g.s - 1) / g.s) * ld + g.n * g.d) * 4;
         const int grid1 = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * 4));
         if ((g.k + g.s - 1) / g.s <= 3) col2im_t1_smem_kernel<3><<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
