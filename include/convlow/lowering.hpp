@@ -9,6 +9,7 @@
 #pragma once
 
 #include <utility>
+#include <vector>
 
 #include "convlow/gemm.hpp"
 #include "convlow/tensor.hpp"
@@ -55,5 +56,31 @@ DataBatch convolve_backward_data(const OutputBatch& dy, const KernelBank& bank, 
                                  LoweringStrategy strategy, ConvGeometry geom = {});
 KernelBank convolve_backward_weight(const DataBatch& batch, const OutputBatch& dy, std::size_t k,
                                     LoweringStrategy strategy, ConvGeometry geom = {});
+
+// Layer extension (beyond the reference, whose SPEC puts groups out of
+// scope): grouped convolution as in bvlc_reference_caffenet and the bias + ReLU
+// epilogue around the layer.  The KernelBank holds (o, k, k, d / groups); output channel j
+// reads input-channel group j / (o / groups).  y = relu ? max(conv + bias, 0) : conv + bias
+// (empty bias = none).  Over cct_conv_fwd_ex / cct_conv_bwd_ex (include/cct.h).
+struct LayerExtension {
+    std::size_t groups = 1;
+    std::vector<real> bias;  // o values, or empty
+    bool relu = false;
+};
+
+std::pair<OutputBatch, PhaseTimings> convolve_lowered_ex(const DataBatch& batch, const KernelBank& bank,
+                                                         LoweringStrategy strategy, const LayerExtension& ext,
+                                                         ConvGeometry geom = {});
+
+struct LayerGradients {
+    DataBatch dx;          // gradient of the input
+    KernelBank dw;         // (o, k, k, d / groups)
+    std::vector<real> db;  // o values (empty when the layer has no bias)
+};
+
+// dy: gradient of the layer output y (after the ReLU; y is the forward's output).
+LayerGradients convolve_backward_ex(const DataBatch& batch, const OutputBatch& y, const OutputBatch& dy,
+                                    const KernelBank& bank, LoweringStrategy strategy, const LayerExtension& ext,
+                                    ConvGeometry geom = {});
 
 }  // namespace convlow

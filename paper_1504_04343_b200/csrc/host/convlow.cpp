@@ -531,6 +531,87 @@ KernelBank convolve_backward_weight(const DataBatch& batch, const OutputBatch& d
     return dwb;
 }
 
+// ----------------------------------------------------- layer extension (groups, bias, ReLU)
+namespace {
+LayerConfig ext_layer(const DataBatch& batch, const KernelBank& bank, const LayerExtension& ext, ConvGeometry geom) {
+    const Tensor3& first = batch[0];
+    if (ext.groups < 1 || first.depth() % ext.groups || bank.o() % ext.groups || bank.depth() * ext.groups != first.depth())
+        throw config_error("grouped layer: kernel bank " + bank_shape_str(bank) + " with groups=" +
+                           std::to_string(ext.groups) + " does not match data tensor " + tensor_shape_str(first));
+    if (!ext.bias.empty() && ext.bias.size() != bank.o())
+        throw config_error("bias has " + std::to_string(ext.bias.size()) + " values for o=" + std::to_string(bank.o()));
+    LayerConfig L;
+    L.n = first.rows();
+    L.k = bank.k();
+    L.d = first.depth();
+    L.o = bank.o();
+    L.b = batch.b();
+    return layer_with(L, geom);
+}
+}  // namespace
+
+std::pair<OutputBatch, PhaseTimings> convolve_lowered_ex(const DataBatch& batch, const KernelBank& bank,
+                                                         LoweringStrategy strategy, const LayerExtension& ext,
+                                                         ConvGeometry geom) {
+    const LayerConfig L = ext_layer(batch, bank, ext, geom);
+    cct_conv_desc d = make_desc(L);
+    float* dx = upload_batch(batch, kX);
+    float* dw = upload(bank.values(), kW);
+    float* db = ext.bias.empty() ? nullptr : upload(ext.bias, kAux);
+    const cct_conv_ext e{int64_t(ext.groups), db, ext.relu ? 1 : 0};
+    OutputBatch out(L.b, L.o, L.m());
+    auto* dy = static_cast<float*>(ctx().get(kY, out.size() * sizeof(float)));
+    size_t need = 0;
+    check(cct_workspace_size_ex(&d, to_c(strategy), &e, CCT_PASS_FWD, &need), "workspace");
+    void* ws = ctx().get(kWs, need);
+    PhaseProbe probe;
+    check(cct_conv_fwd_ex(&d, to_c(strategy), &e, dx, dw, dy, ws, need, ctx().stream), "convolve_lowered_ex");
+    ctx().sync();
+    PhaseTimings t = probe.finish();
+    download(out.values(), dy);
+    ctx().sync();
+    return {std::move(out), t};
+}
+
+LayerGradients convolve_backward_ex(const DataBatch& batch, const OutputBatch& y, const OutputBatch& dy,
+                                    const KernelBank& bank, LoweringStrategy strategy, const LayerExtension& ext,
+                                    ConvGeometry geom) {
+    const LayerConfig L = ext_layer(batch, bank, ext, geom);
+    if (dy.b() != L.b || dy.o() != L.o || dy.m() != L.m() || (ext.relu && (y.b() != L.b || y.o() != L.o || y.m() != L.m())))
+        throw config_error("dy / y do not match the layer output (b=" + std::to_string(L.b) + ", o=" +
+                           std::to_string(L.o) + ", m=" + std::to_string(L.m()) + ")");
+    cct_conv_desc d = make_desc(L);
+    float* dx_in = upload_batch(batch, kX);
+    float* dw_in = upload(bank.values(), kW);
+    float* ddy = upload(dy.values(), kY);
+    float* dyo = ext.relu ? upload(y.values(), kA) : nullptr;
+    const size_t per = L.n * L.n * L.d;
+    auto* gdx = static_cast<float*>(ctx().get(kB, per * L.b * sizeof(float)));
+    auto* gdw = static_cast<float*>(ctx().get(kC, bank.values().size() * sizeof(float)));
+    auto* gdb = ext.bias.empty() ? nullptr : static_cast<float*>(ctx().get(kAux, L.o * sizeof(float)));
+    const cct_conv_ext e{int64_t(ext.groups), nullptr, ext.relu ? 1 : 0};
+    size_t need = 0;
+    check(cct_workspace_size_ex(&d, to_c(strategy), &e, CCT_PASS_BWD, &need), "workspace");
+    void* ws = ctx().get(kWs, need);
+    check(cct_conv_bwd_ex(&d, to_c(strategy), &e, dx_in, dyo, ddy, dw_in, gdx, gdw, gdb, ws, need, ctx().stream),
+          "convolve_backward_ex");
+    LayerGradients g;
+    std::vector<Tensor3> imgs(L.b, Tensor3(L.n, L.d));
+    for (size_t q = 0; q < L.b; ++q)
+        cuda_check(cudaMemcpyAsync(imgs[q].values().data(), gdx + q * per, per * sizeof(float), cudaMemcpyDeviceToHost,
+                                   ctx().stream),
+                   "D2H");
+    g.dw = KernelBank(bank.k(), bank.depth(), bank.o());
+    download(g.dw.values(), gdw);
+    if (gdb) {
+        g.db.resize(L.o);
+        download(g.db, gdb);
+    }
+    ctx().sync();
+    g.dx = DataBatch(std::move(imgs));
+    return g;
+}
+
 // ------------------------------------------------------------ cost_model.hpp
 namespace {
 cct_calibration weights_to_cal(const CostWeights& w) {

@@ -268,6 +268,63 @@ static void gpu_tests() {
             CHECK(rel_l2(convolve_backward_weight(b, dy, kk, LoweringStrategy(t), g).values(), rdw) <= 1e-4);
         }
     });
+    run("layer extension: groups = 2 + bias + ReLU == per-group convolutions (cct_conv_*_ex)", [] {
+        std::mt19937_64 rng(31);
+        const size_t n = 13, kk = 3, d = 16, o = 24, bb = 2, G = 2, s = 1, p = 1;
+        DataBatch b = DataBatch::random(bb, n, d, rng);
+        KernelBank k = KernelBank::random(kk, d / G, o, rng);
+        LayerExtension ext;
+        ext.groups = G;
+        ext.relu = true;
+        std::uniform_real_distribution<float> u(-1, 1);
+        for (size_t j = 0; j < o; ++j) ext.bias.push_back(u(rng));
+        const size_t m = (n + 2 * p - kk) / s + 1;
+        OutputBatch dy(bb, o, m);
+        for (auto& v : dy.values()) v = u(rng);
+        // reference: each group through the oracle, then bias + ReLU; backward with the mask of y
+        std::vector<float> x = flat(b), ry(bb * o * m * m), rdx(x.size()), rdw(k.values().size()), rdb(o, 0.f);
+        const size_t dg = d / G, og = o / G;
+        for (size_t g = 0; g < G; ++g) {
+            std::vector<float> xg(bb * n * n * dg), wg(k.values().begin() + g * og * kk * kk * dg,
+                                                          k.values().begin() + (g + 1) * og * kk * kk * dg);
+            for (size_t i = 0; i < bb * n * n; ++i)
+                for (size_t c = 0; c < dg; ++c) xg[i * dg + c] = x[i * d + g * dg + c];
+            std::vector<float> yg(bb * og * m * m);
+            orc_conv_fwd(xg.data(), wg.data(), yg.data(), bb, n, dg, kk, og, s, p);
+            for (size_t q = 0; q < bb; ++q)
+                for (size_t j = 0; j < og; ++j)
+                    for (size_t e = 0; e < m * m; ++e)
+                        ry[(q * o + g * og + j) * m * m + e] = std::max(0.f, yg[(q * og + j) * m * m + e] + ext.bias[g * og + j]);
+        }
+        auto [y, t] = convolve_lowered_ex(b, k, LoweringStrategy::Type1, ext, ConvGeometry{s, p});
+        CHECK(rel_l2(y.values(), ry) <= 1e-4);
+        OutputBatch dz = dy;
+        for (size_t i = 0; i < dz.values().size(); ++i) dz.values()[i] = y.values()[i] > 0 ? dy.values()[i] : 0.f;
+        for (size_t g = 0; g < G; ++g) {
+            std::vector<float> xg(bb * n * n * dg), wg(k.values().begin() + g * og * kk * kk * dg,
+                                                          k.values().begin() + (g + 1) * og * kk * kk * dg);
+            for (size_t i = 0; i < bb * n * n; ++i)
+                for (size_t c = 0; c < dg; ++c) xg[i * dg + c] = x[i * d + g * dg + c];
+            std::vector<float> dzg(bb * og * m * m), dxg(xg.size()), dwg(wg.size());
+            for (size_t q = 0; q < bb; ++q)
+                for (size_t e = 0; e < og * m * m; ++e) dzg[q * og * m * m + e] = dz.values()[(q * o + g * og) * m * m + e];
+            orc_conv_bwd_data(dzg.data(), wg.data(), dxg.data(), bb, n, dg, kk, og, s, p);
+            orc_conv_bwd_weight(xg.data(), dzg.data(), dwg.data(), bb, n, dg, kk, og, s, p);
+            for (size_t i = 0; i < bb * n * n; ++i)
+                for (size_t c = 0; c < dg; ++c) rdx[i * d + g * dg + c] = dxg[i * dg + c];
+            std::copy(dwg.begin(), dwg.end(), rdw.begin() + g * og * kk * kk * dg);
+        }
+        for (size_t q = 0; q < bb; ++q)
+            for (size_t j = 0; j < o; ++j)
+                for (size_t e = 0; e < m * m; ++e) rdb[j] += dz.values()[(q * o + j) * m * m + e];
+        LayerGradients gr = convolve_backward_ex(b, y, dy, k, LoweringStrategy::Type1, ext, ConvGeometry{s, p});
+        CHECK(rel_l2(flat(gr.dx), rdx) <= 1e-4);
+        CHECK(rel_l2(gr.dw.values(), rdw) <= 1e-4);
+        CHECK(rel_l2(gr.db, rdb) <= 1e-5);
+        LayerExtension bad = ext;
+        bad.groups = 5;
+        expect_throw<config_error>([&] { convolve_lowered_ex(b, k, LoweringStrategy::Type1, bad); });
+    });
     run("execute_partitioned invariant under p (SPEC.md:319, 333)", [] {
         std::mt19937_64 rng(4);
         DataBatch b = DataBatch::random(8, 11, 16, rng);
