@@ -48,6 +48,7 @@ struct KParams {
     int64_t s_nq;
     int64_t mlim;
     int nmlim;  // with ndiv: columns with (n % ndiv) >= nmlim are not stored
+    int split_producer;  // A and B tiles issued by two producer threads
     const float* bias;  // fused epilogue: v = act(v + bias[n])
     int relu;
     // implicit (im2col) A: layer geometry (ic_d = channels per tap of the lowered index)
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int group = blockIdx.x / CG;
     const int ngroups = gridDim.x / CG;
 
-    if (warp == 0 && lane == 0) {
+    if (warp == 0 && lane == 0) {  // (warp 3 lane 0 is the B producer)
         ptx::prefetch_tmap(&tmA);
         ptx::prefetch_tmap(&tmB);
         for (int s = 0; s < STAGES; ++s) {
@@ -244,9 +245,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tdone_leader = (CG == 2) ? ptx::mapa(ptx::smem_u32(tdone), 0) : 0u;
     const uint32_t tempty_leader = (CG == 2) ? ptx::mapa(ptx::smem_u32(tempty), 0) : 0u;
 
-    if (warp == 0) {
-        // ===================== TMA producer (every CTA loads its own share) =====================
-        if (lane == 0) {
+    if (warp == 0 || warp == 3) {
+        // ===================== TMA producers (every CTA loads its own share) =====================
+        // warp 0 issues the A tiles (and arms the stage's barrier), warp 3 the B tiles: the
+        // MN-major operands take up to 4 + 8 boxes per stage and one issuing thread was the
+        // limit of the backward-weight GEMMs ($CCT_SPLIT_PRODUCER=0: warp 0 issues both)
+        const bool role_a = warp == 0;
+        const bool role_b = (warp == 3) == (p.split_producer != 0);
+        if (lane == 0 && (role_a || role_b)) {
             int stage = 0;
             uint32_t phase = 0;
             WorkIter wi(p, group);
@@ -258,8 +264,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const int m0 = mt * (kBM * CG) + int(rank) * kBM;
                 const int n0 = nt * BN + int(rank) * BNL;
                 const int kb0 = w.kb0, kb1 = w.kb1;
-                // implicit lowering: the producer is one thread issuing every TMA of the
-                // CTA, so all im2col coordinates are per-tile constants or walked
+                // implicit lowering: each producer is one thread issuing every TMA of its
+                // operand, so all im2col coordinates are per-tile constants or walked
                 // incrementally (no divisions inside the k-loop)
                 Pix px{};      // forward: first pixel of the tile; bwd-weight: pixel of k0
                 int tap_i = 0, tap_j = 0, cc = 0;   // forward: filter tap and channel block of kb
@@ -303,66 +309,69 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 for (int kb = kb0; kb < kb1; ++kb) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[stage], C_::RAW_BYTES);
+                    // one arrival per stage (the A producer) with the whole stage's bytes; B's
+                    // bytes may land first (the transaction count may dip below zero)
+                    if (role_a) ptx::mbar_arrive_expect_tx(&full[stage], C_::RAW_BYTES);
                     uint8_t* a_dst = smem + stage * C_::STAGE_BYTES;
                     uint8_t* b_dst = a_dst + C_::A_BYTES;
                     const int k0 = kb * kBK;
-                    if constexpr (A_IM == 2) {
-                        // A: ordinary K-major tile (kernel bank rows); B: BNL pixels x 16 channels of tap (ti, tj)
-                        ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
-                        ptx::tma_load_im2col_4d(b_dst, &tmB, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
-                                                p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
-                        if (++cc == p.ic_cpt) {
-                            cc = 0;
-                            if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
-                        }
-                    } else if constexpr (A_IM == 1 && !A_MN) {
-                        // implicit lowering, forward: 128 pixels x 16 channels of filter tap (ti, tj)
-                        ptx::tma_load_im2col_4d(a_dst, &tmA, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
-                                                p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
-                        if (++cc == p.ic_cpt) {
-                            cc = 0;
-                            if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
-                        }
-                    } else if constexpr (A_IM == 1 && A_MN) {
-                        // implicit lowering, backward-weight: K rows = 16 pixels, M = (tap, ch)
+                    if (role_a) {
+                        if constexpr (A_IM == 1 && !A_MN) {
+                            // implicit lowering, forward: 128 pixels x 16 channels of filter tap (ti, tj)
+                            ptx::tma_load_im2col_4d(a_dst, &tmA, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
+                                                    p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
+                            if (++cc == p.ic_cpt) {
+                                cc = 0;
+                                if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
+                            }
+                        } else if constexpr (A_IM == 1 && A_MN) {
+                            // implicit lowering, backward-weight: K rows = 16 pixels, M = (tap, ch)
 #pragma unroll
-                        for (int c = 0; c < kBM / 32; ++c)
-                            ptx::tma_load_im2col_4d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], bw_ch[c],
-                                                    p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
-                                                    uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
-                        px.c += kBK;
-                        while (px.c >= p.ic_m) {
-                            px.c -= p.ic_m;
-                            if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
-                        }
-                    } else if constexpr (!A_MN) {
-                        ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
-                    } else {
+                            for (int c = 0; c < kBM / 32; ++c)
+                                ptx::tma_load_im2col_4d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], bw_ch[c],
+                                                        p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
+                                                        uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
+                            px.c += kBK;
+                            while (px.c >= p.ic_m) {
+                                px.c -= p.ic_m;
+                                if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
+                            }
+                        } else if constexpr (!A_MN) {
+                            ptx::tma_load_2d(a_dst, &tmA, &full[stage], k0, m0);
+                        } else {
 #pragma unroll
-                        for (int c = 0; c < kBM / 32; ++c)
-                            ptx::tma_load_2d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], m0 + 32 * c, k0);
+                            for (int c = 0; c < kBM / 32; ++c)
+                                ptx::tma_load_2d(a_dst + c * 32 * kBK * 4, &tmA, &full[stage], m0 + 32 * c, k0);
+                        }
                     }
-                    if constexpr (A_IM == 2) {
-                        // B issued above (im2col)
-                    } else if constexpr (A_IM == 3) {
-                        // swapped backward-weight: B = 16 pixels x (BNL/32 x 32 channels of a tap)
+                    if (role_b) {
+                        if constexpr (A_IM == 2) {
+                            // B: BNL pixels x 16 channels of tap (ti, tj)
+                            ptx::tma_load_im2col_4d(b_dst, &tmB, &full[stage], cc * kBK, p.ic_s * px.c - p.ic_p,
+                                                    p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
+                            if (++cc == p.ic_cpt) {
+                                cc = 0;
+                                if (++tap_j == p.ic_k) { tap_j = 0; ++tap_i; }
+                            }
+                        } else if constexpr (A_IM == 3) {
+                            // swapped backward-weight: B = 16 pixels x (BNL/32 x 32 channels of a tap)
 #pragma unroll
-                        for (int c = 0; c < NBW; ++c)
-                            ptx::tma_load_im2col_4d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage], bw_ch[c],
-                                                    p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
-                                                    uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
-                        px.c += kBK;
-                        while (px.c >= p.ic_m) {
-                            px.c -= p.ic_m;
-                            if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
+                            for (int c = 0; c < NBW; ++c)
+                                ptx::tma_load_im2col_4d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage], bw_ch[c],
+                                                        p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
+                                                        uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
+                            px.c += kBK;
+                            while (px.c >= p.ic_m) {
+                                px.c -= p.ic_m;
+                                if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
+                            }
+                        } else if constexpr (!B_MN) {
+                            ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
+                        } else {
+#pragma unroll
+                            for (int c = 0; c < BNL / 32; ++c)
+                                ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage], n0 + 32 * c, k0);
                         }
-                    } else if constexpr (!B_MN) {
-                        ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
-                    } else {
-#pragma unroll
-                        for (int c = 0; c < BNL / 32; ++c)
-                            ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage], n0 + 32 * c, k0);
                     }
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
@@ -1013,6 +1022,13 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.s_nq = g.C.s_nq;
     kp.mlim = g.C.mlim;
     kp.nmlim = g.C.nmlim < (int64_t(1) << 31) ? int(g.C.nmlim) : INT32_MAX;
+    kp.split_producer = [] {
+        static const int v = [] {
+            const char* e = getenv("CCT_SPLIT_PRODUCER");
+            return e ? atoi(e) : 1;
+        }();
+        return v;
+    }();
     kp.bias = g.C.bias;
     kp.relu = g.C.relu;
 
