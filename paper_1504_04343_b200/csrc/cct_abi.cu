@@ -302,7 +302,18 @@ const float* dhat_of(const Geo& g, int type, const Lowered& L, const float* x, f
 cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStream_t st, const char* what,
                        bool* fused = nullptr) {
     const int64_t kb = (gp.K + kBK - 1) / kBK;
-    const int splits = int((kb + kMaxChainKB - 1) / kMaxChainKB);
+    int splits = int((kb + kMaxChainKB - 1) / kMaxChainKB);
+    // a 2-way accuracy split of a wide-tile K-major GEMM runs as two TMEM chains of one tile
+    // (no partial tiles, no reduce kernel); $CCT_CHAIN2=0 keeps the split-K form (A/B)
+    static const int chain2_env = [] {
+        const char* e = getenv("CCT_CHAIN2");
+        return e ? atoi(e) : 1;
+    }();
+    if (splits == 2 && chain2_env && gp.A.major == Major::K && gp.B.major == Major::K && !gp.C.transposed &&
+        gp.passes == 3 && tile_n(gp) >= 192) {
+        splits = 1;
+        gp.chain2 = 1;
+    }
     // a fused epilogue (bias / ReLU) applies to final stores only: not to split partials
     if (fused) *fused = splits == 1;
     if (splits > 1) {

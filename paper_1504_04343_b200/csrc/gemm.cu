@@ -184,7 +184,10 @@ struct WorkIter {
 // smem and writes it back column by column, so an output whose ROWS are contiguous
 // along the tile's N index (NCHW y of a swapped GEMM: rows = channels, columns =
 // pixels) is stored as 128-byte row segments instead of 4-byte scatters.
-template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0, int TRO = 0>
+// CH2: the tile's K range is accumulated as two chains (first / second half of the
+// k-blocks) in two TMEM accumulators and summed in the epilogue (fp32 round-to-nearest),
+// single-buffered: a 2-way accuracy split without partial tiles in HBM or a reduce kernel.
+template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0, int TRO = 0, int CH2 = 0>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm3xtf32_kernel(const __grid_constant__ CUtensorMap tmA,
                       const __grid_constant__ CUtensorMap tmB, const KParams p) {
@@ -192,13 +195,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int STAGES = C_::STAGES;
     constexpr int BNL = C_::BNL;
     // A_TM == 2: one accumulator per tile, the freed TMEM columns deepen the A ring
-    constexpr int NACC = (A_TM == 2) ? 1 : C_::NACC;
+    constexpr int NACC = CH2 ? 2 : (A_TM == 2) ? 1 : C_::NACC;
+    static_assert(!CH2 || (!A_TM && BN > 128), "CH2 config");
     constexpr uint32_t A_COL = uint32_t(2 * NACC * BN);               // first A column
     constexpr int kASlotsFit = int((512u - A_COL) / (2 * kBK));
     constexpr int kASlots = A_TM ? (kASlotsFit < 12 ? (kASlotsFit < STAGES - 1 ? kASlotsFit : STAGES - 1)
                                                     : (12 < STAGES - 1 ? 12 : STAGES - 1))
                                  : 4;                                 // TMEM ring of A tiles
-    constexpr uint32_t TMEM_COLS = A_TM ? 512u : C_::TMEM_COLS;
+    constexpr uint32_t TMEM_COLS = A_TM ? 512u : CH2 ? tmem_cols_for(BN) : C_::TMEM_COLS;
     static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots && kASlots >= 4),
                   "A_TM config");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -389,8 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             Work w;
             for (; wi.next(p, ngroups, w); ++local) {
                 const int kb0 = w.kb0, kb1 = w.kb1;
-                const int acc = local & 1;
-                const uint32_t use = uint32_t(local >> 1);
+                const int acc = CH2 ? 0 : (local & 1);  // CH2: one (two-chain) accumulator set
+                const uint32_t use = CH2 ? uint32_t(local) : uint32_t(local >> 1);
                 ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * NACC * BN);
@@ -426,6 +430,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk)
                             mma_ts(d_tmem + kk * (NACC - 1) * BN, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
+                    } else if constexpr (CH2) {
+                        // chain 0: k-blocks [kb0, kbh), chain 1: [kbh, kb1), each in its accumulator
+                        const int kbh = kb0 + (kb1 - kb0 + 1) / 2;
+                        const uint32_t dch = d_tmem + (kb >= kbh ? uint32_t(BN) : 0u);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 8; ++kk) {
+                            const uint64_t ad = tile_desc<A_MN>(a_raw, kk);
+                            const uint64_t bd = tile_desc<B_MN>(b_raw, kk);
+                            const uint32_t first = ((kb != kb0 && kb != kbh) || kk > 0) ? 1u : 0u;
+                            mma(dch, tile_desc<A_MN>(a_sml, kk), bd, first);
+                            mma(dch, ad, tile_desc<B_MN>(b_sml, kk), 1u);
+                            mma(dch, ad, bd, 1u);
+                        }
                     } else if constexpr (NACC == 1) {
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk) {
@@ -482,8 +499,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int rest = u / p.num_m_tiles;
             const int nt = rest % p.num_n_tiles;
             const int sp = rest / p.num_n_tiles;
-            const int acc = local & 1;
-            const uint32_t use = uint32_t(local >> 1);
+            const int acc = CH2 ? 0 : (local & 1);
+            const uint32_t use = CH2 ? uint32_t(local) : uint32_t(local >> 1);
             ptx::mbar_wait(&tfull[acc], use & 1);
             ptx::tc_fence_after();
             const int64_t row = int64_t(mt) * (kBM * CG) + int64_t(rank) * kBM + rit;
@@ -802,10 +819,10 @@ bool make_tmap_im2col(CUtensorMap* map, const Im2col& ic, bool mn_major, int box
     return true;
 }
 
-template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0, int TRO = 0>
+template <int BN, int A_MN, int B_MN, int CG, int A_IM, int A_TM = 0, int TRO = 0, int CH2 = 0>
 cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& kp, cudaStream_t st) {
     using C_ = Cfg<BN, CG, TRO>;
-    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM, A_TM, TRO>;
+    auto kern = gemm3xtf32_kernel<BN, A_MN, B_MN, CG, A_IM, A_TM, TRO, CH2>;
     // per call (idempotent, ~1 us): the attribute is per device, and callers may switch devices
     // or threads; a process-wide "done" flag would miss the second GPU
     {
@@ -847,6 +864,15 @@ template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
+    if (g.chain2) {  // two-chain accumulation (K-major operands, wide tiles)
+        if constexpr (BN >= 192) {
+            if (amn || bmn || g.passes != 3) return cudaErrorInvalidValue;
+            if (g.im2col.x && g.im2col.operand == 1) return launch<BN, 0, 0, CG, 2, 0, 0, 1>(ta, tb, kp, st);
+            if (g.im2col.x && g.im2col.operand == 0) return launch<BN, 0, 0, CG, 1, 0, 0, 1>(ta, tb, kp, st);
+            if (!g.im2col.x) return launch<BN, 0, 0, CG, 0, 0, 0, 1>(ta, tb, kp, st);
+        }
+        return cudaErrorInvalidValue;
+    }
     if (g.C.transposed) {  // swapped forward of a narrow bank: y rows = channels
         if constexpr (CG == 1 && BN >= 192) {
             if (amn || bmn) return cudaErrorInvalidValue;
@@ -975,7 +1001,7 @@ SkPlan sk_plan(const GemmProblem& g) {
         const char* e = getenv("CCT_STREAMK");
         return e ? atoi(e) : 1;
     }();
-    if (!enabled || g.splits > 1 || g.M <= 0 || g.N <= 0 || g.K <= 0) return sp;
+    if (!enabled || g.splits > 1 || g.chain2 || g.M <= 0 || g.N <= 0 || g.K <= 0) return sp;
     const int bn = tile_n(g);
     const int cg = choose_cg(g, bn);
     const int64_t tiles = ((g.M + kBM * cg - 1) / (kBM * cg)) * ((g.N + bn - 1) / bn);

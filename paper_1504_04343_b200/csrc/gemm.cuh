@@ -64,6 +64,8 @@ struct GemmProblem {
     Operand A, B;
     OutMap C;
     int splits = 1;  // split-K factor; each split writes its own slice (s_split)
+    int chain2 = 0;  // two accumulation chains in TMEM (K halves) summed in the epilogue
+                     // instead of a 2-way split-K (K-major operands, tile width >= 192)
     int passes = 3;  // 3 = 3xTF32 (fp32-accurate), 1 = plain TF32 (diagnostic only)
     int bn = 0;      // 0 = choose
     Im2col im2col;   // implicit lowering of A (Type 1)
@@ -94,6 +96,8 @@ int choose_bn(int64_t N);
 int choose_splits(int64_t M, int64_t N, int64_t K, int num_sms, int bn, int cg);
 // the same for a concrete problem (tile width and CTA-pair mode as run_gemm picks them)
 int plan_splits(const GemmProblem& g);
+// tile width the kernel uses for a problem
+int tile_n(const GemmProblem& g);
 
 cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream);
 
