@@ -349,6 +349,18 @@ void wgrad_im2col(GemmProblem& gp, const Geo& g, const float* x) {
     }
 }
 
+// Backward-weight reductions (K = b m^2 pixels) are split for accuracy and wave fill; with
+// two TMEM chains per unit (CH2) the accuracy floor halves, so half as many partial tiles
+// reach HBM.  Wide tiles only (two 256-column accumulators fit TMEM).  $CCT_CHAIN2=0: off.
+int wgrad_chain2(const GemmProblem& gp) {
+    static const int env = [] {
+        const char* e = getenv("CCT_CHAIN2");
+        return e ? atoi(e) : 1;
+    }();
+    return (env && gp.passes == 3 && !gp.C.transposed && tile_n(gp) >= 192 &&
+            gp.K > int64_t(kMaxChainKB) * kBK) ? 1 : 0;
+}
+
 // backward-weight GEMM: dW^T (cols x ncols) = Dhat^T * dRhat, reduction over rows
 GemmProblem wgrad_problem(const Lowered& L, Operand a, Operand b) {
     GemmProblem gp;
@@ -529,6 +541,7 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
         } else if (implicit) {
             wgrad_im2col(gp, g, x);
         }
+        gp.chain2 = wgrad_chain2(gp);
         const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;
@@ -636,6 +649,7 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
             gp.B = {dh, ldd, Major::MN};
         }
         if (implicit) wgrad_im2col(gp, g, x);
+        gp.chain2 = wgrad_chain2(gp);
         const int splits = plan_splits(gp);
         const int64_t wsize = L.ncols * L.cols;
         float* parts = splits > 1 ? ws.take(int64_t(splits) * wsize) : dw;

@@ -864,12 +864,28 @@ template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
-    if (g.chain2) {  // two-chain accumulation (K-major operands, wide tiles)
+    if (g.chain2) {  // two-chain accumulation (wide tiles)
         if constexpr (BN >= 192) {
-            if (amn || bmn || g.passes != 3) return cudaErrorInvalidValue;
-            if (g.im2col.x && g.im2col.operand == 1) return launch<BN, 0, 0, CG, 2, 0, 0, 1>(ta, tb, kp, st);
-            if (g.im2col.x && g.im2col.operand == 0) return launch<BN, 0, 0, CG, 1, 0, 0, 1>(ta, tb, kp, st);
-            if (!g.im2col.x) return launch<BN, 0, 0, CG, 0, 0, 0, 1>(ta, tb, kp, st);
+            if (g.passes != 3) return cudaErrorInvalidValue;
+            if (g.im2col.x && g.im2col.operand == 1) {
+                if (amn || bmn) return cudaErrorInvalidValue;
+                return launch<BN, 0, 0, CG, 2, 0, 0, 1>(ta, tb, kp, st);
+            }
+            if (g.im2col.x && g.im2col.operand == 2) {  // swapped backward-weight of a narrow bank
+                if (!bmn) return cudaErrorInvalidValue;
+                return amn ? launch<BN, 1, 1, CG, 3, 0, 0, 1>(ta, tb, kp, st) : launch<BN, 0, 1, CG, 3, 0, 0, 1>(ta, tb, kp, st);
+            }
+            if (g.im2col.x && g.im2col.operand == 0) {  // forward (K, K) / backward-weight (MN, K | MN)
+                if (!amn && !bmn) return launch<BN, 0, 0, CG, 1, 0, 0, 1>(ta, tb, kp, st);
+                if (amn && bmn) return launch<BN, 1, 1, CG, 1, 0, 0, 1>(ta, tb, kp, st);
+                if (amn) return launch<BN, 1, 0, CG, 1, 0, 0, 1>(ta, tb, kp, st);
+                return cudaErrorInvalidValue;
+            }
+            if (!g.im2col.x) {
+                if (!amn && !bmn) return launch<BN, 0, 0, CG, 0, 0, 0, 1>(ta, tb, kp, st);
+                if (amn && !bmn) return launch<BN, 1, 0, CG, 0, 0, 0, 1>(ta, tb, kp, st);  // materialised wgrad
+                if (!amn && bmn) return launch<BN, 0, 1, CG, 0, 0, 0, 1>(ta, tb, kp, st);  // swapped (narrow bank)
+            }
         }
         return cudaErrorInvalidValue;
     }
@@ -951,11 +967,12 @@ int choose_bn(int64_t N) {
 // kMaxChainK; longer reductions are split and the partials summed in fp32
 // round-to-nearest by the deterministic reduce kernel.  Short-K problems with
 // too few tiles to fill the machine are also split.
-int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn, int cg) {
+int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn, int cg, int chains) {
     const int64_t tiles = ((M + kBM * cg - 1) / (kBM * cg)) * ((N + bn - 1) / bn);
     const int64_t slots = sms / cg;  // one CTA (pair) per SM (pair)
     const int64_t kb = (K + kBK - 1) / kBK;
-    const int64_t s_min = std::max<int64_t>(1, (kb + kMaxChainKB - 1) / kMaxChainKB);  // accuracy floor
+    // accuracy floor: every TMEM chain <= kMaxChainKB k-blocks (chains per unit: 1, or 2 with CH2)
+    const int64_t s_min = std::max<int64_t>(1, (kb + int64_t(kMaxChainKB) * chains - 1) / (int64_t(kMaxChainKB) * chains));
     if (kb < 64) return int(s_min);
     // Pick the split count in [s_min, 4 s_min] (>= 16 k-blocks per split) whose
     // (pair-)units fill the last wave of the machine best; ties keep the smaller
@@ -984,7 +1001,7 @@ int tile_n(const GemmProblem& g) {
 
 int plan_splits(const GemmProblem& g) {
     const int bn = tile_n(g);
-    return choose_splits(g.M, g.N, g.K, num_sms(), bn, choose_cg(g, bn));
+    return choose_splits(g.M, g.N, g.K, num_sms(), bn, choose_cg(g, bn), g.chain2 ? 2 : 1);
 }
 
 // Stream-K plan: used for an unsplit GEMM of at least one wave whose whole-tile

@@ -93,7 +93,7 @@ constexpr int kMaxChainKB = 256;
 int choose_bn(int64_t N);
 // split-K factor: at least the accuracy floor (chains <= kMaxChainKB k-blocks),
 // then the count whose (pair-)units fill the last wave best
-int choose_splits(int64_t M, int64_t N, int64_t K, int num_sms, int bn, int cg);
+int choose_splits(int64_t M, int64_t N, int64_t K, int num_sms, int bn, int cg, int chains = 1);
 // the same for a concrete problem (tile width and CTA-pair mode as run_gemm picks them)
 int plan_splits(const GemmProblem& g);
 // tile width the kernel uses for a problem
