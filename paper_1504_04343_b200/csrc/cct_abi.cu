@@ -310,7 +310,7 @@ cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStr
         return e ? atoi(e) : 1;
     }();
     if (splits == 2 && chain2_env && gp.A.major == Major::K && gp.B.major == Major::K && !gp.C.transposed &&
-        gp.passes == 3 && tile_n(gp) >= 192) {
+        gp.passes == 3 && tile_n(gp) >= 192 && tile_n(gp) <= 256) {
         splits = 1;
         gp.chain2 = 1;
     }
@@ -357,7 +357,8 @@ int wgrad_chain2(const GemmProblem& gp) {
         const char* e = getenv("CCT_CHAIN2");
         return e ? atoi(e) : 1;
     }();
-    return (env && gp.passes == 3 && !gp.C.transposed && tile_n(gp) >= 192 &&
+    const int bn = tile_n(gp);
+    return (env && gp.passes == 3 && !gp.C.transposed && bn >= 192 && bn <= 256 &&
             gp.K > int64_t(kMaxChainKB) * kBK) ? 1 : 0;
 }
 

@@ -72,7 +72,9 @@ double interp_rate(double bn, double k) {
     return (r0 * (1 - fb) + r1 * fb) * 1e12;
 }
 
-// GEMM time: padded flops / measured rate for the tile width the kernel picks.
+// GEMM time: padded flops / measured rate for the tile width the kernel picks.  N a
+// multiple of 384 runs the 256 + 128 composite tile (gemm.cu tile_n), measured at the
+// 256-wide rate (conv4 forward: 271 TF/s algorithmic).
 double gemm_seconds(double M, double N, double K, const cct_calibration* c) {
     static const double cands[] = {256, 192, 128, 96, 64};
     double bn = 256, best = 1e300;
@@ -80,7 +82,8 @@ double gemm_seconds(double M, double N, double K, const cct_calibration* c) {
         const double pad = rup(N, x);
         if (pad < best) { best = pad; bn = x; }
     }
-    const double rate = interp_rate(bn, std::min(K, 4096.0)) * (c->gemm_flops_per_s / kRateRef);
+    const bool wide384 = std::fmod(N, 384.0) == 0;
+    const double rate = interp_rate(wide384 ? 256.0 : bn, std::min(K, 4096.0)) * (c->gemm_flops_per_s / kRateRef);
     return 2.0 * rup(M, 128) * rup(N, bn) * K / rate;
 }
 

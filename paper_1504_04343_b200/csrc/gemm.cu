@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int kASlots = A_TM ? (kASlotsFit < 12 ? (kASlotsFit < STAGES - 1 ? kASlotsFit : STAGES - 1)
                                                     : (12 < STAGES - 1 ? 12 : STAGES - 1))
                                  : 4;                                 // TMEM ring of A tiles
-    constexpr uint32_t TMEM_COLS = A_TM ? 512u : CH2 ? tmem_cols_for(BN) : C_::TMEM_COLS;
+    // single-buffered accumulator: CH2 (two chains) and the 384-wide tile (256 + 128 columns)
+    constexpr bool SB = CH2 || BN > 256;
+    static_assert(BN <= 256 || (BN == 384 && !A_TM && !CH2 && !TRO && !A_MN && !B_MN), "BN 384 config");
+    constexpr uint32_t TMEM_COLS = A_TM ? 512u : SB ? 512u : C_::TMEM_COLS;
     static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots && kASlots >= 4),
                   "A_TM config");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -369,6 +372,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 px.c -= p.ic_m;
                                 if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
                             }
+                        } else if constexpr (BN == 384) {
+                            // 64-row boxes: the CTA's rows of sub-tile 1 (256/CG), then of sub-tile 2 (128/CG)
+                            const int nb = nt * BN;
+#pragma unroll
+                            for (int c = 0; c < 4 / CG; ++c)
+                                ptx::tma_load_2d(b_dst + c * 64 * kBK * 4, &tmB, &full[stage], k0,
+                                                 nb + int(rank) * (256 / CG) + 64 * c);
+#pragma unroll
+                            for (int c = 0; c < 2 / CG; ++c)
+                                ptx::tma_load_2d(b_dst + (4 / CG + c) * 64 * kBK * 4, &tmB, &full[stage], k0,
+                                                 nb + 256 + int(rank) * (128 / CG) + 64 * c);
                         } else if constexpr (!B_MN) {
                             ptx::tma_load_2d(b_dst, &tmB, &full[stage], k0, n0);
                         } else {
@@ -384,7 +398,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA only) =====================
         if (lane == 0 && leader) {
-            constexpr uint32_t idesc = ptx::idesc_tf32(kBM * CG, BN, A_MN, B_MN);
+            // (BN = 384: two MMAs per step, N = 256 into columns [0, 256) and N = 128 into [256, 384))
+            constexpr uint32_t idesc = ptx::idesc_tf32(kBM * CG, BN > 256 ? 256 : BN, A_MN, B_MN);
+            constexpr uint32_t idesc2 = ptx::idesc_tf32(kBM * CG, BN > 256 ? BN - 256 : BN, A_MN, B_MN);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -393,14 +409,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             Work w;
             for (; wi.next(p, ngroups, w); ++local) {
                 const int kb0 = w.kb0, kb1 = w.kb1;
-                const int acc = CH2 ? 0 : (local & 1);  // CH2: one (two-chain) accumulator set
-                const uint32_t use = CH2 ? uint32_t(local) : uint32_t(local >> 1);
+                const int acc = SB ? 0 : (local & 1);  // single-buffered: one accumulator set
+                const uint32_t use = SB ? uint32_t(local) : uint32_t(local >> 1);
                 ptx::mbar_wait(&tempty[acc], (use & 1) ^ 1);
                 ptx::tc_fence_after();
                 const uint32_t d_tmem = tmem_base + uint32_t(acc * NACC * BN);
                 auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
                     if constexpr (CG == 1) ptx::mma_tf32(d, a, b, idesc, accumulate);
                     else ptx::mma_tf32_cg2(d, a, b, idesc, accumulate);
+                };
+                auto mma2 = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t accumulate) {
+                    if constexpr (CG == 1) ptx::mma_tf32(d, a, b, idesc2, accumulate);
+                    else ptx::mma_tf32_cg2(d, a, b, idesc2, accumulate);
                 };
                 auto mma_ts = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t accumulate) {
                     if constexpr (CG == 1) ptx::mma_tf32_ts(d, a, b, idesc, accumulate);
@@ -430,6 +450,22 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk)
                             mma_ts(d_tmem + kk * (NACC - 1) * BN, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
+                    } else if constexpr (BN == 384) {
+                        // this CTA's B rows: 256/CG of the first sub-tile, then 128/CG of the second
+                        constexpr uint32_t SUB2 = uint32_t(256 / CG) * kBK * 4;
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 8; ++kk) {
+                            const uint64_t ad = tile_desc<0>(a_raw, kk), as = tile_desc<0>(a_sml, kk);
+                            const uint64_t b1 = tile_desc<0>(b_raw, kk), b2 = tile_desc<0>(b_raw + SUB2, kk);
+                            const uint64_t s1 = tile_desc<0>(b_sml, kk), s2 = tile_desc<0>(b_sml + SUB2, kk);
+                            const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
+                            mma(d_tmem, as, b1, first);
+                            mma2(d_tmem + 256, as, b2, first);
+                            mma(d_tmem, ad, s1, 1u);
+                            mma2(d_tmem + 256, ad, s2, 1u);
+                            mma(d_tmem, ad, b1, 1u);
+                            mma2(d_tmem + 256, ad, b2, 1u);
+                        }
                     } else if constexpr (CH2) {
                         // chain 0: k-blocks [kb0, kbh), chain 1: [kbh, kb1), each in its accumulator
                         const int kbh = kb0 + (kb1 - kb0 + 1) / 2;
@@ -499,8 +535,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int rest = u / p.num_m_tiles;
             const int nt = rest % p.num_n_tiles;
             const int sp = rest / p.num_n_tiles;
-            const int acc = CH2 ? 0 : (local & 1);
-            const uint32_t use = CH2 ? uint32_t(local) : uint32_t(local >> 1);
+            const int acc = SB ? 0 : (local & 1);
+            const uint32_t use = SB ? uint32_t(local) : uint32_t(local >> 1);
             ptx::mbar_wait(&tfull[acc], use & 1);
             ptx::tc_fence_after();
             const int64_t row = int64_t(mt) * (kBM * CG) + int64_t(rank) * kBM + rit;
@@ -861,8 +897,8 @@ int a_in_tmem_mode() {
 }
 
 template <int BN, int CG>
-cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
-                            const KParams& kp, cudaStream_t st) {
+cudaError_t dispatch_std(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
+                         const KParams& kp, cudaStream_t st) {
     const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
     if (g.chain2) {  // two-chain accumulation (wide tiles)
         if constexpr (BN >= 192) {
@@ -926,6 +962,19 @@ cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const C
     if (amn && bmn) return launch<BN, 1, 1, CG, 0>(ta, tb, kp, st);
     if (amn && !bmn) return launch<BN, 1, 0, CG, 0>(ta, tb, kp, st);
     return launch<BN, 0, 1, CG, 0>(ta, tb, kp, st);
+}
+
+template <int BN, int CG>
+cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
+                            const KParams& kp, cudaStream_t st) {
+    if constexpr (BN == 384) {  // 256 + 128 composite tile: K-major operands, A ordinary or im2col
+        const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
+        if (amn || bmn || g.chain2 || g.C.transposed || g.passes != 3 || (g.im2col.x && g.im2col.operand != 0))
+            return cudaErrorInvalidValue;
+        return g.im2col.x ? launch<384, 0, 0, CG, 1>(ta, tb, kp, st) : launch<384, 0, 0, CG, 0>(ta, tb, kp, st);
+    } else {
+        return dispatch_std<BN, CG>(g, ta, tb, kp, st);
+    }
 }
 
 // CTA-pair mode needs >= 2 row tiles and, for an MN-major B, B halves that are
@@ -996,6 +1045,16 @@ int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn, int cg, int 
 int tile_n(const GemmProblem& g) {
     if (g.bn) return g.bn;
     if (g.C.transposed) return ((g.N + 191) / 192) * 192 < ((g.N + 255) / 256) * 256 ? 192 : 256;
+    // N a multiple of 384 (conv3/4 o, conv4/5 d): one 256 + 128 composite tile instead of two
+    // 192-wide ones (a 192-wide MMA costs about as much as a 256-wide one); K-major operands,
+    // no epilogue transposition, no chain split.  $CCT_BN384=0 disables it (A/B).
+    static const int bn384 = [] {
+        const char* e = getenv("CCT_BN384");
+        return e ? atoi(e) : 1;
+    }();
+    if (bn384 && g.N % 384 == 0 && g.A.major == Major::K && g.B.major == Major::K && !g.chain2 && g.passes == 3 &&
+        !(g.im2col.x && g.im2col.operand != 0))
+        return 384;
     return choose_bn(g.N);
 }
 
@@ -1118,9 +1177,10 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     } else if (!make_tmap(&ta, g.A, g.M, g.K, kBM)) {
         return cudaErrorInvalidValue;
     }
-    if (!b_im && !make_tmap(&tb, g.B, g.N, g.K, bn / cg)) return cudaErrorInvalidValue;
+    if (!b_im && !make_tmap(&tb, g.B, g.N, g.K, bn == 384 ? 64 : bn / cg)) return cudaErrorInvalidValue;
     if (cg == 2) {
         switch (bn) {
+        case 384: return dispatch_layout<384, 2>(g, ta, tb, kp, stream);
         case 256: return dispatch_layout<256, 2>(g, ta, tb, kp, stream);
         case 192: return dispatch_layout<192, 2>(g, ta, tb, kp, stream);
         case 128: return dispatch_layout<128, 2>(g, ta, tb, kp, stream);
@@ -1130,6 +1190,7 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
         }
     }
     switch (bn) {
+    case 384: return dispatch_layout<384, 1>(g, ta, tb, kp, stream);
     case 256: return dispatch_layout<256, 1>(g, ta, tb, kp, stream);
     case 192: return dispatch_layout<192, 1>(g, ta, tb, kp, stream);
     case 128: return dispatch_layout<128, 1>(g, ta, tb, kp, stream);
