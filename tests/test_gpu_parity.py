@@ -216,7 +216,8 @@ def test_wgrad_full_batch_vs_fp64_gemm(cct, dev):
     assert err <= TOL, err
 
 
-@pytest.mark.parametrize("layer", [("conv3", 13, 3, 256, 384, 1, 1), ("conv5", 13, 3, 384, 256, 1, 1),
+@pytest.mark.parametrize("layer", [("conv3", 13, 3, 256, 384, 1, 1), ("conv4", 13, 3, 384, 384, 1, 1),
+                                   ("conv5", 13, 3, 384, 256, 1, 1), ("conv2", 27, 5, 96, 256, 1, 2),
                                    ("conv1", 227, 11, 3, 96, 4, 0)], ids=lambda l: l[0])
 def test_caffenet_b256_vs_fp64(cct, dev, layer):
     """Full-batch (b = 256) training step of CaffeNet layers exactly as the bench runs it
@@ -521,3 +522,26 @@ def test_swapped_forward_opt_in(cct, dev):
     assert r.returncode == 0, r.stderr[-3000:]
     errs = json.loads(r.stdout.strip().splitlines()[-1])
     assert len(errs) == 4 and max(errs.values()) <= TOL, errs
+
+
+@pytest.mark.parametrize("M,N,K", [(100, 384, 40), (300, 384, 3000), (5000, 768, 1000), (40000, 384, 3456),
+                                   (700, 1152, 17)])
+def test_composite_384_tile(cct, dev, M, N, K):
+    """N a multiple of 384 with K-major operands runs the 256 + 128 composite tile
+    (single-buffered, 64-row B boxes), CTA pairs or not, stream-K when ragged: against
+    an fp64 GEMM (checker only)."""
+    import ctypes as C
+    L = cct.lib()
+    L.cct_debug_gemm.argtypes = [C.c_int64] * 3 + [C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_int64, C.c_int,
+                                                   C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_int, C.c_void_p]
+    g = torch.Generator(device=dev).manual_seed(M + N + K)
+    ld = (K + 3) // 4 * 4
+    A = torch.rand((M, ld), generator=g, device=dev) * 2 - 1
+    B = torch.rand((N, ld), generator=g, device=dev) * 2 - 1
+    Cm = torch.empty((M, N), device=dev)
+    st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    rc = L.cct_debug_gemm(M, N, K, A.data_ptr(), ld, 0, B.data_ptr(), ld, 0, Cm.data_ptr(), N, 1, 3, 0, st)
+    assert rc == 0, L.cct_last_error()
+    ref = A[:, :K].double() @ B[:, :K].double().t()
+    err = float(torch.linalg.norm(Cm.double() - ref) / torch.linalg.norm(ref))
+    assert err <= TOL, err
