@@ -302,7 +302,7 @@ const float* dhat_of(const Geo& g, int type, const Lowered& L, const float* x, f
 cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStream_t st, const char* what,
                        bool* fused = nullptr) {
     const int64_t kb = (gp.K + kBK - 1) / kBK;
-    int splits = int((kb + kMaxChainKB - 1) / kMaxChainKB);
+    int splits = effective_splits(kb, int((kb + kMaxChainKB - 1) / kMaxChainKB));
     // a 2-way accuracy split of a wide-tile K-major GEMM runs as two TMEM chains of one tile
     // (no partial tiles, no reduce kernel); $CCT_CHAIN2=0 keeps the split-K form (A/B)
     static const int chain2_env = [] {
@@ -1243,7 +1243,7 @@ static cct_status gemm_common(int64_t M, int64_t N, int64_t K, const float* A, i
     gp.A = {B, ldb, Major::MN};
     gp.B = {A, lda, Major::K};
     gp.passes = passes;
-    int splits = split_k > 0 ? split_k : plan_splits(gp);
+    int splits = split_k > 0 ? effective_splits((K + kBK - 1) / kBK, split_k) : plan_splits(gp);
     if (passes != 3) splits = 1;
     if (splits > 1) {
         const size_t need = size_t(splits) * size_t(M) * size_t(N) * 4;
@@ -1268,7 +1268,7 @@ cct_status cct_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int split_k,
     gp.K = K;
     gp.A.major = Major::MN;
     gp.B.major = Major::K;
-    const int splits = split_k > 0 ? split_k : plan_splits(gp);
+    const int splits = split_k > 0 ? effective_splits((K + kBK - 1) / kBK, split_k) : plan_splits(gp);
     *bytes = splits > 1 ? size_t(splits) * size_t(M) * size_t(N) * 4 : 0;
     return CCT_OK;
 }

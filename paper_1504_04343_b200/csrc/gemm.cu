@@ -204,7 +204,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                  : 4;                                 // TMEM ring of A tiles
     // single-buffered accumulator: CH2 (two chains) and the 384-wide tile (256 + 128 columns)
     constexpr bool SB = CH2 || BN > 256;
-    static_assert(BN <= 256 || (BN == 384 && !A_TM && !CH2 && !TRO && !A_MN && !B_MN), "BN 384 config");
+    static_assert(BN <= 256 || (BN == 384 && !A_TM && !CH2 && !TRO && A_IM <= 1), "BN 384 config");
     constexpr uint32_t TMEM_COLS = A_TM ? 512u : SB ? 512u : C_::TMEM_COLS;
     static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots && kASlots >= 4),
                   "A_TM config");
@@ -372,6 +372,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 px.c -= p.ic_m;
                                 if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
                             }
+                        } else if constexpr (BN == 384 && B_MN) {
+                            // 32-column boxes: the CTA's columns of sub-tile 1 (256/CG), then of sub-tile 2
+                            const int nb = nt * BN;
+#pragma unroll
+                            for (int c = 0; c < 8 / CG; ++c)
+                                ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, &full[stage],
+                                                 nb + int(rank) * (256 / CG) + 32 * c, k0);
+#pragma unroll
+                            for (int c = 0; c < 4 / CG; ++c)
+                                ptx::tma_load_2d(b_dst + (8 / CG + c) * 32 * kBK * 4, &tmB, &full[stage],
+                                                 nb + 256 + int(rank) * (128 / CG) + 32 * c, k0);
                         } else if constexpr (BN == 384) {
                             // 64-row boxes: the CTA's rows of sub-tile 1 (256/CG), then of sub-tile 2 (128/CG)
                             const int nb = nt * BN;
@@ -452,12 +463,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             mma_ts(d_tmem + kk * (NACC - 1) * BN, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
                     } else if constexpr (BN == 384) {
                         // this CTA's B rows: 256/CG of the first sub-tile, then 128/CG of the second
+                        // (K-major: 256/CG rows of 64 B; MN-major: (256/CG)/32 chunks of 2 KB -- same bytes)
                         constexpr uint32_t SUB2 = uint32_t(256 / CG) * kBK * 4;
 #pragma unroll
                         for (int kk = 0; kk < kBK / 8; ++kk) {
-                            const uint64_t ad = tile_desc<0>(a_raw, kk), as = tile_desc<0>(a_sml, kk);
-                            const uint64_t b1 = tile_desc<0>(b_raw, kk), b2 = tile_desc<0>(b_raw + SUB2, kk);
-                            const uint64_t s1 = tile_desc<0>(b_sml, kk), s2 = tile_desc<0>(b_sml + SUB2, kk);
+                            const uint64_t ad = tile_desc<A_MN>(a_raw, kk), as = tile_desc<A_MN>(a_sml, kk);
+                            const uint64_t b1 = tile_desc<B_MN>(b_raw, kk), b2 = tile_desc<B_MN>(b_raw + SUB2, kk);
+                            const uint64_t s1 = tile_desc<B_MN>(b_sml, kk), s2 = tile_desc<B_MN>(b_sml + SUB2, kk);
                             const uint32_t first = (kb > kb0 || kk > 0) ? 1u : 0u;
                             mma(d_tmem, as, b1, first);
                             mma2(d_tmem + 256, as, b2, first);
@@ -967,11 +979,20 @@ cudaError_t dispatch_std(const GemmProblem& g, const CUtensorMap& ta, const CUte
 template <int BN, int CG>
 cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const CUtensorMap& tb,
                             const KParams& kp, cudaStream_t st) {
-    if constexpr (BN == 384) {  // 256 + 128 composite tile: K-major operands, A ordinary or im2col
+    if constexpr (BN == 384) {  // 256 + 128 composite tile; A ordinary or im2col (A side)
         const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
-        if (amn || bmn || g.chain2 || g.C.transposed || g.passes != 3 || (g.im2col.x && g.im2col.operand != 0))
+        if (g.chain2 || g.C.transposed || g.passes != 3 || (g.im2col.x && g.im2col.operand != 0))
             return cudaErrorInvalidValue;
-        return g.im2col.x ? launch<384, 0, 0, CG, 1>(ta, tb, kp, st) : launch<384, 0, 0, CG, 0>(ta, tb, kp, st);
+        if (g.im2col.x) {
+            if (!amn && !bmn) return launch<384, 0, 0, CG, 1>(ta, tb, kp, st);     // forward
+            if (amn && bmn) return launch<384, 1, 1, CG, 1>(ta, tb, kp, st);       // backward-weight, dy NHWC
+            if (amn) return launch<384, 1, 0, CG, 1>(ta, tb, kp, st);              // backward-weight, dRhat
+            return cudaErrorInvalidValue;
+        }
+        if (!amn && !bmn) return launch<384, 0, 0, CG, 0>(ta, tb, kp, st);
+        if (!amn && bmn) return launch<384, 0, 1, CG, 0>(ta, tb, kp, st);          // swapped materialised wgrad
+        if (amn && !bmn) return launch<384, 1, 0, CG, 0>(ta, tb, kp, st);          // materialised wgrad
+        return launch<384, 1, 1, CG, 0>(ta, tb, kp, st);
     } else {
         return dispatch_std<BN, CG>(g, ta, tb, kp, st);
     }
@@ -1016,6 +1037,15 @@ int choose_bn(int64_t N) {
 // kMaxChainK; longer reductions are split and the partials summed in fp32
 // round-to-nearest by the deterministic reduce kernel.  Short-K problems with
 // too few tiles to fill the machine are also split.
+// The kernel gives every split ceil(kb / s) k-blocks and drops empty splits, so a request of
+// s splits may run as fewer (e.g. kb 6050, s 96 -> 64 k-blocks each -> 95 splits).  Callers
+// size and reduce the partial slices with the count that actually runs.
+int effective_splits(int64_t kb, int s) {
+    if (s <= 1 || kb <= 1) return 1;
+    const int64_t per = (kb + s - 1) / s;
+    return int((kb + per - 1) / per);
+}
+
 int choose_splits(int64_t M, int64_t N, int64_t K, int sms, int bn, int cg, int chains) {
     const int64_t tiles = ((M + kBM * cg - 1) / (kBM * cg)) * ((N + bn - 1) / bn);
     const int64_t slots = sms / cg;  // one CTA (pair) per SM (pair)
@@ -1052,7 +1082,8 @@ int tile_n(const GemmProblem& g) {
         const char* e = getenv("CCT_BN384");
         return e ? atoi(e) : 1;
     }();
-    if (bn384 && g.N % 384 == 0 && g.A.major == Major::K && g.B.major == Major::K && !g.chain2 && g.passes == 3 &&
+    // (also 256 < N <= 384: one composite tile pads no more than two 192-wide ones)
+    if (bn384 && (g.N % 384 == 0 || (g.N > 256 && g.N <= 384)) && !g.chain2 && g.passes == 3 &&
         !(g.im2col.x && g.im2col.operand != 0))
         return 384;
     return choose_bn(g.N);
@@ -1060,7 +1091,8 @@ int tile_n(const GemmProblem& g) {
 
 int plan_splits(const GemmProblem& g) {
     const int bn = tile_n(g);
-    return choose_splits(g.M, g.N, g.K, num_sms(), bn, choose_cg(g, bn), g.chain2 ? 2 : 1);
+    return effective_splits((g.K + kBK - 1) / kBK,
+                            choose_splits(g.M, g.N, g.K, num_sms(), bn, choose_cg(g, bn), g.chain2 ? 2 : 1));
 }
 
 // Stream-K plan: used for an unsplit GEMM of at least one wave whose whole-tile

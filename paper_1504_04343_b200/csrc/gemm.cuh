@@ -94,8 +94,11 @@ int choose_bn(int64_t N);
 // split-K factor: at least the accuracy floor (chains <= kMaxChainKB k-blocks),
 // then the count whose (pair-)units fill the last wave best
 int choose_splits(int64_t M, int64_t N, int64_t K, int num_sms, int bn, int cg, int chains = 1);
-// the same for a concrete problem (tile width and CTA-pair mode as run_gemm picks them)
+// the same for a concrete problem (tile width and CTA-pair mode as run_gemm picks them);
+// the count that actually runs (no empty split)
 int plan_splits(const GemmProblem& g);
+// splits that run when s are requested over kb k-blocks (empty trailing splits dropped)
+int effective_splits(int64_t kb, int s);
 // tile width the kernel uses for a problem
 int tile_n(const GemmProblem& g);
 

@@ -152,3 +152,16 @@ def test_select_scale_invariance(cct):
     cal.launch_s /= 10
     t1, _ = cct.select_lowering(desc, 3, cal)
     assert t0 == t1
+
+
+def test_split_k_request_is_normalised_to_running_splits():
+    """CPU: a split-K request that would leave empty trailing splits (kb 6050 over 96 ->
+    64 k-blocks each -> 95 run) is sized for the splits that actually run."""
+    import ctypes as C
+    import paper_1504_04343_b200 as cct
+    out = C.c_size_t()
+    M, N, K = 20, 30, 6050 * 16
+    assert cct.lib().cct_gemm_workspace_size(M, N, K, 96, C.byref(out)) == 0
+    assert out.value == 95 * M * N * 4
+    assert cct.lib().cct_gemm_workspace_size(M, N, K, 50, C.byref(out)) == 0
+    assert out.value == 50 * M * N * 4  # 121 k-blocks each: all 50 run

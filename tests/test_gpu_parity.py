@@ -545,3 +545,18 @@ def test_composite_384_tile(cct, dev, M, N, K):
     ref = A[:, :K].double() @ B[:, :K].double().t()
     err = float(torch.linalg.norm(Cm.double() - ref) / torch.linalg.norm(ref))
     assert err <= TOL, err
+
+
+@pytest.mark.parametrize("split_k", [7, 96, 300])
+def test_split_k_with_empty_trailing_splits(cct, dev, split_k):
+    """Requested split counts the kernel trims (no empty split) reduce over exactly the
+    slices that were written: regression for a stale slice summed into the result."""
+    from paper_1504_04343_b200 import conv
+    g = torch.Generator(device=dev).manual_seed(split_k)
+    a = torch.rand((96, 6050 * 16), generator=g, device=dev) * 2 - 1
+    b = torch.rand((6050 * 16, 40), generator=g, device=dev) * 2 - 1
+    ws = conv.Workspace(dev)
+    ws.get(512 << 20).fill_(255)  # stale garbage (NaN bytes) in the scratch
+    c = conv.multiply(a, b, split_k=split_k, ws=ws)
+    ref = a.double() @ b.double()
+    assert float(torch.linalg.norm(c.double() - ref) / torch.linalg.norm(ref)) <= TOL
