@@ -306,6 +306,10 @@ __global__ void col2im_kernel(const float* __restrict__ dd, int64_t ld, float* _
 // copies, zero-padded to the padded width; each lowered row (q, r, c) is then
 // written as float4s by one warp through an offset table.  All index tables
 // are built once per CTA, so the per-row loops do no integer division.
+// NT > 0: the lane's NT column offsets (e = lane + 32 t, ld <= 32 NT) are kept in
+// registers for the whole kernel instead of re-read from smem per element (ncu: the
+// per-element table read made the kernel issue-bound at 78 % issue activity).
+template <int NT>
 __global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restrict__ dh, Geo g, RowMap rm,
                                      int64_t ld, int cols) {
     extern __shared__ float sm[];
@@ -326,6 +330,15 @@ __global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restr
     const int ld4 = int(ld / 4);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
     const int64_t nqr = g.b * m;
+    int oreg[NT > 0 ? NT : 1];
+    if constexpr (NT > 0) {
+        __syncthreads();  // offs table built
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const int e = lane + 32 * t;
+            oreg[t] = e < cols ? offs[e] : -1;
+        }
+    }
     for (int64_t qr = blockIdx.x; qr < nqr; qr += gridDim.x) {
         const int r = int(qr % m);
         const int64_t q = qr / m;
@@ -342,11 +355,23 @@ __global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restr
         __syncthreads();
         // one warp per lowered row; lane-consecutive elements: conflict-free smem
         // gathers and 128-byte coalesced stores
-        for (int c = warp; c < m; c += nwarps) {
-            const int base = s * c * d;
-            float* row = dh + (q * rm.rpi + int64_t(r) * rm.sr + int64_t(c) * rm.sc) * ld;
+        if constexpr (NT > 0) {
+            for (int c = warp; c < m; c += nwarps) {
+                const int base = s * c * d;
+                float* row = dh + (q * rm.rpi + int64_t(r) * rm.sr + int64_t(c) * rm.sc) * ld;
+#pragma unroll
+                for (int t = 0; t < NT; ++t) {
+                    const int e = lane + 32 * t;
+                    if (e < ld4 * 4) row[e] = oreg[t] >= 0 ? tile[oreg[t] + base] : 0.f;
+                }
+            }
+        } else {
+            for (int c = warp; c < m; c += nwarps) {
+                const int base = s * c * d;
+                float* row = dh + (q * rm.rpi + int64_t(r) * rm.sr + int64_t(c) * rm.sc) * ld;
 #pragma unroll 4
-            for (int e = lane; e < ld4 * 4; e += 32) row[e] = e < cols ? tile[offs[e] + base] : 0.f;
+                for (int e = lane; e < ld4 * 4; e += 32) row[e] = e < cols ? tile[offs[e] + base] : 0.f;
+            }
         }
     }
 }
@@ -529,10 +554,18 @@ cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, floa
     const size_t smem1 = size_t(g.k * (g.n + 2 * g.p) * g.d) * 4 + size_t(cols) * 4 + size_t((g.n + 2 * g.p) * g.d) * 4;
     if (type == 1 && !vec && ld % 4 == 0 && reinterpret_cast<uintptr_t>(dhat) % 16 == 0 && smem1 <= 96 * 1024 &&
         rm.ny == g.m && rm.nc == g.m) {
-        cudaFuncSetAttribute(lower_t1_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);  // per device
         const int64_t nqr = g.b * g.m;
         const int grid1 = int(std::min<int64_t>(nqr, int64_t(num_sms()) * 4));
-        lower_t1_smem_kernel<<<grid1, 512, smem1, st>>>(x, dhat, g, rm, ld, int(cols));
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);  // per device
+            kern<<<grid1, 512, smem1, st>>>(x, dhat, g, rm, ld, int(cols));
+        };
+        const int64_t nt = cdiv(ld, 32);
+        if (nt <= 4) go(lower_t1_smem_kernel<4>);
+        else if (nt <= 8) go(lower_t1_smem_kernel<8>);
+        else if (nt <= 12) go(lower_t1_smem_kernel<12>);
+        else if (nt <= 16) go(lower_t1_smem_kernel<16>);
+        else go(lower_t1_smem_kernel<0>);
         note_launch();
         return cudaGetLastError();
     }
