@@ -197,16 +197,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     // A_TM == 2: one accumulator per tile, the freed TMEM columns deepen the A ring
     constexpr int NACC = CH2 ? 2 : (A_TM == 2) ? 1 : C_::NACC;
     static_assert(!CH2 || (!A_TM && BN > 128), "CH2 config");
-    constexpr uint32_t A_COL = uint32_t(2 * NACC * BN);               // first A column
+    // single-buffered accumulator: CH2 (two chains), the 384-wide tile (256 + 128 columns), and
+    // a 256-wide tile with A in TMEM (the A ring takes the second accumulator's columns)
+    constexpr bool SB = CH2 || BN > 256 || (A_TM && BN == 256);
+    constexpr uint32_t A_COL = uint32_t((SB ? 1 : 2) * NACC * BN);    // first A column
     constexpr int kASlotsFit = int((512u - A_COL) / (2 * kBK));
     constexpr int kASlots = A_TM ? (kASlotsFit < 12 ? (kASlotsFit < STAGES - 1 ? kASlotsFit : STAGES - 1)
                                                     : (12 < STAGES - 1 ? 12 : STAGES - 1))
                                  : 4;                                 // TMEM ring of A tiles
-    // single-buffered accumulator: CH2 (two chains) and the 384-wide tile (256 + 128 columns)
-    constexpr bool SB = CH2 || BN > 256;
-    static_assert(BN <= 256 || (BN == 384 && !A_TM && !CH2 && !TRO && A_IM <= 1), "BN 384 config");
+    static_assert(BN <= 256 || (BN == 384 && !CH2 && !TRO && A_IM <= 1), "BN 384 config");
     constexpr uint32_t TMEM_COLS = A_TM ? 512u : SB ? 512u : C_::TMEM_COLS;
-    static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots && kASlots >= 4),
+    static_assert(!A_TM || (A_COL + kASlots * 2 * kBK <= 512 && !A_MN && STAGES > kASlots && kASlots >= 2),
                   "A_TM config");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // align inside the shared window without leaving the shared address space
@@ -437,6 +438,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (CG == 1) ptx::mma_tf32_ts(d, a, b, idesc, accumulate);
                     else ptx::mma_tf32_ts_cg2(d, a, b, idesc, accumulate);
                 };
+                auto mma2_ts = [&](uint32_t d, uint32_t a, uint64_t b, uint32_t accumulate) {
+                    if constexpr (CG == 1) ptx::mma_tf32_ts(d, a, b, idesc2, accumulate);
+                    else ptx::mma_tf32_ts_cg2(d, a, b, idesc2, accumulate);
+                };
                 for (int kb = kb0; kb < kb1; ++kb, ++gi) {
                     // tdone implies the raw tiles of every CTA in the group landed
                     // (each transform warp waited on its own CTA's full barrier)
@@ -451,6 +456,26 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const uint32_t a_big = tmem_base + A_COL + (gi % kASlots) * (2 * kBK);
                         const uint32_t a_small = a_big + kBK;
                         const uint32_t first = (kb > kb0) ? 1u : 0u;
+                        if constexpr (BN == 384) {
+                            // composite tile: N = 256 into [0, 256), N = 128 into [256, 384), same A
+                            constexpr uint32_t SUB2 = uint32_t(256 / CG) * kBK * 4;
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk) {
+                                const uint32_t f = kk ? 1u : first;
+                                mma_ts(d_tmem, a_small + kk * 8, tile_desc<B_MN>(b_raw, kk), f);
+                                mma2_ts(d_tmem + 256, a_small + kk * 8, tile_desc<B_MN>(b_raw + SUB2, kk), f);
+                            }
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk) {
+                                mma_ts(d_tmem, a_big + kk * 8, tile_desc<B_MN>(b_sml, kk), 1u);
+                                mma2_ts(d_tmem + 256, a_big + kk * 8, tile_desc<B_MN>(b_sml + SUB2, kk), 1u);
+                            }
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk) {
+                                mma_ts(d_tmem, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
+                                mma2_ts(d_tmem + 256, a_big + kk * 8, tile_desc<B_MN>(b_raw + SUB2, kk), 1u);
+                            }
+                        } else {
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk)
                             mma_ts(d_tmem + kk * (NACC - 1) * BN, a_small + kk * 8, tile_desc<B_MN>(b_raw, kk),
@@ -461,6 +486,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk)
                             mma_ts(d_tmem + kk * (NACC - 1) * BN, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
+                        }
                     } else if constexpr (BN == 384) {
                         // this CTA's B rows: 256/CG of the first sub-tile, then 128/CG of the second
                         // (K-major: 256/CG rows of 64 B; MN-major: (256/CG)/32 chunks of 2 KB -- same bytes)
@@ -898,6 +924,18 @@ cudaError_t launch(const CUtensorMap& ta, const CUtensorMap& tb, const KParams& 
     return cudaGetLastError();
 }
 
+// $CCT_A_TMEM_WIDE (default 1): 192 / 256 / 384-wide CTA-pair tiles with a K-major A keep A
+// in TMEM too (the 3xTF32 MMAs then read only B from smem): +12 % on a 192-wide microbenchmark,
+// 1-4 % on the CaffeNet forward / backward-data GEMMs (the 256 / 384 tiles give up the second
+// accumulator buffer for the A ring)
+int a_tmem_wide() {
+    static const int v = [] {
+        const char* e = getenv("CCT_A_TMEM_WIDE");
+        return e ? atoi(e) : 1;
+    }();
+    return v;
+}
+
 // $CCT_A_TMEM: 0 keeps narrow tiles on the smem-A path, 1 A in TMEM with two
 // sub-accumulators, 2 A in TMEM with one accumulator and a deeper A ring (A/B)
 int a_in_tmem_mode() {
@@ -945,6 +983,14 @@ cudaError_t dispatch_std(const GemmProblem& g, const CUtensorMap& ta, const CUte
         }
         return cudaErrorInvalidValue;
     }
+    if constexpr (BN == 192 || BN == 256) {  // A in TMEM for wide tiles (K-major A): fewer smem reads
+        if (CG == 2 && a_tmem_wide() && !amn && g.passes == 3 && !g.chain2 && !g.C.transposed) {
+            if (g.im2col.x && g.im2col.operand == 1) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 2, 1>(ta, tb, kp, st);
+            if (g.im2col.x && g.im2col.operand == 0) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 1>(ta, tb, kp, st);
+            if (!g.im2col.x)
+                return bmn ? launch<BN, 0, 1, CG, 0, 1>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 1>(ta, tb, kp, st);
+        }
+    }
     if constexpr (BN <= 96) {
         const int atm = g.im2col.operand >= 1 ? 0 : a_in_tmem_mode();
         if (!amn && g.passes == 3 && atm == 2) {
@@ -983,6 +1029,10 @@ cudaError_t dispatch_layout(const GemmProblem& g, const CUtensorMap& ta, const C
         const bool amn = g.A.major == Major::MN, bmn = g.B.major == Major::MN;
         if (g.chain2 || g.C.transposed || g.passes != 3 || (g.im2col.x && g.im2col.operand != 0))
             return cudaErrorInvalidValue;
+        if (CG == 2 && a_tmem_wide() && !amn) {  // A in TMEM (CTA pairs: single CTAs have too few stages)
+            if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<384, 0, 0, CG, 1, 1>(ta, tb, kp, st);
+            return bmn ? launch<384, 0, 1, CG, 0, 1>(ta, tb, kp, st) : launch<384, 0, 0, CG, 0, 1>(ta, tb, kp, st);
+        }
         if (g.im2col.x) {
             if (!amn && !bmn) return launch<384, 0, 0, CG, 1>(ta, tb, kp, st);     // forward
             if (amn && bmn) return launch<384, 1, 1, CG, 1>(ta, tb, kp, st);       // backward-weight, dy NHWC
