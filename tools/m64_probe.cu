@@ -13,7 +13,7 @@ __device__ __forceinline__ uint32_t sw64(int r, int k) {  // K-major SWIZZLE_64B
     return uint32_t(r * 64 + ((c ^ ((r >> 1) & 3)) << 4) + (k & 3) * 4);
 }
 
-__global__ void probe(float* out, long long* cyc, int M, int N, int reps) {
+__global__ void probe(float* out, long long* cyc, int M, int N, int reps, int alt = 1) {
     __shared__ __align__(1024) uint8_t a_s[128 * 64];
     __shared__ __align__(1024) uint8_t b_s[256 * 64];
     __shared__ __align__(8) uint64_t bar;
@@ -57,7 +57,7 @@ __global__ void probe(float* out, long long* cyc, int M, int N, int reps) {
     ptx::tc_fence_after();
     if (tid == 0) {
         const long long t0 = clock64();
-        for (int i = 0; i < reps; ++i) ptx::mma_tf32(tmem + 256 * (i & 1), ad, bd, idesc, 1u);
+        for (int i = 0; i < reps; ++i) ptx::mma_tf32(tmem + (alt ? 256 * (i & 1) : 0), ad, bd, idesc, 1u);
         ptx::mma_commit(&bar);
         ptx::mbar_wait(&bar, 1);
         cyc[0] = clock64() - t0;
@@ -92,6 +92,15 @@ int main() {
             long long c = 0;
             cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
             printf("M=%3d N=%3d: %.1f cycles per MMA\n", M, N, double(c) / 2000.0);
+        }
+    }
+    for (int N : {128, 256}) {
+        for (int alt : {0, 1}) {
+            probe<<<1, 128>>>(out, cyc, 128, N, 2000, alt);
+            cudaDeviceSynchronize();
+            long long c = 0;
+            cudaMemcpy(&c, cyc, 8, cudaMemcpyDeviceToHost);
+            printf("M=128 N=%3d %s accumulator: %.1f cycles per MMA\n", N, alt ? "alternating" : "same", double(c) / 2000.0);
         }
     }
     return 0;
