@@ -376,6 +376,79 @@ __global__ void lower_t1_smem_kernel(const float* __restrict__ x, float* __restr
     }
 }
 
+// The same lowering for unpadded layers with 16-byte aligned x and a whole number
+// of float4s in x (conv1): the k input rows are staged with 16-byte cp.async from
+// the float4 boundary below each row start (the row's misalignment sh_i, 0..3
+// floats, is folded into the per-lane smem offsets once per tile), lowered
+// columns past `cols` read a zeroed smem slot instead of taking a branch, and the
+// gathers use 32-bit shared addresses.  Each thread keeps its NT = ld / 32
+// (rounded up) smem offsets in registers, with i * n d mod 4 for filter row i in
+// bits 28..29 (row i starts sh_0 + i n d floats past a float4 boundary).  The zero
+// slot tolerates the shift (rowfS >= n d + 4 > the largest column offset + 3).
+template <int NT>
+__global__ void __launch_bounds__(512) lower_t1_vec_kernel(const float* __restrict__ x, float* __restrict__ dh, Geo g,
+                                                             RowMap rm, int64_t ld, int cols) {
+    extern __shared__ __align__(16) float sm[];
+    const int n = int(g.n), d = int(g.d), k = int(g.k), s = int(g.s), m = int(g.m);
+    const int rowf = n * d;                     // floats per input row
+    const int rowfS = (rowf + 7) & ~3;          // slot: up to 3 leading floats + the row, float4 multiple
+    const int nvmax = rowfS / 4;
+    float* zero = sm + k * rowfS;               // slot k: zeros (padding columns read here)
+    const uint32_t sbase = ptx::smem_u32(sm);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
+    for (int e = threadIdx.x; e < rowfS; e += blockDim.x) zero[e] = 0.f;
+    const int kd = k * d, nd4 = rowf & 3;
+    uint32_t oreg[NT];
+#pragma unroll
+    for (int t = 0; t < NT; ++t) {
+        const int e = lane + 32 * t;
+        if (e < cols) {
+            const int i = e / kd, rr = e - i * kd;
+            oreg[t] = uint32_t(i * rowfS + rr) | (uint32_t((i * nd4) & 3) << 28);
+        } else {
+            oreg[t] = uint32_t(k * rowfS);  // zero slot (no shift)
+        }
+    }
+    const int last = int(ld) - 32 * (NT - 1);   // lanes of the final 32-column group that store
+    const int64_t nqr = g.b * m;
+    for (int64_t qr = blockIdx.x; qr < nqr; qr += gridDim.x) {
+        const int r = int(qr % m);
+        const int64_t q = qr / m;
+        const int64_t g00 = ((q * n + int64_t(s) * r) * n) * d;   // float index of input row s r
+        const int sh0 = int(g00 & 3);
+        __syncthreads();  // previous tile consumed (and the zero slot written)
+        for (int idx = threadIdx.x; idx < k * nvmax; idx += blockDim.x) {
+            const int i = idx / nvmax, v = idx - i * nvmax;
+            const int64_t gi = g00 + int64_t(i) * rowf;
+            const int sh = int(gi & 3);
+            if (4 * v < sh + rowf) cp_async16(sm + i * rowfS + 4 * v, x + (gi - sh) + 4 * v);
+        }
+        cp_async_wait_all();
+        __syncthreads();
+        uint32_t addr[NT];
+#pragma unroll
+        for (int t = 0; t < NT; ++t) {
+            const uint32_t o = oreg[t];
+            addr[t] = sbase + 4u * ((o & 0x0fffffffu) + uint32_t((sh0 + int(o >> 28)) & 3));
+        }
+        for (int c = warp; c < m; c += nwarps) {
+            const uint32_t boff = 4u * uint32_t(s * c * d);
+            float* row = dh + (q * rm.rpi + int64_t(r) * rm.sr + int64_t(c) * rm.sc) * ld + lane;
+#pragma unroll
+            for (int t = 0; t < NT - 1; ++t) {
+                float v;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr[t] + boff));
+                row[32 * t] = v;
+            }
+            if (lane < last) {
+                float v;
+                asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr[NT - 1] + boff));
+                row[32 * (NT - 1)] = v;
+            }
+        }
+    }
+}
+
 // col2im (Type 1, small d): one CTA per input row (q, y).  dDhat arrives
 // slab-major (col2im_slab_layout): slab (q, r, i) = the m x k*d block of rows
 // (q, r, c) and filter row i, contiguous and 16-byte aligned (stride S floats),
@@ -435,8 +508,11 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t S, f
                            &full[buf]);
         }
     };
-    uint32_t phase[2] = {0, 0};
+    uint32_t phase = 0;  // bit b: parity of buffer b
     if (threadIdx.x == 0 && blockIdx.x < nqy) issue(blockIdx.x, 0);
+    const uint32_t sbase = ptx::smem_u32(sm);
+    const uint32_t slab4 = uint32_t(S) * 4u;
+    const uint32_t delta4 = uint32_t(s * d - kd) * 4u;  // slab step from tap t to t + 1 (bytes)
     int it = 0;
     for (int64_t qy = blockIdx.x; qy < nqy; qy += gridDim.x, ++it) {
         const int buf = it & 1;
@@ -445,29 +521,38 @@ __global__ void col2im_t1_smem_kernel(const float* __restrict__ dd, int64_t S, f
         int rtop;
         const int np = pairs(qy, &rtop);
         if (np > 0) {
-            ptx::mbar_wait(&full[buf], phase[buf]);
-            phase[buf] ^= 1;
+            ptx::mbar_wait(&full[buf], (phase >> buf) & 1u);
+            phase ^= 1u << buf;
         }
-        const float* slabs = sm + buf * npair_max * S;
+        const uint32_t slabs = sbase + uint32_t(buf * npair_max) * slab4;
         float* out = dx + qy * int64_t(n) * d;
-        const int delta = s * d - kd;  // slab step from tap t to t + 1
         for (int e = threadIdx.x; e < n * d; e += blockDim.x) {
             const int mt = meta[e];
-            const int off = mt & 0xFFFFFF, cnt = mt >> 24;
+            const int cnt = mt >> 24;
+            const uint32_t a0 = slabs + 4u * uint32_t(mt & 0xFFFFFF);
             float acc = 0.f;
             if constexpr (NP > 0) {
 #pragma unroll
                 for (int a = 0; a < NP; ++a) {
-                    const float* sl = slabs + a * S + off;
+                    if (a < np) {  // block-uniform
 #pragma unroll
-                    for (int t = 0; t < NP; ++t)
-                        if (a < np && t < cnt) acc += sl[t * delta];
+                        for (int t = 0; t < NP; ++t) {
+                            float v = 0.f;  // +0 terms leave the sum bit-identical (it is never -0)
+                            asm volatile(
+                                "{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %2, %3;\n\t@p ld.shared.f32 %0, [%1];\n\t}"
+                                : "+f"(v)
+                                : "r"(a0 + uint32_t(a) * slab4 + uint32_t(t) * delta4), "r"(t), "r"(cnt));
+                            acc += v;
+                        }
+                    }
                 }
             } else {
-                for (int a = 0; a < np; ++a) {
-                    const float* sl = slabs + a * S + off;
-                    for (int t = 0; t < cnt; ++t) acc += sl[t * delta];
-                }
+                for (int a = 0; a < np; ++a)
+                    for (int t = 0; t < cnt; ++t) {
+                        float v;
+                        asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a0 + uint32_t(a) * slab4 + uint32_t(t) * delta4));
+                        acc += v;
+                    }
             }
             out[e] = acc;
         }
@@ -543,6 +628,15 @@ __global__ void __launch_bounds__(256) transpose_batched_kernel(const float* __r
 
 }  // namespace
 
+// $CCT_LOWER_VEC=0 keeps the scalar-staged small-channel lowering (A/B runs)
+static bool lower_vec_enabled() {
+    static const bool on = [] {
+        const char* e = getenv("CCT_LOWER_VEC");
+        return !(e && atoi(e) == 0);
+    }();
+    return on;
+}
+
 cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, float* dhat, int64_t ld,
                   cudaStream_t st) {
     const int64_t cols = lowered_cols(g, type);
@@ -561,6 +655,23 @@ cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, floa
             kern<<<grid1, 512, smem1, st>>>(x, dhat, g, rm, ld, int(cols));
         };
         const int64_t nt = cdiv(ld, 32);
+        const size_t smemv = size_t((g.k + 1) * ((g.n * g.d + 7) & ~int64_t(3))) * 4;
+        const int64_t total = g.b * g.n * g.n * g.d;
+        if (g.p == 0 && total % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && nt >= 2 && nt <= 16 &&
+            smemv <= 96 * 1024 && lower_vec_enabled()) {
+            auto gov = [&](auto kern) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);  // per device
+                kern<<<grid1, 512, smemv, st>>>(x, dhat, g, rm, ld, int(cols));
+            };
+            switch (nt) {
+#define CCT_LV(N) case N: gov(lower_t1_vec_kernel<N>); break;
+                CCT_LV(2) CCT_LV(3) CCT_LV(4) CCT_LV(5) CCT_LV(6) CCT_LV(7) CCT_LV(8) CCT_LV(9)
+                CCT_LV(10) CCT_LV(11) CCT_LV(12) CCT_LV(13) CCT_LV(14) CCT_LV(15) CCT_LV(16)
+#undef CCT_LV
+            }
+            note_launch();
+            return cudaGetLastError();
+        }
         if (nt <= 4) go(lower_t1_smem_kernel<4>);
         else if (nt <= 8) go(lower_t1_smem_kernel<8>);
         else if (nt <= 12) go(lower_t1_smem_kernel<12>);
