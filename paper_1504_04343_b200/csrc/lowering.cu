@@ -661,7 +661,12 @@ cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, floa
             smemv <= 96 * 1024 && lower_vec_enabled()) {
             auto gov = [&](auto kern) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);  // per device
-                kern<<<grid1, 512, smemv, st>>>(x, dhat, g, rm, ld, int(cols));
+                int threads = 512;
+                if (const char* e = getenv("CCT_LOWER_THREADS")) threads = atoi(e);
+                int per_sm = 0;
+                cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smemv);
+                const int gridv = int(std::min<int64_t>(nqr, int64_t(num_sms()) * std::max(1, per_sm)));
+                kern<<<gridv, threads, smemv, st>>>(x, dhat, g, rm, ld, int(cols));
             };
             switch (nt) {
 #define CCT_LV(N) case N: gov(lower_t1_vec_kernel<N>); break;
@@ -734,9 +739,17 @@ cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* d
         cudaFuncSetAttribute(col2im_t1_smem_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         cudaFuncSetAttribute(col2im_t1_smem_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         const size_t smem1 = size_t(2 * ((g.k + g.s - 1) / g.s) * ld + g.n * g.d) * 4;
-        const int grid1 = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * 4));
-        if ((g.k + g.s - 1) / g.s <= 3) col2im_t1_smem_kernel<3><<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
-        else col2im_t1_smem_kernel<0><<<grid1, 512, smem1, st>>>(dd, ld, dx, g);
+        // threads: the fewest warps that cover a dx row in the same number of passes
+        // as 256 threads would (conv1: 681 floats -> 3 x 256).  Measured on conv1
+        // b = 256 (ncu): 512 threads 376 us, 352 261 us, 256 219 us (5.8 TB/s), 224 225 us.
+        const int64_t nd = g.n * g.d, passes = cdiv(nd, 256);
+        int threads = int(std::min<int64_t>(256, (cdiv(nd, passes) + 31) / 32 * 32));
+        if (const char* e = getenv("CCT_COL2IM_THREADS")) threads = atoi(e);
+        auto kern = (g.k + g.s - 1) / g.s <= 3 ? col2im_t1_smem_kernel<3> : col2im_t1_smem_kernel<0>;
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem1);
+        const int grid1 = int(std::min<int64_t>(rowsq, int64_t(num_sms()) * std::max(1, per_sm)));
+        kern<<<grid1, threads, smem1, st>>>(dd, ld, dx, g);
         note_launch();
         return cudaGetLastError();
     }
