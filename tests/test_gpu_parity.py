@@ -119,6 +119,26 @@ def test_lower_internal_bit_exact(cct, dev, orc, t, geom):
     assert np.array_equal(dh, orc.lower_internal(t, x, b, n, d, k, s, p))
 
 
+@pytest.mark.parametrize("geom", [(23, 11, 3, 4, 4), (19, 5, 3, 2, 4), (21, 7, 3, 1, 8), (227, 11, 3, 4, 4)],
+                         ids=["s4", "s2", "s1", "conv1"])
+def test_lower_small_channel_float4_staging_bit_exact(cct, dev, orc, geom):
+    """Unpadded small-channel Type 1 with b n^2 d % 4 == 0 takes lower_t1_vec_kernel (rows staged
+    from the float4 boundary below each row start: every misalignment 0..3 occurs, since n d is
+    odd here) -- bit-exact against the oracle in both row orders."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, s, b = geom
+    assert (b * n * n * d) % 4 == 0 and (n * d) % 2 == 1
+    x = orc.uniform(43, b * n * n * d)
+    desc = cct.ConvDesc(n, k, d, 5, b, s, 0)
+    dh = conv.lower(T(x, dev, b, n, n, d), desc, 1, cct.ROWS_INTERNAL).cpu().numpy()
+    assert np.array_equal(dh, orc.lower_internal(1, x, b, n, d, k, s, 0))
+    if s == 1:
+        xs, w = orc.random_problem(47, b, n, d, k, 4)
+        dh_ref, _ = orc.lower(1, xs, w, b, n, d, k, 4)
+        dh = conv.lower(T(xs, dev, b, n, n, d), cct.ConvDesc(n, k, d, 4, b), 1, cct.ROWS_SPEC).cpu().numpy()
+        assert np.array_equal(dh, dh_ref)
+
+
 # --------------------------------------------------------- full conv passes
 @pytest.mark.parametrize("t", [1, 2, 3])
 @pytest.mark.parametrize("path", CONV_CASES, ids=[os.path.basename(p)[:-4] for p in CONV_CASES])
