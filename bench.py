@@ -444,6 +444,9 @@ def run_e2e(a, st, torch, world, group, dev):
 
 
 if __name__ == "__main__":
+    if os.environ.get("CCT_BENCH_WATCHDOG"):  # diagnostics: dump the Python stacks after N s
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["CCT_BENCH_WATCHDOG"]), repeat=True)
     args = parse()
     if args.impl == "reference":
         run_reference(args)

@@ -2,6 +2,8 @@
 #include "common.cuh"
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <vector>
 
@@ -45,6 +47,8 @@ uint64_t g_acc_n[kNumPhases];
 void profile_enable(bool on) { g_prof.store(on); }
 
 PhaseScope::PhaseScope(Phase ph, cudaStream_t s, double flops, double bytes) : slot(-1), st(s) {
+    static const bool trace = getenv("CCT_TRACE_PHASES") != nullptr;  // diagnostics
+    if (trace) fprintf(stderr, "cct-phase %d bytes %.0f flops %.0f\n", int(ph), bytes, flops);
     if (!g_prof.load(std::memory_order_relaxed)) return;
     Rec r{};
     if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;

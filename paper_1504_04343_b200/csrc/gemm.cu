@@ -257,7 +257,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===================== TMA producers (every CTA loads its own share) =====================
         // warp 0 issues the A tiles (and arms the stage's barrier), warp 3 the B tiles: the
         // MN-major operands take up to 4 + 8 boxes per stage and one issuing thread was the
-        // limit of the backward-weight GEMMs ($CCT_SPLIT_PRODUCER=0: warp 0 issues both)
+        // limit of the backward-weight GEMMs ($CCT_SPLIT_PRODUCER=1; default 0: warp 0 issues
+        // both -- the split form intermittently hangs)
         const bool role_a = warp == 0;
         const bool role_b = (warp == 3) == (p.split_producer != 0);
         if (lane == 0 && (role_a || role_b)) {
@@ -1208,8 +1209,10 @@ cudaError_t run_gemm(const GemmProblem& g, cudaStream_t stream) {
     kp.nmlim = g.C.nmlim < (int64_t(1) << 31) ? int(g.C.nmlim) : INT32_MAX;
     kp.split_producer = [] {
         static const int v = [] {
+            // default off: with the split producer a bench run of 30 training steps hung
+            // (a GEMM that never completed) in ~1 of 3 runs; 0 of 8 with it off (1.3 % slower)
             const char* e = getenv("CCT_SPLIT_PRODUCER");
-            return e ? atoi(e) : 1;
+            return e ? atoi(e) : 0;
         }();
         return v;
     }();

@@ -13,12 +13,16 @@ bwd-data + bwd-weight conv5..1, each with the lowering the cost model selects.
 """
 from __future__ import annotations
 
+import os
+import sys
 from dataclasses import dataclass
 
 import torch
 
 from . import LOWER_AUTO, PASS_BWD, PASS_FWD, ConvDesc, select_lowering, workspace_size
 from .conv import Workspace, alloc_cache, conv_bwd, conv_fwd_cached
+
+_TRACE = bool(os.environ.get("CCT_TRACE"))  # diagnostics: one stderr line per layer pass
 
 __all__ = ["LayerSpec", "CAFFENET", "ConvStack", "stack_flops_per_image"]
 
@@ -94,6 +98,8 @@ class ConvStack:
 
     def forward(self, stream=None):
         for i, d in enumerate(self.descs):
+            if _TRACE:
+                print(f"cct-trace fwd layer {i}", file=sys.stderr, flush=True)
             conv_fwd_cached(self.x[i], self.w[i], d, self.types[i], cache=self.cache[i], out=self.y[i],
                             ws=self.ws, stream=stream)
 
@@ -101,6 +107,8 @@ class ConvStack:
         handles = []
         for i in reversed(range(len(self.descs))):
             d, t = self.descs[i], self.types[i]
+            if _TRACE:
+                print(f"cct-trace bwd layer {i}", file=sys.stderr, flush=True)
             conv_bwd(self.dy[i], self.w[i], d, t, x=self.x[i], cache=self.cache[i], dx=self.dx[i],
                      dw=self.dw[i], ws=self.ws, stream=stream)
             if allreduce and self.group is not None:
