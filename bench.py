@@ -13,12 +13,17 @@ exceeds the 126 MB L2, so no flush is needed between steps.
 
 value  = images/s over all ranks, inputs resident in HBM, CUDA-event timed on
          the compute stream, max over ranks.
-e2e    = the same step through the C ABI fed from pinned HOST buffers: per step
-         H2D of every layer's x and dy, D2H of every layer's dW (the result).
+e2e    = the same step through the C ABI fed from and returned to pinned HOST
+         buffers: per step H2D of every layer's x and dy, D2H of every layer's
+         y, dx and dW (the results the reference API returns on the host).
+configs = device-timed configs[0] (conv2 b=256 T1), configs[2] (conv1 b=256) and
+         the configs[1] ratio sweep, plus configs[0] on the reference CPU path.
+--global-batch G = strong scaling (configs[4]: 2048 split over the ranks).
 roofline = the dominant kernel (the tcgen05 3xTF32 GEMM), timed live with CUDA
          events around every GEMM launch inside the timed region.
 cpu_baseline = the reference's own CPU path (oracle/_ref: its multiply,
-         gemm.cpp:93, around the restated lowering) on a bounded sample, rank 0, N = 1.
+         gemm.cpp:93, around the restated lowering) on a bounded sample (32 images of
+         the stack), rank 0, N = 1.
 """
 from __future__ import annotations
 
@@ -36,6 +41,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "conv fwd+bwd images/s and TFLOPS vs B200 peak at 1/2/4/8 GPUs vs CPU ref"
+WORKLOAD = "caffenet conv1-5 fwd+bwd_data+bwd_weight, auto lowering per layer"
 UNIT = "images/s"
 PHASES = ["lower", "gemm", "lift", "expand", "col2im", "reduce", "other"]
 
@@ -51,6 +57,10 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="images in the CPU sample (0 = auto)")
+    ap.add_argument("--global-batch", type=int, default=0,
+                    help="strong scaling (configs[4]): split this many images over the ranks "
+                         "(0 = weak scaling, --batch images per GPU)")
+    ap.add_argument("--no-configs", action="store_true", help="skip the configs[0..2] device / CPU lines")
     return ap.parse_args()
 
 
@@ -114,68 +124,104 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------------------
-# reference CPU path (oracle/_ref), used by --impl reference and cpu_baseline
+# reference CPU path (oracle/_ref), used by --impl reference and cpu_baseline.
+# This half of the file never imports the package or loads libcct.so: the
+# reference arm is the reference's own code only.
 # ---------------------------------------------------------------------------
-def cpu_reference_stack(images: int, types, threads: int):
-    """Time the reference CPU path on `images` images of the conv1-5 stack.
-    Returns (seconds, images, kind, threads)."""
-    import numpy as np
+# (name, n, k, d, o, stride, pad) -- BASELINE.json configs: conv1 227x227x3 -> 96 k11 s4;
+# conv2 27x27x96 -> 256 k5 p2; conv3-5 13x13, k3, p1 (= stack.CAFFENET, tests/test_bench_contract.py)
+CAFFENET_GEOM = (("conv1", 227, 11, 3, 96, 4, 0), ("conv2", 27, 5, 96, 256, 1, 2),
+                 ("conv3", 13, 3, 256, 384, 1, 1), ("conv4", 13, 3, 384, 384, 1, 1),
+                 ("conv5", 13, 3, 384, 256, 1, 1))
+# the lowering the B200 arm's cost model picks for the stack at b = 256 (checked against
+# cct_select_lowering by tests/test_bench_contract.py), so both arms run the same types
+REF_TYPES = (1, 1, 1, 1, 1)
+STACK_GFLOP_PER_IMAGE = 6.4598  # 3 passes x sum 2 m^2 k^2 d o
+CPU_STACK_SAMPLE = 32           # images per CPU step (b = 32 for the stack)
+
+
+def _reference_impl():
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     from oracle_py import REF_SO, Oracle, Reference  # noqa: E402
-    from paper_1504_04343_b200.stack import CAFFENET
-    kind = "reference" if os.path.exists(REF_SO) else "port"
-    impl = Reference() if kind == "reference" else Oracle()
-    orc = Oracle()
-    rng = np.random.default_rng(7)
-    t = 0.0
-    for li, l in enumerate(CAFFENET):
-        m = (l.n + 2 * l.pad - l.k) // l.stride + 1
-        x = rng.uniform(-1, 1, images * l.n * l.n * l.d).astype(np.float32)
-        w = rng.uniform(-1, 1, l.o * l.k * l.k * l.d).astype(np.float32)
-        dy = rng.uniform(-1, 1, images * l.o * m * m).astype(np.float32)
-        args = (images, l.n, l.d, l.k, l.o, l.stride, l.pad)
-        tp = types[li]
-        t0 = time.perf_counter()
-        if kind == "reference":
-            impl.lowered("fwd", tp, x, w, *args, threads=threads)
-            impl.lowered("bwd_data", tp, dy, w, *args, threads=threads)
-            impl.lowered("bwd_weight", tp, x, dy, *args, threads=threads)
-        else:
-            orc.lowered("fwd", tp, x, w, *args)
-            orc.lowered("bwd_data", tp, dy, w, *args)
-            orc.lowered("bwd_weight", tp, x, dy, *args)
-        t += time.perf_counter() - t0
+    if os.path.exists(REF_SO):
+        return Reference(), "reference"
+    return Oracle(), "port"
+
+
+def cpu_reference_layer(impl, kind, geom, images, tp, threads, seed=7):
+    """One layer's fwd + bwd-data + bwd-weight on the reference CPU path; seconds."""
+    import numpy as np
+    _, n, k, d, o, s, p = geom
+    m = (n + 2 * p - k) // s + 1
+    rng = np.random.default_rng(seed)
+    x = rng.uniform(-1, 1, images * n * n * d).astype(np.float32)
+    w = rng.uniform(-1, 1, o * k * k * d).astype(np.float32)
+    dy = rng.uniform(-1, 1, images * o * m * m).astype(np.float32)
+    args = (images, n, d, k, o, s, p)
+    kw = {"threads": threads} if kind == "reference" else {}
+    t0 = time.perf_counter()
+    impl.lowered("fwd", tp, x, w, *args, **kw)
+    impl.lowered("bwd_data", tp, dy, w, *args, **kw)
+    impl.lowered("bwd_weight", tp, x, dy, *args, **kw)
+    return time.perf_counter() - t0
+
+
+def cpu_reference_stack(images: int, types, threads: int):
+    """Time the reference CPU path (its multiply, gemm.cpp:93-122, threaded, around the
+    restated lowering / lifting) on `images` images of the conv1-5 stack.
+    Returns (seconds, images, kind, threads)."""
+    impl, kind = _reference_impl()
+    t = sum(cpu_reference_layer(impl, kind, g, images, types[li], threads, seed=7 + li)
+            for li, g in enumerate(CAFFENET_GEOM))
     return t, images, kind, (threads if kind == "reference" else 1)
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def ref_types(a):
+    if a.lowering in ("auto", ""):
+        return list(REF_TYPES)
+    if "," in a.lowering:
+        return [int(t) for t in a.lowering.split(",")]
+    return [int(a.lowering)] * len(CAFFENET_GEOM)
 
 
 def run_reference(a):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    import paper_1504_04343_b200 as cct
-    from paper_1504_04343_b200.stack import CAFFENET
-    types = [cct.select_lowering(l.desc(a.batch), 3)[0] for l in CAFFENET]
+    types = ref_types(a)
     threads = min(os.cpu_count() or 1, 256)
-    sample = a.cpu_sample or 1
+    sample = a.cpu_sample or CPU_STACK_SAMPLE
     for _ in range(a.warmup):
         cpu_reference_stack(sample, types, threads)
-    tot, imgs = 0.0, 0
+    times = []
+    kind, thr = "port", 1
     for _ in range(a.steps):
         t, n, kind, thr = cpu_reference_stack(sample, types, threads)
-        tot += t
-        imgs += n
-    v = imgs / tot
+        times.append(t)
+    tot = sum(times)
+    v = sample * a.steps / tot
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32 (fp64 accumulate)", "data": "synthetic U(-1,1)",
-        "config": {"workload": "caffenet conv1-5 fwd+bwd_data+bwd_weight, per-layer lowering as the B200 arm",
-                   "images_per_step": sample, "lowering": types},
-        "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": kind,
-                         "sample": f"{sample} image(s) of the conv1-5 stack per step, fwd+bwd, reference "
-                                   f"multiply (gemm.cpp:93) with {thr} threads around the restated lowering"},
+        "vs_baseline": None, "dtype": "f32 (fp64 accumulate)", "data": "synthetic U(-1,1), CaffeNet conv1-5 shapes",
+        "config": {"workload": WORKLOAD, "images_per_step": sample,
+                   "lowering": {g[0]: t for g, t in zip(CAFFENET_GEOM, types)}},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": kind, "cpu_model": cpu_model(),
+                         "sample": f"{sample} images of the conv1-5 stack per step (BASELINE.md section 3), "
+                                   f"fwd+bwd_data+bwd_weight, the reference's multiply (gemm.cpp:93) with {thr} "
+                                   f"threads around the restated lowering; median step {1e3 * statistics.median(times):.0f} ms"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "tflops": v * 6.4598e9 / 1e12,
+        "tflops": v * STACK_GFLOP_PER_IMAGE / 1e3,
     }
     print(json.dumps(line), flush=True)
 
@@ -223,6 +269,72 @@ def tf32_cublas_probe(torch):
     return 2.0 * n ** 3 / (e0.elapsed_time(e1) / 5 * 1e-3) / 1e12
 
 
+def time_layer_step(torch, desc, tp, steps=5, warmup=2):
+    """Device ms of one layer's training step (fwd with the lowered cache, then bwd-data +
+    bwd-weight) through the C ABI, CUDA events on the current stream."""
+    from paper_1504_04343_b200 import PASS_BWD, PASS_FWD, workspace_size
+    from paper_1504_04343_b200.conv import Workspace, alloc_cache, conv_bwd, conv_fwd_cached
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev)
+    g.manual_seed(11)
+
+    def u(*shape):
+        return torch.rand(shape, generator=g, device=dev).mul_(2).sub_(1)
+
+    x, w = u(desc.b, desc.n, desc.n, desc.d), u(desc.o, desc.k, desc.k, desc.d)
+    dy = u(desc.b, desc.o, desc.m, desc.m)
+    y, dx, dw = torch.empty_like(dy), torch.empty_like(x), torch.empty_like(w)
+    cache = alloc_cache(desc, tp, dev)
+    ws = Workspace(dev)
+    ws.get(max(workspace_size(desc, tp, PASS_FWD), workspace_size(desc, tp, PASS_BWD)))
+
+    def one():
+        conv_fwd_cached(x, w, desc, tp, cache=cache, out=y, ws=ws)
+        conv_bwd(dy, w, desc, tp, x=x, cache=cache, dx=dx, dw=dw, ws=ws)
+
+    for _ in range(warmup):
+        one()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / steps
+
+
+def run_configs(torch, ceiling):
+    """Device-timed numbers for the other BASELINE.json configs on this GPU: configs[0]
+    (conv2, b = 256, Type 1), configs[2] (conv1, b = 256, cost-model lowering) and the
+    configs[1] ratio sweep (n = 13, k = 3, p = 1, b = 256; every type at every point)."""
+    import paper_1504_04343_b200 as cct
+    out = {}
+
+    def rec(desc, tp):
+        ms = time_layer_step(torch, desc, tp)
+        fl = 3 * desc.flops_per_pass()
+        return {"lowering": tp, "ms_per_step": ms, "images_per_s": desc.b / (ms * 1e-3),
+                "tflops": fl / (ms * 1e-3) / 1e12, "frac_of_3xtf32_ceiling": fl / (ms * 1e-3) / 1e12 / ceiling}
+
+    out["configs[0] conv2 b256 T1 fwd+bwd"] = rec(cct.ConvDesc(27, 5, 96, 256, 256, 1, 2), 1)
+    c1 = cct.ConvDesc(227, 11, 3, 96, 256, 4, 0)
+    out["configs[2] conv1 b256 auto fwd+bwd"] = rec(c1, cct.select_lowering(c1, 3)[0])
+    sweep = []
+    for d, o in ((64, 1024), (128, 512), (256, 256), (512, 128), (1024, 64),
+                 (128, 1024), (256, 512), (512, 256), (1024, 128)):
+        desc = cct.ConvDesc(13, 3, d, o, 256, 1, 1)
+        row = {"d": d, "o": o, "d_over_o": d / o, "model_choice": cct.select_lowering(desc, 3)[0]}
+        for tp in (1, 2, 3):
+            r = rec(desc, tp)
+            row[f"T{tp}_ms"] = r["ms_per_step"]
+            row[f"T{tp}_tflops"] = r["tflops"]
+        row["measured_best"] = min((1, 2, 3), key=lambda t: row[f"T{t}_ms"])
+        sweep.append(row)
+    out["configs[1] ratio sweep n13 k3 p1 b256 fwd+bwd"] = sweep
+    return out
+
+
 def run_ours(a):
     import torch
     import torch.distributed as dist
@@ -242,10 +354,14 @@ def run_ours(a):
     group = None
     if world > 1:
         if backend == "nccl":
+            # NCCL's own log (stderr) records the communicator's rank count and transport
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
         group = dist.group.WORLD
+        print(f"cct-bench rank {rank}/{world} on cuda:{local} backend {backend}", file=sys.stderr, flush=True)
     L = cct.lib()
     if a.lowering == "auto":
         lowering = cct.LOWER_AUTO
@@ -253,7 +369,9 @@ def run_ours(a):
         lowering = [int(t) for t in a.lowering.split(",")]
     else:
         lowering = int(a.lowering)
-    st = ConvStack(a.batch, dev, CAFFENET, lowering, group=group, seed=1234 + rank)
+    strong = a.global_batch > 0
+    st = ConvStack(a.batch, dev, CAFFENET, lowering, group=group, seed=1234,
+                   global_batch=a.global_batch if strong else None)
     stream = torch.cuda.current_stream()
 
     def barrier():
@@ -297,9 +415,9 @@ def run_ours(a):
     phase = {PHASES[i]: {"ms_per_step": pms[i] / a.steps, "launches_per_step": pn[i] / a.steps}
              for i in range(7) if pn[i]}
 
-    images = a.batch * world
+    images = st.global_batch
     value = images / (ms_max * 1e-3)
-    flops_step = st.flops_per_step() * world
+    flops_step = stack_flops(CAFFENET) * images
     tflops = flops_step / (ms_max * 1e-3) / 1e12
 
     # ---- e2e: host-fed step through the C ABI -------------------------------
@@ -332,94 +450,130 @@ def run_ours(a):
     }
 
     cpu = None
+    cfg = None
     if rank == 0 and world == 1 and not a.no_cpu:
         try:
             thr = min(os.cpu_count() or 1, 256)
-            sample = a.cpu_sample or 1
+            sample = a.cpu_sample or CPU_STACK_SAMPLE
             t, n, kind, used = cpu_reference_stack(sample, st.types, thr)
-            cpu = {"value": n / t, "unit": UNIT, "cores": used, "kind": kind,
-                   "sample": f"{n} image(s) of the conv1-5 stack fwd+bwd ({t:.1f} s), lowering {st.types}"}
+            cpu = {"value": n / t, "unit": UNIT, "cores": used, "kind": kind, "cpu_model": cpu_model(),
+                   "sample": f"{n} images of the conv1-5 stack fwd+bwd_data+bwd_weight ({t:.1f} s; BASELINE.md "
+                             f"section 3), lowering {st.types}, the reference's multiply with {used} threads"}
+            if not a.no_configs:
+                # configs[0] on the CPU at its full batch: conv2, b = 256, Type 1
+                impl, kind1 = _reference_impl()
+                t1 = cpu_reference_layer(impl, kind1, CAFFENET_GEOM[1], 256, 1, thr)
+                cpu["configs[0] conv2 b256 T1 fwd+bwd"] = {
+                    "images_per_s": 256 / t1, "seconds": t1, "tflops": 3 * 2 * 27 ** 2 * 25 * 96 * 256 * 256 / t1 / 1e12,
+                    "cores": thr if kind1 == "reference" else 1, "kind": kind1}
         except Exception as exc:  # noqa: BLE001
             cpu = {"value": None, "unit": UNIT, "cores": None, "kind": "unavailable", "sample": repr(exc)}
+    if rank == 0 and world == 1 and not a.no_configs:
+        cfg = run_configs(torch, peak)
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
-            "warmup": a.warmup, "ms_per_step": ms_max, "higher_is_better": True, "scaling": "weak",
+            "warmup": a.warmup, "ms_per_step": ms_max, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 accumulate)",
             "data": "synthetic U(-1,1), CaffeNet conv1-5 shapes",
-            "config": {"workload": "caffenet conv1-5 fwd+bwd_data+bwd_weight, auto lowering per layer",
-                       "images_per_gpu": a.batch, "global_batch": images,
+            "config": {"workload": WORKLOAD,
+                       "images_per_gpu": st.batch, "global_batch": images,
                        "lowering": {l.name: t for l, t in zip(st.layers, st.types)},
                        "parallelism": f"dp{world} (batch split, NCCL all-reduce of dW)" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (step working set > 2 GB)"},
             "tflops": tflops, "tflops_per_gpu": tflops / world,
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
-            "clocks": clk, "phases": phase,
+            "clocks": clk, "phases": phase, "configs": cfg,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+def stack_flops(layers):
+    return float(sum(3 * l.desc(1).flops_per_pass() for l in layers))
+
+
 def run_e2e(a, st, torch, world, group, dev):
-    """K steps fed from pinned host memory: H2D x/dy of every layer on a copy
-    stream (overlapping the previous layer's compute), D2H of every dW.  The device
-    inputs are double-buffered, so step k+1's copies start while step k computes
-    (the copy stream waits only for the step that last read the same buffer set)."""
+    """K steps through the C ABI fed from, and returning to, pinned HOST memory.
+    Per step: H2D of every layer's x and dy (copy stream 1), D2H of every layer's
+    y, dx and dW (copy stream 2) -- the reference API returns OutputBatch and the
+    gradients on the host.  Inputs and outputs are double-buffered on
+    the device, so step k+1's uploads and step k's downloads overlap compute."""
     import torch.distributed as dist
-    hx = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in st.x]
-    hdy = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in st.dy]
-    hdw = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in st.dw]
+
+    from paper_1504_04343_b200.conv import conv_bwd, conv_fwd_cached
+    nl = len(st.layers)
+    pin = lambda ts: [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in ts]  # noqa: E731
+    hx, hdy = pin(st.x), pin(st.dy)
+    hy, hdx, hdw = pin(st.y), pin(st.dx), pin(st.dw)
     for h, t in zip(hx + hdy, st.x + st.dy):
         h.copy_(t.cpu())
     comp = torch.cuda.current_stream()
-    copy = torch.cuda.Stream(device=dev)
-    nl = len(st.layers)
+    up = torch.cuda.Stream(device=dev)
+    down = torch.cuda.Stream(device=dev)
     h2d = sum(t.numel() * 4 for t in hx + hdy)
-    d2h = sum(t.numel() * 4 for t in hdw)
-    bufs = [(st.x, st.dy), ([torch.empty_like(t) for t in st.x], [torch.empty_like(t) for t in st.dy])]
-    done = [None, None]  # comp-stream event: the last step that read buffer set s finished
+    d2h = sum(t.numel() * 4 for t in hy + hdx + hdw)
+    ins = [(st.x, st.dy), ([torch.empty_like(t) for t in st.x], [torch.empty_like(t) for t in st.dy])]
+    outs = [(st.y, st.dx, st.dw), ([torch.empty_like(t) for t in st.y], [torch.empty_like(t) for t in st.dx],
+                                   [torch.empty_like(t) for t in st.dw])]
+    in_free = [None, None]   # comp event: the last step that read input set s is done
+    out_free = [None, None]  # down event: the downloads of output set s are done
     step = [0]
+
+    def ev(s):
+        e = torch.cuda.Event()
+        e.record(s)
+        return e
 
     def one():
         s = step[0] & 1
         step[0] += 1
-        xs, dys = bufs[s]
-        evx, evdy = [], []
-        with torch.cuda.stream(copy):
-            if done[s] is not None:
-                copy.wait_event(done[s])
+        xs, dys = ins[s]
+        ys, dxs, dws = outs[s]
+        evx, evdy = [None] * nl, [None] * nl
+        with torch.cuda.stream(up):
+            if in_free[s] is not None:
+                up.wait_event(in_free[s])
             for i in range(nl):
                 xs[i].copy_(hx[i], non_blocking=True)
-                e = torch.cuda.Event()
-                e.record(copy)
-                evx.append(e)
+                evx[i] = ev(up)
             for i in reversed(range(nl)):
                 dys[i].copy_(hdy[i], non_blocking=True)
-                e = torch.cuda.Event()
-                e.record(copy)
-                evdy.append(e)
-        evdy = evdy[::-1]
-        from paper_1504_04343_b200.conv import conv_bwd, conv_fwd_cached
+                evdy[i] = ev(up)
+        if out_free[s] is not None:
+            comp.wait_event(out_free[s])
         for i, d in enumerate(st.descs):
             comp.wait_event(evx[i])
-            conv_fwd_cached(xs[i], st.w[i], d, st.types[i], cache=st.cache[i], out=st.y[i], ws=st.ws)
+            conv_fwd_cached(xs[i], st.w[i], d, st.types[i], cache=st.cache[i], out=ys[i], ws=st.ws)
+            e = ev(comp)
+            with torch.cuda.stream(down):
+                down.wait_event(e)
+                hy[i].copy_(ys[i], non_blocking=True)
         handles = []
         for i in reversed(range(nl)):
             d, t = st.descs[i], st.types[i]
             comp.wait_event(evdy[i])
-            conv_bwd(dys[i], st.w[i], d, t, x=xs[i], cache=st.cache[i], dx=st.dx[i], dw=st.dw[i], ws=st.ws)
+            conv_bwd(dys[i], st.w[i], d, t, x=xs[i], cache=st.cache[i], dx=dxs[i], dw=dws[i], ws=st.ws)
+            e = ev(comp)
+            with torch.cuda.stream(down):
+                down.wait_event(e)
+                hdx[i].copy_(dxs[i], non_blocking=True)
             if group is not None:
-                handles.append((i, dist.all_reduce(st.dw[i], group=group, async_op=True)))
+                handles.append((i, dist.all_reduce(dws[i], group=group, async_op=True)))
             else:
-                hdw[i].copy_(st.dw[i], non_blocking=True)
+                with torch.cuda.stream(down):
+                    hdw[i].copy_(dws[i], non_blocking=True)
         for i, h in handles:
             h.wait()
-            hdw[i].copy_(st.dw[i], non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record(comp)
-        done[s] = ev
+            e = ev(comp)
+            with torch.cuda.stream(down):
+                down.wait_event(e)
+                hdw[i].copy_(dws[i], non_blocking=True)
+        in_free[s] = ev(comp)
+        out_free[s] = ev(down)
 
     for _ in range(2):
         one()
@@ -430,6 +584,7 @@ def run_e2e(a, st, torch, world, group, dev):
     e0.record(comp)
     for _ in range(a.steps):
         one()
+    comp.wait_stream(down)  # the last step's results are on the host
     e1.record(comp)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
@@ -437,10 +592,11 @@ def run_e2e(a, st, torch, world, group, dev):
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    return {"value": a.batch * world / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
+    return {"value": st.global_batch / (ms * 1e-3), "unit": UNIT, "ms_per_step": ms,
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "h2d_gb_per_s": h2d / (ms * 1e-3) / 1e9,
-            "path": "C ABI (cct_conv_*) on double-buffered device inputs fed by pinned-host H2D copies on a side stream"}
+            "h2d_gb_per_s": h2d / (ms * 1e-3) / 1e9, "d2h_gb_per_s": d2h / (ms * 1e-3) / 1e9,
+            "path": "C ABI (cct_conv_fwd_cached / cct_conv_bwd) on double-buffered device buffers: pinned-host "
+                    "H2D of x, dy and D2H of y, dx, dW on two copy streams overlapping compute"}
 
 
 if __name__ == "__main__":

@@ -105,7 +105,7 @@ CCT_API cct_status cct_conv_bwd_weight(const cct_conv_desc* desc, cct_lowering l
                                const float* dy, float* dw, void* ws, size_t ws_bytes,
                                void* stream);
 
-/* Workspace limit (bytes; default 16 GiB or $CCT_WORKSPACE_LIMIT).  A pass whose
+/* Workspace limit (bytes; default 16 GiB).  A pass whose
  * scratch would exceed it runs over batch chunks that reuse one scratch region
  * (the SPEC batching module's partitions), e.g. Type 3 on
  * conv1, whose Rhat is 2.4 GB per image.  cct_workspace_size() reports the
@@ -114,7 +114,7 @@ CCT_API void cct_set_workspace_limit(size_t bytes);
 CCT_API size_t cct_get_workspace_limit(void);
 
 /* Implicit Type 1 lowering (the paper's "fusion").
- * mode 1 (default; $CCT_IMPLICIT): for Type 1 layers with d % 16 == 0 the
+ * mode 1 (default): for Type 1 layers with d % 16 == 0 the
  *   forward and backward-weight GEMMs read their lowered operand straight from
  *   x through TMA im2col tiles -- Dhat never exists in HBM (the forward is
  *   bit-identical to the materialised path).  At stride 1 with o % 16 == 0,
@@ -128,6 +128,32 @@ CCT_API size_t cct_get_workspace_limit(void);
  * mode 0: everything materialised. */
 CCT_API void cct_set_implicit_lowering(int mode);
 CCT_API int cct_get_implicit_lowering(void);
+
+/* Tuning switches.  Process-wide and explicit: the library reads no environment
+ * variables, so results and kernel choices depend only on calls made through
+ * this ABI.  Each key selects between measured variants of the same computation
+ * (every value stays within the parity tolerance; the defaults are the forms
+ * measured fastest on B200).  cct_set_tuning returns
+ * CCT_ERR_CONFIG for an unknown key or an out-of-range value. */
+typedef enum {
+    CCT_TUNE_SPLIT_PRODUCER = 0, /* 1 (default): A and B TMA tiles issued by two producer threads       */
+    CCT_TUNE_A_TMEM = 1,         /* N <= 96 tiles: 0 A from smem, 1 A in TMEM (default), 2 deeper A ring */
+    CCT_TUNE_A_TMEM_WIDE = 2,    /* 1 (default): 192/256/384-wide CTA-pair tiles keep A in TMEM          */
+    CCT_TUNE_CTA_PAIRS = 3,      /* 0 auto (default), 1 single CTAs only, 2 CTA pairs whenever legal     */
+    CCT_TUNE_BN384 = 4,          /* 1 (default): one 256 + 128 composite tile for N = 384                */
+    CCT_TUNE_STREAMK = 5,        /* 1 (default): stream-K for GEMMs whose last wave would idle           */
+    CCT_TUNE_CHAIN2 = 6,         /* 1 (default): two TMEM accumulation chains instead of 2-way split-K   */
+    CCT_TUNE_S2D = 7,            /* strided Type 1: 0 never space-to-depth, 1 cost model (default), 2 always */
+    CCT_TUNE_IMPLICIT_BWD = 8,   /* implicit Type 1 backward-data: 0 never, 1 cost model (default), 2 always */
+    CCT_TUNE_WGRAD_SWAP = 9,     /* 1 (default): swapped implicit backward-weight for o < 128            */
+    CCT_TUNE_DGRAD_SWAP = 10,    /* swapped implicit backward-data: 0 never, 1 d < 128 (default), 2 d <= 128 */
+    CCT_TUNE_FWD_SWAP = 11,      /* 1: swapped forward for o < 128 (default 0: measured slower)          */
+    CCT_TUNE_TRACE_PHASES = 12,  /* 1: one stderr line per kernel launch (diagnostics)                   */
+    CCT_TUNE_COUNT = 13
+} cct_tuning;
+CCT_API cct_status cct_set_tuning(cct_tuning key, int value);
+CCT_API int cct_get_tuning(cct_tuning key); /* -1 for an unknown key */
+CCT_API void cct_reset_tuning(void);        /* every key back to its default */
 
 /* Training-step entry points (the lowered-matrix cache).
  * cct_conv_fwd_cached leaves the data-side matrix Dhat of the forward pass in a

@@ -19,7 +19,7 @@ from dataclasses import dataclass
 __all__ = [
     "lib", "ConvDesc", "CctError", "ConfigError", "ResourceError",
     "LOWER_AUTO", "LOWER_T1", "LOWER_T2", "LOWER_T3", "PASS_FWD", "PASS_BWD_DATA", "PASS_BWD_WEIGHT", "PASS_BWD",
-    "ROWS_SPEC", "ROWS_INTERNAL",
+    "ROWS_SPEC", "ROWS_INTERNAL", "TUNE", "set_tuning", "get_tuning", "reset_tuning", "tuning",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -30,6 +30,10 @@ LOWER_AUTO, LOWER_T1, LOWER_T2, LOWER_T3 = 0, 1, 2, 3
 PASS_FWD, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_BWD = 0, 1, 2, 3
 ROWS_SPEC, ROWS_INTERNAL = 0, 1
 OK, ERR_CONFIG, ERR_RESOURCE, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+# cct_tuning keys (include/cct.h): explicit process-wide switches between measured variants
+TUNE = {"split_producer": 0, "a_tmem": 1, "a_tmem_wide": 2, "cta_pairs": 3, "bn384": 4, "streamk": 5,
+        "chain2": 6, "s2d": 7, "implicit_bwd": 8, "wgrad_swap": 9, "dgrad_swap": 10, "fwd_swap": 11,
+        "trace_phases": 12}
 
 
 class CctError(RuntimeError):
@@ -115,6 +119,11 @@ def lib() -> C.CDLL:
     L.cct_set_implicit_lowering.argtypes = [C.c_int]
     L.cct_set_implicit_lowering.restype = None
     L.cct_get_implicit_lowering.restype = C.c_int
+    L.cct_set_tuning.argtypes = [C.c_int, C.c_int]
+    L.cct_set_tuning.restype = C.c_int
+    L.cct_get_tuning.argtypes = [C.c_int]
+    L.cct_get_tuning.restype = C.c_int
+    L.cct_reset_tuning.restype = None
     L.cct_launch_count.restype = C.c_uint64
     L.cct_reset_launch_count.restype = None
     _lib = L
@@ -165,6 +174,38 @@ def lowered_cache_size(desc: ConvDesc, lowering: int) -> int:
     out = C.c_size_t()
     check(lib().cct_lowered_cache_size(C.byref(desc.c()), lowering, C.byref(out)))
     return out.value
+
+
+def set_tuning(key: str, value: int) -> None:
+    """cct_set_tuning: select a measured kernel variant (see include/cct.h)."""
+    check(lib().cct_set_tuning(TUNE[key], int(value)))
+
+
+def get_tuning(key: str) -> int:
+    return int(lib().cct_get_tuning(TUNE[key]))
+
+
+def reset_tuning() -> None:
+    lib().cct_reset_tuning()
+
+
+class tuning:
+    """Context manager: ``with tuning(split_producer=0): ...`` restores the old values on exit."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            self.old[k] = get_tuning(k)
+            set_tuning(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.old.items():
+            set_tuning(k, v)
+        return False
 
 
 def launch_count() -> int:

@@ -138,15 +138,8 @@ const float* weights_view(const Lowered& L, const float* w, Ws& ws, cudaStream_t
 // Implicit Type 1 lowering (TMA im2col A operand) -- on by default; the
 // materialised path stays available for parity tests and small-channel layers.
 // process-wide knobs (atomics: the ABI may be called from several host threads)
-std::atomic<int> g_implicit{-1};
-bool implicit_enabled() {
-    if (g_implicit.load() < 0) {
-        const char* e = getenv("CCT_IMPLICIT");
-        int expected = -1;
-        g_implicit.compare_exchange_strong(expected, e ? std::max(0, std::min(2, atoi(e))) : 1);
-    }
-    return g_implicit.load() != 0;
-}
+std::atomic<int> g_implicit{1};
+bool implicit_enabled() { return g_implicit.load() != 0; }
 
 // Type 1 with d % 16 == 0 runs forward and backward-weight on the input itself.
 bool t1_implicit(const Geo& g, int type, const float* x) {
@@ -156,7 +149,7 @@ bool t1_implicit(const Geo& g, int type, const float* x) {
 
 // A strided Type 1 layer whose blocked depth s^2 d is a multiple of 16 runs in
 // space-to-depth form (s2d.cuh): the implicit stride-1 GEMMs on X' (CaffeNet
-// conv1: 3 x 3 taps of depth 48).  $CCT_S2D=0 keeps the materialised path.
+// conv1: 3 x 3 taps of depth 48).  CCT_TUNE_S2D = 0 keeps the materialised path.
 // Whether that form is used is the cost model's call per pass (prefer_s2d): the
 // entry points set the pass context (0 fwd, 1 bwd-data, 2 bwd-weight, 3 training
 // step: cct_conv_fwd_cached + cct_conv_bwd, whose lowered cache must agree).
@@ -174,15 +167,12 @@ bool prefer_s2d(const cct_conv_desc* desc, int pass);  // cost_model.cpp
 namespace {
 
 bool t1_s2d(const Geo& g, int type) {
-    static const int env = [] {
-        const char* e = getenv("CCT_S2D");
-        return e ? atoi(e) : 1;
-    }();
+    const int env = tuning(CCT_TUNE_S2D);
     if (!(env && implicit_enabled() && type == 1 && g.s > 1)) return false;
     const Geo v = s2d_geo(g);
     if (!(im2col_ok(v.d, false) && v.b * v.n * v.n * v.d < (int64_t(1) << 40) && v.b * v.n * v.n < (int64_t(1) << 31)))
         return false;
-    if (env == 2) return true;  // $CCT_S2D=2: always (profiling)
+    if (env == 2) return true;  // CCT_TUNE_S2D = 2: always (profiling)
     cct_conv_desc d{};
     d.n = g.n; d.k = g.k; d.d = g.d; d.o = g.o; d.b = g.b; d.stride = g.s; d.pad = g.p;
     return prefer_s2d(&d, t_pass);
@@ -223,10 +213,7 @@ bool t1_implicit_bwd(const Geo& g, int type) {
     if (!(implicit_enabled() && type == 1 && g.s == 1 && g.p <= g.k - 1 && im2col_ok(g.o, false) &&
           g.b * g.n * g.n < (int64_t(1) << 31) && g.b * g.m * g.m * g.o < (int64_t(1) << 40)))
         return false;
-    static const int env = [] {  // $CCT_IMPLICIT_BWD: 0 never, 2 always (profiling)
-        const char* e = getenv("CCT_IMPLICIT_BWD");
-        return e ? atoi(e) : 1;
-    }();
+    const int env = tuning(CCT_TUNE_IMPLICIT_BWD);  // 0 never, 2 always (profiling)
     if (env == 0) return false;
     if (env == 2) return true;
     cct_conv_desc d{};
@@ -236,24 +223,18 @@ bool t1_implicit_bwd(const Geo& g, int type) {
 
 // Implicit backward-weight of a narrow bank (o < 128) runs swapped: dW rows = the o
 // channels, columns = (tap, channel) -- B is the MN-major TMA im2col of x -- instead of
-// an o-wide tile.  $CCT_WGRAD_SWAP=0 disables it (A/B).
+// an o-wide tile.  CCT_TUNE_WGRAD_SWAP = 0 disables it (A/B).
 bool wgrad_swapped(const Geo& g) {
-    static const int env = [] {
-        const char* e = getenv("CCT_WGRAD_SWAP");
-        return e ? atoi(e) : 1;
-    }();
+    const int env = tuning(CCT_TUNE_WGRAD_SWAP);
     return env != 0 && g.o < 128 && g.k * g.k * im2col_dk(g.d, true) >= 192;
 }
 
 // Implicit backward-data with a narrow kernel depth (d < 128) runs swapped, the
 // pixels as the GEMM's N side (B = TMA im2col of dy): a 128-row tile with d useful
 // rows beats a d-wide tile (measured narrow-tile rate ~ 0.58 of the 256-wide one at
-// d = 96).  $CCT_DGRAD_SWAP: 0 never, 2 always (A/B).
+// d = 96).  CCT_TUNE_DGRAD_SWAP: 0 never, 2 always (A/B).
 bool dgrad_swapped(const Geo& g) {
-    static const int env = [] {
-        const char* e = getenv("CCT_DGRAD_SWAP");
-        return e ? atoi(e) : 1;
-    }();
+    const int env = tuning(CCT_TUNE_DGRAD_SWAP);
     if (env == 0) return false;
     if (env == 2) return g.d <= 128;
     return g.d < 128;
@@ -263,12 +244,9 @@ bool dgrad_swapped(const Geo& g) {
 // 128-row side, pixels as the 256-wide tile, NCHW rows written by the transposing epilogue.
 // Measured on conv1 (b = 256): 0.50 ms vs 0.40 ms for the o-wide tile (materialised) and
 // 0.64 vs 0.56 ms in space-to-depth form -- the NCHW row stores (one 1 KB run per channel per
-// tile) cost more than the narrow MMAs -- so it is off by default; $CCT_FWD_SWAP=1 enables it.
+// tile) cost more than the narrow MMAs -- so it is off by default; CCT_TUNE_FWD_SWAP = 1 enables it.
 bool fwd_swapped(const Geo& g) {
-    static const int env = [] {
-        const char* e = getenv("CCT_FWD_SWAP");
-        return e ? atoi(e) : 0;
-    }();
+    const int env = tuning(CCT_TUNE_FWD_SWAP);
     return env != 0 && g.o < 128 && g.b * g.m * g.m >= 4096;
 }
 
@@ -304,11 +282,8 @@ cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStr
     const int64_t kb = (gp.K + kBK - 1) / kBK;
     int splits = effective_splits(kb, int((kb + kMaxChainKB - 1) / kMaxChainKB));
     // a 2-way accuracy split of a wide-tile K-major GEMM runs as two TMEM chains of one tile
-    // (no partial tiles, no reduce kernel); $CCT_CHAIN2=0 keeps the split-K form (A/B)
-    static const int chain2_env = [] {
-        const char* e = getenv("CCT_CHAIN2");
-        return e ? atoi(e) : 1;
-    }();
+    // (no partial tiles, no reduce kernel); CCT_TUNE_CHAIN2 = 0 keeps the split-K form (A/B)
+    const int chain2_env = tuning(CCT_TUNE_CHAIN2);
     if (splits == 2 && chain2_env && gp.A.major == Major::K && gp.B.major == Major::K && !gp.C.transposed &&
         gp.passes == 3 && tile_n(gp) >= 192 && tile_n(gp) <= 256) {
         splits = 1;
@@ -351,12 +326,9 @@ void wgrad_im2col(GemmProblem& gp, const Geo& g, const float* x) {
 
 // Backward-weight reductions (K = b m^2 pixels) are split for accuracy and wave fill; with
 // two TMEM chains per unit (CH2) the accuracy floor halves, so half as many partial tiles
-// reach HBM.  Wide tiles only (two 256-column accumulators fit TMEM).  $CCT_CHAIN2=0: off.
+// reach HBM.  Wide tiles only (two 256-column accumulators fit TMEM).  CCT_TUNE_CHAIN2 = 0: off.
 int wgrad_chain2(const GemmProblem& gp) {
-    static const int env = [] {
-        const char* e = getenv("CCT_CHAIN2");
-        return e ? atoi(e) : 1;
-    }();
+    const int env = tuning(CCT_TUNE_CHAIN2);
     const int bn = tile_n(gp);
     return (env && gp.passes == 3 && !gp.C.transposed && bn >= 192 && bn <= 256 &&
             gp.K > int64_t(kMaxChainKB) * kBK) ? 1 : 0;
@@ -676,16 +648,9 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
 // reuse the same scratch region in stream order.  Backward-weight partials of
 // the chunks are summed in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
-std::atomic<size_t> g_ws_limit{0};
+std::atomic<size_t> g_ws_limit{size_t(16) << 30};
 
-size_t ws_limit() {
-    if (!g_ws_limit.load()) {
-        const char* e = getenv("CCT_WORKSPACE_LIMIT");
-        size_t expected = 0;
-        g_ws_limit.compare_exchange_strong(expected, e ? size_t(strtoull(e, nullptr, 10)) : (size_t(16) << 30));
-    }
-    return g_ws_limit.load();
-}
+size_t ws_limit() { return g_ws_limit.load(); }
 
 Geo with_batch(Geo g, int64_t b) {
     g.b = b;
@@ -1064,8 +1029,11 @@ cct_status cct_conv_bwd(const cct_conv_desc* desc, cct_lowering lowering, const 
     if (!wsp || ws_bytes < need) return fail(CCT_ERR_RESOURCE, "workspace too small for " + desc_str(desc));
     Ws ws(wsp);
     const Geo g = geo_of(desc);
-    // a cache is only meaningful when Dhat is not the input itself
-    const float* c = (cache && !(x && dhat_is_input(g, type, x))) ? cache : nullptr;
+    // a cache is only meaningful when the forward wrote one: not when Dhat is the input itself, and
+    // not for the implicit forms (cct_lowered_cache_size 0: cct_conv_fwd_cached left it untouched)
+    size_t cneed = 0;
+    if ((s = cct_lowered_cache_size(desc, cct_lowering(type), &cneed)) != CCT_OK) return s;
+    const float* c = (cache && cneed && !(x && dhat_is_input(g, type, x))) ? cache : nullptr;
     if (dw && !x && !c) return fail(CCT_ERR_CONFIG, "bwd-weight needs x for this lowering");
     PassCtx pc(3);
     return run_bwd(g, type, x, c, dy, w, dx, dw, ws, as_stream(stream));
@@ -1243,11 +1211,24 @@ static cct_status gemm_common(int64_t M, int64_t N, int64_t K, const float* A, i
     gp.A = {B, ldb, Major::MN};
     gp.B = {A, lda, Major::K};
     gp.passes = passes;
-    int splits = split_k > 0 ? effective_splits((K + kBK - 1) / kBK, split_k) : plan_splits(gp);
+    const int64_t kb = (K + kBK - 1) / kBK;
+    // accuracy floor: every TMEM accumulation chain <= kMaxChainKB k-blocks (the tensor core
+    // truncates its fp32 accumulation, so one long chain drifts ~linearly with K)
+    const int floor_splits = effective_splits(kb, int((kb + kMaxChainKB - 1) / kMaxChainKB));
+    int splits = split_k > 0 ? effective_splits(kb, std::max(split_k, floor_splits)) : plan_splits(gp);
     if (passes != 3) splits = 1;
     if (splits > 1) {
         const size_t need = size_t(splits) * size_t(M) * size_t(N) * 4;
-        if (!ws || ws_bytes < need) splits = 1;  // degrade gracefully: no workspace, no split
+        if (!ws || ws_bytes < need) {
+            if (passes == 3 && floor_splits > 1) {
+                std::ostringstream os;
+                os << "gemm (" << M << " x " << N << " x " << K << "): K needs " << floor_splits
+                   << " accumulation chains for fp32 accuracy; workspace of " << need << " bytes required, got "
+                   << (ws ? ws_bytes : 0) << " (cct_gemm_workspace_size)";
+                return fail(CCT_ERR_RESOURCE, os.str());
+            }
+            splits = 1;  // wave-fill splits only: run unsplit
+        }
     }
     if (splits > 1) {
         float* parts = static_cast<float*>(ws);
@@ -1268,7 +1249,9 @@ cct_status cct_gemm_workspace_size(int64_t M, int64_t N, int64_t K, int split_k,
     gp.K = K;
     gp.A.major = Major::MN;
     gp.B.major = Major::K;
-    const int splits = split_k > 0 ? effective_splits((K + kBK - 1) / kBK, split_k) : plan_splits(gp);
+    const int64_t kb = (K + kBK - 1) / kBK;
+    const int floor_splits = effective_splits(kb, int((kb + kMaxChainKB - 1) / kMaxChainKB));
+    const int splits = split_k > 0 ? effective_splits(kb, std::max(split_k, floor_splits)) : plan_splits(gp);
     *bytes = splits > 1 ? size_t(splits) * size_t(M) * size_t(N) * 4 : 0;
     return CCT_OK;
 }

@@ -1,6 +1,8 @@
 // common.cu -- device property cache, launch counter, thread-local error text.
 #include "common.cuh"
 
+#include "cct.h"
+
 #include <atomic>
 #include <cstdio>
 #include <cstdlib>
@@ -27,6 +29,23 @@ int num_sms() {
     return g_sms[dev];
 }
 
+// Tuning switches (cct_set_tuning): explicit, process-wide; the library reads no
+// environment variables, so results and tile choices depend only on the caller's calls.
+namespace {
+constexpr int kTuneDefaults[CCT_TUNE_COUNT] = {
+    /* SPLIT_PRODUCER */ 1, /* A_TMEM */ 1,     /* A_TMEM_WIDE */ 1, /* CTA_PAIRS */ 0,
+    /* BN384 */ 1,          /* STREAMK */ 1,    /* CHAIN2 */ 1,      /* S2D */ 1,
+    /* IMPLICIT_BWD */ 1,   /* WGRAD_SWAP */ 1, /* DGRAD_SWAP */ 1,  /* FWD_SWAP */ 0,
+    /* TRACE_PHASES */ 0};
+constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 2, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1};
+std::atomic<int> g_tune[CCT_TUNE_COUNT] = {
+    {kTuneDefaults[0]}, {kTuneDefaults[1]}, {kTuneDefaults[2]},  {kTuneDefaults[3]},  {kTuneDefaults[4]},
+    {kTuneDefaults[5]}, {kTuneDefaults[6]}, {kTuneDefaults[7]},  {kTuneDefaults[8]},  {kTuneDefaults[9]},
+    {kTuneDefaults[10]}, {kTuneDefaults[11]}, {kTuneDefaults[12]}};
+}  // namespace
+
+int tuning(int key) { return (key >= 0 && key < CCT_TUNE_COUNT) ? g_tune[key].load(std::memory_order_relaxed) : 0; }
+
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 void reset_launch_count() { g_launches.store(0, std::memory_order_relaxed); }
@@ -47,8 +66,7 @@ uint64_t g_acc_n[kNumPhases];
 void profile_enable(bool on) { g_prof.store(on); }
 
 PhaseScope::PhaseScope(Phase ph, cudaStream_t s, double flops, double bytes) : slot(-1), st(s) {
-    static const bool trace = getenv("CCT_TRACE_PHASES") != nullptr;  // diagnostics
-    if (trace) fprintf(stderr, "cct-phase %d bytes %.0f flops %.0f\n", int(ph), bytes, flops);
+    if (tuning(CCT_TUNE_TRACE_PHASES)) fprintf(stderr, "cct-phase %d bytes %.0f flops %.0f\n", int(ph), bytes, flops);
     if (!g_prof.load(std::memory_order_relaxed)) return;
     Rec r{};
     if (cudaEventCreate(&r.a) != cudaSuccess || cudaEventCreate(&r.b) != cudaSuccess) return;
@@ -94,3 +112,24 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 const char* last_error() { return g_last_error.c_str(); }
 
 }  // namespace cct
+
+extern "C" {
+cct_status cct_set_tuning(cct_tuning key, int value) {
+    const int k = int(key);
+    if (k < 0 || k >= CCT_TUNE_COUNT) {
+        cct::set_error("unknown tuning key " + std::to_string(k));
+        return CCT_ERR_CONFIG;
+    }
+    if (value < 0 || value > cct::kTuneMax[k]) {
+        cct::set_error("tuning key " + std::to_string(k) + ": value " + std::to_string(value) + " out of range [0, " +
+                       std::to_string(cct::kTuneMax[k]) + "]");
+        return CCT_ERR_CONFIG;
+    }
+    cct::g_tune[k].store(value);
+    return CCT_OK;
+}
+int cct_get_tuning(cct_tuning key) { return (int(key) >= 0 && int(key) < CCT_TUNE_COUNT) ? cct::tuning(int(key)) : -1; }
+void cct_reset_tuning(void) {
+    for (int k = 0; k < CCT_TUNE_COUNT; ++k) cct::g_tune[k].store(cct::kTuneDefaults[k]);
+}
+}  // extern "C"

@@ -10,7 +10,8 @@
 namespace cct {
 
 int num_sms();              // SM count of the current device (cached per device)
-void note_launch();         // count one kernel launch (cct_launch_count)
+void note_launch();
+int tuning(int key);        // cct_set_tuning value of a cct_tuning key         // count one kernel launch (cct_launch_count)
 void set_error(const std::string& msg);
 const char* last_error();
 

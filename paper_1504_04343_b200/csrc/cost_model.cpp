@@ -134,8 +134,7 @@ double dgrad_seconds(const G& g, bool implicit, double rows, double cols, double
 // (s2d.cuh, cct_abi.cu t1_s2d): the stride-1 layer of side m + k' - 1, k' = ceil(k/s)
 // taps, depth s^2 d, plus the blocking / unblocking passes.
 bool s2d_possible(const G& g) {
-    const char* e = getenv("CCT_S2D");
-    return (!e || atoi(e) != 0) && cct_get_implicit_lowering() && g.s > 1 && std::fmod(g.s * g.s * g.d, 16) == 0;
+    return cct_get_tuning(CCT_TUNE_S2D) != 0 && cct_get_implicit_lowering() && g.s > 1 && std::fmod(g.s * g.s * g.d, 16) == 0;
 }
 G s2d_of(const G& g) {
     G v = g;

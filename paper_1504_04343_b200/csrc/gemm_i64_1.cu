@@ -1,0 +1,4 @@
+// gemm_i64_1.cu -- kernel variants of tile width 64, CTA group 1 (see gemm_kernel.cuh)
+#include "gemm_kernel.cuh"
+
+CCT_GEMM_INSTANTIATE(64, 1)

@@ -628,15 +628,6 @@ __global__ void __launch_bounds__(256) transpose_batched_kernel(const float* __r
 
 }  // namespace
 
-// $CCT_LOWER_VEC=0 keeps the scalar-staged small-channel lowering (A/B runs)
-static bool lower_vec_enabled() {
-    static const bool on = [] {
-        const char* e = getenv("CCT_LOWER_VEC");
-        return !(e && atoi(e) == 0);
-    }();
-    return on;
-}
-
 cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, float* dhat, int64_t ld,
                   cudaStream_t st) {
     const int64_t cols = lowered_cols(g, type);
@@ -658,11 +649,10 @@ cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, floa
         const size_t smemv = size_t((g.k + 1) * ((g.n * g.d + 7) & ~int64_t(3))) * 4;
         const int64_t total = g.b * g.n * g.n * g.d;
         if (g.p == 0 && total % 4 == 0 && reinterpret_cast<uintptr_t>(x) % 16 == 0 && nt >= 2 && nt <= 16 &&
-            smemv <= 96 * 1024 && lower_vec_enabled()) {
+            smemv <= 96 * 1024) {
             auto gov = [&](auto kern) {
                 cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);  // per device
-                int threads = 512;
-                if (const char* e = getenv("CCT_LOWER_THREADS")) threads = atoi(e);
+                const int threads = 512;
                 int per_sm = 0;
                 cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smemv);
                 const int gridv = int(std::min<int64_t>(nqr, int64_t(num_sms()) * std::max(1, per_sm)));
@@ -743,8 +733,7 @@ cudaError_t col2im(const Geo& g, int type, const float* dd, int64_t ld, float* d
         // as 256 threads would (conv1: 681 floats -> 3 x 256).  Measured on conv1
         // b = 256 (ncu): 512 threads 376 us, 352 261 us, 256 219 us (5.8 TB/s), 224 225 us.
         const int64_t nd = g.n * g.d, passes = cdiv(nd, 256);
-        int threads = int(std::min<int64_t>(256, (cdiv(nd, passes) + 31) / 32 * 32));
-        if (const char* e = getenv("CCT_COL2IM_THREADS")) threads = atoi(e);
+        const int threads = int(std::min<int64_t>(256, (cdiv(nd, passes) + 31) / 32 * 32));
         auto kern = (g.k + g.s - 1) / g.s <= 3 ? col2im_t1_smem_kernel<3> : col2im_t1_smem_kernel<0>;
         int per_sm = 0;
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem1);

@@ -58,14 +58,32 @@ def stack_flops_per_image(layers=CAFFENET, passes: int = 3) -> float:
 
 
 class ConvStack:
-    """Device buffers + one fwd/bwd step of a conv stack on this rank's shard."""
+    """Device buffers + one fwd/bwd step of a conv stack on this rank's shard.
+
+    Data-parallel layout: the global batch is ``batch`` images per
+    rank (weak scaling) or ``global_batch`` images split by ``batching.shard_of``
+    (strong scaling, BASELINE configs[4]); rank r owns a contiguous image range.
+    Weights are generated from ``seed`` alone, so every rank holds the same model;
+    x and dy of the global batch come from per-layer seeds and each rank keeps its
+    slice, so the all-reduced dW of the shards is the full-batch dW.
+    """
 
     def __init__(self, batch: int, device: torch.device, layers=CAFFENET, lowering=LOWER_AUTO,
-                 group=None, seed: int = 1234):
+                 group=None, seed: int = 1234, global_batch: int | None = None):
+        from .batching import shard_of
         self.layers = tuple(layers)
-        self.batch = batch
         self.device = device
         self.group = group
+        if group is not None:
+            import torch.distributed as dist
+            self.world, self.rank = dist.get_world_size(group), dist.get_rank(group)
+        else:
+            self.world, self.rank = 1, 0
+        self.global_batch = global_batch if global_batch is not None else batch * self.world
+        self.first, batch = shard_of(self.global_batch, self.world, self.rank)
+        if batch < 1:
+            raise ValueError(f"rank {self.rank} of {self.world} gets no images of a {self.global_batch}-image batch")
+        self.batch = batch
         self.descs = [l.desc(batch) for l in self.layers]
         if isinstance(lowering, (list, tuple)):
             self.types = list(lowering)
@@ -73,15 +91,21 @@ class ConvStack:
             self.types = [select_lowering(d, 3)[0] for d in self.descs]
         else:
             self.types = [lowering] * len(self.layers)
-        g = torch.Generator(device=device)
-        g.manual_seed(seed)
 
-        def u(*shape):
+        def u(sd, *shape):
+            g = torch.Generator(device=device)
+            g.manual_seed(sd)
             return torch.rand(shape, generator=g, device=device, dtype=torch.float32).mul_(2).sub_(1)
 
-        self.x = [u(batch, l.n, l.n, l.d) for l in self.layers]
-        self.w = [u(l.o, l.k, l.k, l.d) for l in self.layers]
-        self.dy = [u(batch, l.o, d.m, d.m) for l, d in zip(self.layers, self.descs)]
+        def shard(sd, *shape):  # this rank's images of a global-batch tensor
+            full = u(sd, self.global_batch, *shape)
+            return full.narrow(0, self.first, batch).contiguous() if self.world > 1 else full
+
+        nl = len(self.layers)
+        self.w = [u(seed + li, l.o, l.k, l.k, l.d) for li, l in enumerate(self.layers)]
+        self.x = [shard(seed + nl + li, l.n, l.n, l.d) for li, l in enumerate(self.layers)]
+        self.dy = [shard(seed + 2 * nl + li, l.o, d.m, d.m)
+                   for li, (l, d) in enumerate(zip(self.layers, self.descs))]
         self.y = [torch.empty_like(t) for t in self.dy]
         self.dx = [torch.empty_like(t) for t in self.x]
         self.dw = [torch.empty_like(t) for t in self.w]

@@ -165,3 +165,30 @@ def test_split_k_request_is_normalised_to_running_splits():
     assert out.value == 95 * M * N * 4
     assert cct.lib().cct_gemm_workspace_size(M, N, K, 50, C.byref(out)) == 0
     assert out.value == 50 * M * N * 4  # 121 k-blocks each: all 50 run
+
+
+def test_tuning_switches_are_explicit():
+    """CPU: the kernel-variant switches are set through the ABI (cct_set_tuning), range
+    checked, and restored by cct_reset_tuning -- the library reads no environment."""
+    import paper_1504_04343_b200 as cct
+    L = cct.lib()
+    cct.reset_tuning()
+    defaults = {k: cct.get_tuning(k) for k in cct.TUNE}
+    assert defaults["split_producer"] == 1 and defaults["fwd_swap"] == 0 and defaults["s2d"] == 1
+    with cct.tuning(s2d=2, split_producer=0):
+        assert cct.get_tuning("s2d") == 2 and cct.get_tuning("split_producer") == 0
+    assert {k: cct.get_tuning(k) for k in cct.TUNE} == defaults
+    assert L.cct_set_tuning(7, 3) == 1          # out of range -> CCT_ERR_CONFIG
+    assert b"out of range" in L.cct_last_error()
+    assert L.cct_set_tuning(99, 0) == 1         # unknown key
+    assert L.cct_get_tuning(99) == -1
+    assert cct.get_tuning("s2d") == 1
+
+
+def test_library_reads_no_environment():
+    """CPU: no getenv in the library's own sources (results cannot depend on the caller's
+    environment; the statically linked CUDA runtime's own CUDA_* handling is not ours)."""
+    srcs = glob.glob(os.path.join(ROOT, "paper_1504_04343_b200", "csrc", "**", "*.c*"), recursive=True)
+    assert srcs
+    offenders = [p for p in srcs if "getenv" in open(p).read()]
+    assert not offenders, offenders

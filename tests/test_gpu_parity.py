@@ -510,6 +510,7 @@ sys.path.insert(0, os.environ["ROOT"]); sys.path.insert(0, os.path.join(os.envir
 import paper_1504_04343_b200 as cct
 from paper_1504_04343_b200 import conv
 from oracle_py import Oracle, rel_l2, grouped_fwd
+cct.set_tuning("fwd_swap", 1)
 orc = Oracle(); dev = torch.device("cuda")
 out = {}
 for name, (n, k, d, o, s, p, G, mode) in {"conv1": (227, 11, 3, 96, 4, 0, 1, 1), "conv1_s2d": (227, 11, 3, 96, 4, 0, 1, 2),
@@ -529,7 +530,7 @@ print(json.dumps(out))
 
 
 def test_swapped_forward_opt_in(cct, dev):
-    """$CCT_FWD_SWAP=1: narrow banks (o < 128) run the forward swapped -- channels on the
+    """CCT_TUNE_FWD_SWAP = 1: narrow banks (o < 128) run the forward swapped -- channels on the
     128-row side, pixels 256 wide (materialised Dhat or TMA-im2col B operand), NCHW rows
     through the transposing epilogue with a per-row bias + ReLU.  Off by default (slower
     on conv1); kept correct here."""
@@ -537,7 +538,7 @@ def test_swapped_forward_opt_in(cct, dev):
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    env = dict(os.environ, CCT_FWD_SWAP="1", ROOT=root)
+    env = dict(os.environ, ROOT=root)
     r = subprocess.run([sys.executable, "-c", SWAP_SCRIPT], capture_output=True, text=True, env=env, timeout=600)
     assert r.returncode == 0, r.stderr[-3000:]
     errs = json.loads(r.stdout.strip().splitlines()[-1])

@@ -1,8 +1,13 @@
-"""CPU, world_size 2 over gloo: the data-parallel path of stack.ConvStack --
-contiguous batch shards (batching.shard_of), local fwd / bwd-data, one SUM
-all-reduce of each layer's weight gradient -- reproduces the full-batch
-gradients.  The per-shard compute here is the oracle (test infrastructure);
-on the GPU box the same step runs libcct.so kernels and NCCL."""
+"""Multi-rank data parallelism.
+
+* CPU, world_size 2 over gloo: the sharding algebra of the driver -- contiguous
+  batch shards (batching.shard_of), local fwd / bwd-data, one SUM all-reduce of
+  each layer's weight gradient -- reproduces the full-batch gradients, with the
+  oracle as the per-shard compute (test infrastructure).
+* GPU (``-m gpu``), world_size 2 over gloo, both ranks on cuda:0: the product
+  driver itself, ``stack.ConvStack`` with a process group (libcct.so kernels, the
+  async all-reduce issued per layer), against a single-rank full-batch ConvStack.
+"""
 import os
 import socket
 
@@ -75,3 +80,54 @@ def test_data_parallel_matches_full_batch(orc, world):
             np.testing.assert_allclose(dw, dw_full, rtol=1e-5, atol=1e-5)  # identical on every rank
         assert np.array_equal(np.concatenate(ys), y_full)                  # fwd is shard-local
         assert np.array_equal(np.concatenate(dxs), dx_full)                # bwd-data is shard-local
+
+
+def _stack_worker(rank, world, port, gb, out):
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    from paper_1504_04343_b200.stack import CAFFENET, ConvStack
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda:0")
+    torch.cuda.set_device(dev)
+    st = ConvStack(0, dev, CAFFENET, 1, group=dist.group.WORLD, global_batch=gb)
+    st.step()
+    torch.cuda.synchronize()
+    out[rank] = {"first": st.first, "batch": st.batch, "types": st.types,
+                 "dw": [t.cpu().numpy() for t in st.dw],
+                 "y": [t.cpu().numpy() for t in st.y], "dx": [t.cpu().numpy() for t in st.dx]}
+    dist.destroy_process_group()
+
+
+def _rel(a, b):
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+@pytest.mark.gpu
+@pytest.mark.timeout(900, method="thread")
+@pytest.mark.parametrize("gb", [6, 7])
+def test_convstack_two_ranks_match_full_batch(gb):
+    """The all-reduced dW of two ConvStack ranks (CaffeNet conv1-5, global batch split
+    3/3 or 4/3) equals the single-rank full-batch dW (rel-L2 <= 1e-6: only the
+    summation order differs), identical on both ranks; each rank's y / dx are its
+    slice of the full-batch y / dx."""
+    from paper_1504_04343_b200.stack import CAFFENET, ConvStack
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_stack_worker, args=(2, _free_port(), gb, out), nprocs=2, join=True)
+    dev = torch.device("cuda:0")
+    full = ConvStack(gb, dev, CAFFENET, 1)  # Type 1 everywhere: the same kernels at both batch sizes
+    full.step()
+    torch.cuda.synchronize()
+    assert (out[0]["first"], out[0]["batch"], out[1]["first"], out[1]["batch"]) == (0, (gb + 1) // 2, (gb + 1) // 2,
+                                                                                      gb // 2)
+    for li in range(len(CAFFENET)):
+        dwf = full.dw[li].cpu().numpy()
+        assert np.array_equal(out[0]["dw"][li], out[1]["dw"][li])
+        assert _rel(out[0]["dw"][li], dwf) <= 1e-6, (li, _rel(out[0]["dw"][li], dwf))
+        for key, ref in (("y", full.y[li]), ("dx", full.dx[li])):
+            got = np.concatenate([out[0][key][li], out[1][key][li]])
+            assert _rel(got, ref.cpu().numpy()) <= 1e-6, (key, li)

@@ -1,0 +1,65 @@
+"""Repeatability stress: the training step is deterministic, bit for bit.
+
+The reference's contract is that results do not depend on scheduling: every
+output element is written by exactly one worker and reduced in a fixed order
+(gemm.cpp:36-38; SPEC.md:153, 186 -- thread counts {1, 2, 4} bit-identical).
+The B200 path keeps that contract (fixed split-K / stream-K reduction order), so
+any difference between two runs of the same step exposes a pipeline race (a
+stage consumed before it landed, a skipped barrier phase).  This runs the
+CaffeNet conv1-5 training step of the bench (b = 256, cost-model lowering, the
+lowered cache) many times and compares y, dx and dW of every layer with the first
+run, for both producer forms of the GEMM.
+"""
+import os
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+STEPS = int(os.environ.get("CCT_STRESS_STEPS", "200"))
+
+
+@pytest.mark.timeout(900, method="thread")
+@pytest.mark.parametrize("split_producer", [1, 0])
+def test_training_step_bitwise_repeatable(cct, dev, split_producer):
+    import torch
+    from paper_1504_04343_b200.stack import ConvStack
+    with cct.tuning(split_producer=split_producer):
+        st = ConvStack(256, dev)
+        st.step()
+        torch.cuda.synchronize()
+        outs = st.y + st.dx + st.dw
+        ref = [t.clone() for t in outs]
+        names = [f"{kind}[{l.name}]" for kind in ("y", "dx", "dw") for l in st.layers]
+        bad = {}
+        for i in range(STEPS):
+            st.step()
+            for name, a, b in zip(names, outs, ref):
+                if not torch.equal(a, b):
+                    bad.setdefault(name, []).append(i)
+        torch.cuda.synchronize()
+    assert not bad, f"non-repeatable outputs over {STEPS} steps: " + \
+        ", ".join(f"{k}: {len(v)} steps (first {v[0]})" for k, v in bad.items())
+    assert all(torch.isfinite(t).all() for t in ref)
+
+
+@pytest.mark.timeout(900, method="thread")
+@pytest.mark.parametrize("tune", [{}, {"bn384": 0}, {"streamk": 0}, {"chain2": 0}, {"a_tmem_wide": 0},
+                                  {"cta_pairs": 1}, {"implicit_bwd": 2}, {"s2d": 2}],
+                         ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()) or "default")
+def test_gemm_variants_repeatable(cct, dev, tune):
+    """Every kernel form the tuning keys select (odd and even ring depths, CTA pairs,
+    stream-K, two-chain, A in TMEM) repeats bit for bit over 30 steps at b = 64."""
+    import torch
+    from paper_1504_04343_b200.stack import ConvStack
+    with cct.tuning(**tune):
+        st = ConvStack(64, dev)
+        st.step()
+        torch.cuda.synchronize()
+        outs = st.y + st.dx + st.dw
+        ref = [t.clone() for t in outs]
+        diffs = 0
+        for _ in range(30):
+            st.step()
+            diffs += sum(0 if torch.equal(a, b) else 1 for a, b in zip(outs, ref))
+    assert diffs == 0
