@@ -72,18 +72,30 @@ typedef enum { CCT_PASS_FWD = 0, CCT_PASS_BWD_DATA = 1, CCT_PASS_BWD_WEIGHT = 2,
  * (SURVEY Appendix A), any stride / pad. */
 typedef enum { CCT_ROWS_SPEC = 0, CCT_ROWS_INTERNAL = 1 } cct_row_order;
 
+/* Layout of the layer output y and its gradient dy.  NCHW is the reference's
+ * OutputBatch ((q*o+j)*m+r)*m+c (tensor.hpp:135-150) and the default; NHWC
+ * ((q*m+r)*m+c)*o+j is the DataBatch order of the NEXT layer's input
+ * (tensor.hpp:28-35), so layers chain without a re-layout, and the implicit
+ * backward reads dy as is (no transpose). */
+typedef enum { CCT_LAYOUT_NCHW = 0, CCT_LAYOUT_NHWC = 1 } cct_layout;
+
 /* LayerConfig (tensor.hpp:15-26) extended with stride and zero padding
  * (defaults 1 / 0 keep the reference semantics).  m = (n + 2p - k)/s + 1. */
 typedef struct {
     int64_t n, k, d, o, b, stride, pad;
-    int64_t m;  /* derived output side                        */
-    int64_t R;  /* derived padded extent actually touched: s(m-1)+k */
+    int64_t m;      /* derived output side                        */
+    int64_t R;      /* derived padded extent actually touched: s(m-1)+k */
+    int64_t layout; /* cct_layout of y / dy; cct_conv_desc_init sets NCHW */
 } cct_conv_desc;
 
 /* Replaces LayerConfig::validate (tensor.cpp:23-30) / layer_of (tensor.cpp:66-75):
  * CCT_ERR_CONFIG unless 1 <= k <= n + 2 pad, d, o, b >= 1, stride >= 1, pad >= 0. */
 CCT_API cct_status cct_conv_desc_init(cct_conv_desc* desc, int64_t n, int64_t k, int64_t d, int64_t o,
                               int64_t b, int64_t stride, int64_t pad);
+/* y / dy layout of every pass of this layer (SURVEY 8(b) y_layout): every entry point
+ * honours it except the _ex extension and the exact (oracle) entry points, which
+ * return CCT_ERR_UNSUPPORTED for NHWC. */
+CCT_API cct_status cct_conv_desc_set_layout(cct_conv_desc* desc, cct_layout layout);
 
 /* Scratch bytes one call of (lowering, pass) needs.  AUTO resolves through
  * cct_select_lowering with the default calibration. */

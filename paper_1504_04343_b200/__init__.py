@@ -19,7 +19,7 @@ from dataclasses import dataclass
 __all__ = [
     "lib", "ConvDesc", "CctError", "ConfigError", "ResourceError",
     "LOWER_AUTO", "LOWER_T1", "LOWER_T2", "LOWER_T3", "PASS_FWD", "PASS_BWD_DATA", "PASS_BWD_WEIGHT", "PASS_BWD",
-    "ROWS_SPEC", "ROWS_INTERNAL", "TUNE", "set_tuning", "get_tuning", "reset_tuning", "tuning",
+    "ROWS_SPEC", "ROWS_INTERNAL", "NCHW", "NHWC", "TUNE", "set_tuning", "get_tuning", "reset_tuning", "tuning",
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -29,6 +29,7 @@ LIB_PATH = os.path.join(os.environ.get("CCT_LIB_DIR", os.path.join(_HERE, "_lib"
 LOWER_AUTO, LOWER_T1, LOWER_T2, LOWER_T3 = 0, 1, 2, 3
 PASS_FWD, PASS_BWD_DATA, PASS_BWD_WEIGHT, PASS_BWD = 0, 1, 2, 3
 ROWS_SPEC, ROWS_INTERNAL = 0, 1
+NCHW, NHWC = 0, 1  # cct_layout of y / dy
 OK, ERR_CONFIG, ERR_RESOURCE, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 # cct_tuning keys (include/cct.h): explicit process-wide switches between measured variants
 TUNE = {"split_producer": 0, "a_tmem": 1, "a_tmem_wide": 2, "cta_pairs": 3, "bn384": 4, "streamk": 5,
@@ -54,7 +55,7 @@ class ConvExt(C.Structure):
 
 
 class _Desc(C.Structure):
-    _fields_ = [(f, C.c_int64) for f in ("n", "k", "d", "o", "b", "stride", "pad", "m", "R")]
+    _fields_ = [(f, C.c_int64) for f in ("n", "k", "d", "o", "b", "stride", "pad", "m", "R", "layout")]
 
 
 class CostEstimate(C.Structure):
@@ -85,6 +86,7 @@ def lib() -> C.CDLL:
     D = P(_Desc)
     sigs = {
         "cct_conv_desc_init": [D] + [I64] * 7,
+        "cct_conv_desc_set_layout": [D, C.c_int],
         "cct_workspace_size": [D, C.c_int, C.c_int, P(SZ)],
         "cct_conv_fwd": [D, C.c_int, VP, VP, VP, VP, SZ, VP],
         "cct_conv_bwd_data": [D, C.c_int, VP, VP, VP, VP, SZ, VP],
@@ -149,11 +151,19 @@ class ConvDesc:
     b: int
     stride: int = 1
     pad: int = 0
+    layout: int = 0  # NCHW (OutputBatch) or NHWC y / dy
 
     def c(self) -> _Desc:
         d = _Desc()
         check(lib().cct_conv_desc_init(C.byref(d), self.n, self.k, self.d, self.o, self.b, self.stride, self.pad))
+        if self.layout:
+            check(lib().cct_conv_desc_set_layout(C.byref(d), self.layout))
         return d
+
+    def y_shape(self) -> tuple[int, int, int, int]:
+        """Shape of y / dy: (b, o, m, m) for NCHW, (b, m, m, o) for NHWC."""
+        m = self.m
+        return (self.b, m, m, self.o) if self.layout == NHWC else (self.b, self.o, m, m)
 
     @property
     def m(self) -> int:

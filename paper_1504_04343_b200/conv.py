@@ -70,7 +70,7 @@ def _run(fn, desc: ConvDesc, lowering: int, pass_: int, a, b, out, ws, stream):
 def conv_fwd(x, w, desc: ConvDesc, lowering: int = LOWER_AUTO, out=None, ws=None, stream=None):
     """convolve_lowered (SPEC.md:130): x (b,n,n,d) NHWC, w (o,k,k,d) -> y (b,o,m,m) NCHW."""
     m = desc.m
-    y = out if out is not None else torch.empty((desc.b, desc.o, m, m), dtype=torch.float32, device=x.device)
+    y = out if out is not None else torch.empty(desc.y_shape(), dtype=torch.float32, device=x.device)
     return _run(lib().cct_conv_fwd, desc, lowering, PASS_FWD, x, w, y, ws, stream)
 
 
@@ -99,7 +99,7 @@ def conv_fwd_cached(x, w, desc: ConvDesc, lowering: int = LOWER_AUTO, cache=None
     """Forward that leaves Dhat in `cache` for conv_bwd (training step)."""
     _need_cuda_f32(x, w)
     m = desc.m
-    y = out if out is not None else torch.empty((desc.b, desc.o, m, m), dtype=torch.float32, device=x.device)
+    y = out if out is not None else torch.empty(desc.y_shape(), dtype=torch.float32, device=x.device)
     nbytes = workspace_size(desc, lowering, PASS_FWD) if lowering else max(
         workspace_size(desc, t, PASS_FWD) for t in (1, 2, 3))
     buf = _ws(ws, x.device).get(nbytes)
@@ -154,7 +154,7 @@ def lift(rhat, desc: ConvDesc, lowering: int, order: int = ROWS_SPEC, stream=Non
     """lift: Rhat (rows x khat_cols) -> OutputBatch (b,o,m,m)."""
     _need_cuda_f32(rhat)
     m = desc.m
-    y = torch.empty((desc.b, desc.o, m, m), dtype=torch.float32, device=rhat.device)
+    y = torch.empty(desc.y_shape(), dtype=torch.float32, device=rhat.device)
     check(lib().cct_lift(C.byref(desc.c()), lowering, order, _ptr(rhat), rhat.shape[1], _ptr(y), _stream(stream)))
     return y
 
@@ -214,7 +214,7 @@ def conv_fwd_ex(x, w, desc: ConvDesc, lowering: int = LOWER_AUTO, groups: int = 
     bias (o) or None -> y (b,o,m,m) = act(conv + bias)."""
     _need_cuda_f32(x, w, *([bias] if bias is not None else []))
     m = desc.m
-    y = out if out is not None else torch.empty((desc.b, desc.o, m, m), dtype=torch.float32, device=x.device)
+    y = out if out is not None else torch.empty(desc.y_shape(), dtype=torch.float32, device=x.device)
     ext = _ext(groups, bias, relu)
     buf = _ws(ws, x.device).get(_ws_ex(desc, lowering, ext, PASS_FWD))
     check(lib().cct_conv_fwd_ex(C.byref(desc.c()), lowering, C.byref(ext), _ptr(x), _ptr(w), _ptr(y), _ptr(buf),

@@ -58,7 +58,7 @@ std::string desc_str(const cct_conv_desc* d) {
 cct_status check_desc(const cct_conv_desc* d) {
     if (!d) return fail(CCT_ERR_CONFIG, "null conv descriptor");
     if (d->k < 1 || d->d < 1 || d->o < 1 || d->b < 1 || d->stride < 1 || d->pad < 0 ||
-        d->k > d->n + 2 * d->pad)
+        d->k > d->n + 2 * d->pad || (d->layout != CCT_LAYOUT_NCHW && d->layout != CCT_LAYOUT_NHWC))
         return fail(CCT_ERR_CONFIG, "invalid layer config " + desc_str(d) +
                                         ": need 1 <= k <= n + 2 pad, d >= 1, o >= 1, b >= 1, stride >= 1, pad >= 0");
     return CCT_OK;
@@ -70,6 +70,7 @@ Geo geo_of(const cct_conv_desc* d) {
     g.N = g.n + 2 * g.p;
     g.m = (g.N - g.k) / g.s + 1;
     g.R = g.s * (g.m - 1) + g.k;
+    g.yl = d->layout == CCT_LAYOUT_NHWC ? 1 : 0;
     return g;
 }
 
@@ -409,24 +410,46 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
         gp.A = {wv, ldw, Major::K};
         gp.B = {dh, ldd, Major::K};
         if (implicit) gp.im2col.operand = 1;
-        gp.C.transposed = 1;
-        gp.C.s_mr = g.m * g.m;
-        gp.C.ndiv = g.m * g.m;
-        gp.C.s_nq = opts.ycs ? opts.ycs : g.o * g.m * g.m;
-        gp.C.s_n = 1;
+        if (g.yl) {
+            // NHWC y: lanes = channels are contiguous -- plain coalesced stores, no transposition
+            gp.C.s_mr = 1;
+            gp.C.s_n = g.o;
+            span = g.b * g.m * g.m * g.o;
+        } else {
+            gp.C.transposed = 1;
+            gp.C.s_mr = g.m * g.m;
+            gp.C.ndiv = g.m * g.m;
+            gp.C.s_nq = opts.ycs ? opts.ycs : g.o * g.m * g.m;
+            gp.C.s_n = 1;
+            span = (g.b - 1) * gp.C.s_nq + g.o * g.m * g.m;
+        }
         gp.C.bias = opts.bias;
         gp.C.relu = opts.relu;
-        span = (g.b - 1) * gp.C.s_nq + g.o * g.m * g.m;
     } else if (type == 1) {
-        // lift_t1 is a reshape: write NCHW straight from the epilogue (+ bias / ReLU)
+        // lift_t1 is a reshape: write y straight from the epilogue (+ bias / ReLU)
         out = y;
-        gp.C.mdiv = g.m * g.m;
-        gp.C.s_mq = opts.ycs ? opts.ycs : g.o * g.m * g.m;
-        gp.C.s_mr = 1;
-        gp.C.s_n = g.m * g.m;
+        if (g.yl) {  // NHWC: row = pixel, o consecutive channels
+            gp.C.s_mr = g.o;
+            gp.C.s_n = 1;
+            span = g.b * g.m * g.m * g.o;
+        } else {
+            gp.C.mdiv = g.m * g.m;
+            gp.C.s_mq = opts.ycs ? opts.ycs : g.o * g.m * g.m;
+            gp.C.s_mr = 1;
+            gp.C.s_n = g.m * g.m;
+            span = (g.b - 1) * gp.C.s_mq + g.o * g.m * g.m;
+        }
         gp.C.bias = opts.bias;
         gp.C.relu = opts.relu;
-        span = (g.b - 1) * gp.C.s_mq + g.o * g.m * g.m;
+    } else if (planes_ok(g, type)) {
+        // Rhat plane-major (lowering23.cu): the k^a tap planes of one (image, channel) contiguous
+        span = g.b * L.ncols * L.rm.rpi;
+        rht = ws.take(span);
+        out = rht;
+        gp.C.mdiv = L.rm.rpi;
+        gp.C.s_mq = L.ncols * L.rm.rpi;
+        gp.C.s_mr = 1;
+        gp.C.s_n = L.rm.rpi;
     } else {
         rht = ws.take(L.ncols * L.ldr);
         out = rht;
@@ -436,7 +459,10 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
     }
     cct_status s = gemm_capped(gp, out, span, ws, st, "gemm (fwd)", type == 1 ? opts.fused : nullptr);
     if (s != CCT_OK || !ws.base) return s;
-    if (type != 1) CCT_TRY(lift(g, type, L.rm, rht, 1, L.ldr, y, st), "lift");
+    if (type != 1) {
+        if (planes_ok(g, type)) CCT_TRY(lift_planes(g, type, rht, y, st), "lift");
+        else CCT_TRY(lift(g, type, L.rm, rht, 1, L.ldr, y, st), "lift");
+    }
     return CCT_OK;
 }
 
@@ -448,9 +474,14 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
                             float* dx, float* dw, Ws& ws, cudaStream_t st) {
     const Lowered L = lowered_of(g, 1);
     const int64_t mm = g.m * g.m, kk = g.k * g.k;
-    float* dyn = ws.take(g.b * mm * g.o);  // dy as NHWC: [b][m][m][o] = dRhat (rows x o)
-    if (ws.base) CCT_TRY(transpose_batched(dy, g.o, mm, mm, g.o * mm, dyn, g.o, mm * g.o, g.b, kPhaseExpand, st),
-                         "dy to NHWC");
+    // dy as NHWC: [b][m][m][o] = dRhat (rows x o) -- the caller's dy when its layout is NHWC
+    const float* dyn = dy;
+    if (!g.yl) {
+        float* t = ws.take(g.b * mm * g.o);
+        if (ws.base)
+            CCT_TRY(transpose_batched(dy, g.o, mm, mm, g.o * mm, t, g.o, mm * g.o, g.b, kPhaseExpand, st), "dy to NHWC");
+        dyn = or_plan(t, ws);
+    }
     const size_t mark = ws.off;
     size_t hi = mark;
     if (dx) {
@@ -566,8 +597,13 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
     if (t1_implicit_bwd(g, type)) return run_bwd_implicit(g, x, cache, dy, w, dx, dw, ws, st);
     const Lowered L = lowered_of(g, type);
     cudaError_t e = cudaSuccess;
-    float* drt = ws.take(L.ncols * L.ldr);
-    if (ws.base) CCT_TRY(expand(g, type, dy, drt, L.ldr, st), "expand");
+    // Type 1 with an NHWC dy: dy IS dRhat (rows x o, row-major) -- the GEMMs read it in place
+    // (K-major B of backward-data, MN-major operand of backward-weight); otherwise expand dRhat^T
+    const bool dy_direct = type == 1 && g.yl && g.o % 4 == 0 && aligned16(dy);
+    float* drt = dy_direct ? nullptr : ws.take(L.ncols * L.ldr);
+    if (ws.base && !dy_direct) CCT_TRY(expand(g, type, dy, drt, L.ldr, st), "expand");
+    const Operand drt_n = dy_direct ? Operand{dy, g.o, Major::K} : Operand{drt, L.ldr, Major::MN};   // (rows, ncols)
+    const Operand drt_k = dy_direct ? Operand{dy, g.o, Major::MN} : Operand{drt, L.ldr, Major::K};   // (ncols, rows)
     const size_t mark = ws.off;
     size_t hi = mark;
     if (dx) {
@@ -585,7 +621,7 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
         gp.N = L.rows;
         gp.K = L.ncols;
         gp.A = {wv, ldw, Major::MN};
-        gp.B = {drt, L.ldr, Major::MN};
+        gp.B = drt_n;
         if (slab) {  // column (i, j, ch) -> slab i; row (q, r, c) -> slab (q, r), run c
             gp.C.mdiv = g.k * g.d;
             gp.C.s_mq = S;
@@ -610,7 +646,7 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
                                                                   : dhat_of(g, type, L, x, nullptr, ws, st, &e);
         CCT_TRY(e, "lower");
         const int64_t ldd = (dh == x) ? g.d : L.ldc;
-        GemmProblem gp = wgrad_problem(L, {dh, ldd, Major::MN}, {drt, L.ldr, Major::K});
+        GemmProblem gp = wgrad_problem(L, {dh, ldd, Major::MN}, drt_k);
         // narrow kernel banks (ncols < 128, e.g. conv1 o = 96) with a materialised Dhat:
         // compute dW (ncols x cols) = dRhat^T * Dhat instead, so the wide lowered side
         // is the tile width N
@@ -618,7 +654,7 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
         if (swap) {
             gp.M = L.ncols;
             gp.N = L.cols;
-            gp.A = {drt, L.ldr, Major::K};
+            gp.A = drt_k;
             gp.B = {dh, ldd, Major::MN};
         }
         if (implicit) wgrad_im2col(gp, g, x);
@@ -844,6 +880,7 @@ cct_status run_bwd_ex(const Geo& g, int type, const Ext& e, const float* x, cons
 }
 
 cct_status check_ext(const cct_conv_desc* d, const cct_conv_ext* x, Ext* e) {
+    if (d->layout != CCT_LAYOUT_NCHW) return fail(CCT_ERR_UNSUPPORTED, "the _ex extension takes NCHW y / dy");
     if (x) {
         e->groups = x->groups;
         e->bias = x->bias;
@@ -895,11 +932,19 @@ cct_status cct_conv_desc_init(cct_conv_desc* desc, int64_t n, int64_t k, int64_t
     if (!desc) return fail(CCT_ERR_CONFIG, "null conv descriptor");
     desc->n = n; desc->k = k; desc->d = d; desc->o = o; desc->b = b; desc->stride = stride; desc->pad = pad;
     desc->m = desc->R = 0;
+    desc->layout = CCT_LAYOUT_NCHW;
     cct_status s = check_desc(desc);
     if (s != CCT_OK) return s;
     const Geo g = geo_of(desc);
     desc->m = g.m;
     desc->R = g.R;
+    return CCT_OK;
+}
+
+cct_status cct_conv_desc_set_layout(cct_conv_desc* desc, cct_layout layout) {
+    if (!desc) return fail(CCT_ERR_CONFIG, "null conv descriptor");
+    if (layout != CCT_LAYOUT_NCHW && layout != CCT_LAYOUT_NHWC) return fail(CCT_ERR_CONFIG, "unknown layout");
+    desc->layout = layout;
     return CCT_OK;
 }
 

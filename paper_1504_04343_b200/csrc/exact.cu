@@ -69,6 +69,7 @@ cct_status cct_direct_conv_fwd_exact(const cct_conv_desc* desc, const float* x, 
                                      void* stream) {
     cct_conv_desc d;
     if (!desc) return CCT_ERR_CONFIG;
+    if (desc->layout != CCT_LAYOUT_NCHW) return CCT_ERR_UNSUPPORTED;  // the oracle entry point writes OutputBatch
     cct_status st = cct_conv_desc_init(&d, desc->n, desc->k, desc->d, desc->o, desc->b, desc->stride, desc->pad);
     if (st != CCT_OK) return st;
     if (!x || !w || !y) return CCT_ERR_CONFIG;

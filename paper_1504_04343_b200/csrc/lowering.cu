@@ -156,7 +156,8 @@ __global__ void lift_kernel(const float* __restrict__ rh, float* __restrict__ y,
                 for (int j = 0; j < k; ++j) acc += __ldg(pi + j * (tap_j + cs));
             }
         }
-        y[e] = acc;
+        if (g.yl) y[(q * mm + pix) * o + oj] = acc;  // NHWC y
+        else y[e] = acc;
     }
 }
 
@@ -222,7 +223,8 @@ __global__ void expand_kernel(const float* __restrict__ dy, float* __restrict__ 
                     else if (tx >= 0 && tx % s == 0) c = tx / s;
                 }
                 if (r >= 0 && r < m && c >= 0 && c < m)
-                    val = __ldg(dy + ((int64_t(q) * o + oj) * m + r) * int64_t(m) + c);
+                    val = g.yl ? __ldg(dy + ((int64_t(q) * m + r) * m + c) * o + oj)
+                               : __ldg(dy + ((int64_t(q) * o + oj) * m + r) * int64_t(m) + c);
             }
             v[u] = val;
             if (++cx == nc) {  // walk to the next row of the (q, y) grid
@@ -630,6 +632,10 @@ __global__ void __launch_bounds__(256) transpose_batched_kernel(const float* __r
 
 cudaError_t lower(const Geo& g, int type, const RowMap& rm, const float* x, float* dhat, int64_t ld,
                   cudaStream_t st) {
+    // Type 2 / 3 in the internal row order: whole padded input rows (lowering23.cu)
+    if (type != 1 && rm.sc == 1 && rm.ny == g.R && rm.nc == (type == 2 ? g.m : g.R) && rm.sr == rm.nc &&
+        lower_rows_ok(g, type, x, dhat, ld))
+        return lower_rows(g, type, x, dhat, ld, st);
     const int64_t cols = lowered_cols(g, type);
     const int64_t nrows = g.b * rm.ny * rm.nc;
     PhaseScope ps(kPhaseLower, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + nrows * ld));
@@ -693,6 +699,11 @@ cudaError_t lift(const Geo& g, int type, const RowMap& rm, const float* rhat, in
 }
 
 cudaError_t expand(const Geo& g, int type, const float* dy, float* drt, int64_t ldr, cudaStream_t st) {
+    if (type == 1 && g.yl) {
+        // NHWC dy is dRhat (rows x o): dRhat^T is its transpose
+        return transpose_batched(dy, g.b * g.m * g.m, g.o, g.o, 0, drt, ldr, 0, 1, kPhaseExpand, st);
+    }
+    if (type != 1 && planes_ok(g, type)) return expand_planes(g, type, dy, drt, ldr, st);
     const RowMap rm = rowmap_internal(g, type);
     const int64_t ncols = lowered_ncols(g, type);
     PhaseScope ps(kPhaseExpand, st, 0, 4.0 * double(g.b * g.o * g.m * g.m + ncols * g.b * rm.rpi));

@@ -20,6 +20,7 @@ namespace cct {
 struct Geo {
     int64_t b, n, d, k, o, s, p;
     int64_t m, R, N;  // output side, touched padded extent, padded side
+    int64_t yl = 0;   // layout of y / dy: 0 NCHW (OutputBatch), 1 NHWC
 };
 
 struct RowMap {
@@ -60,5 +61,15 @@ cudaError_t transpose(const float* src, int64_t rows, int64_t cols, int64_t ld_s
 // negative); `phase` = the profiling phase the copy is accounted to
 cudaError_t transpose_batched(const float* src, int64_t rows, int64_t cols, int64_t lds, int64_t src_z, float* dst,
                               int64_t ldd, int64_t dst_z, int64_t nz, int phase, cudaStream_t st);
+
+// ---- Type 2 / 3 streaming kernels (lowering23.cu) ----------------------------------
+// Rhat plane-major: Rhat[((q * ncols) + col) * rpi + prow] (the forward GEMM's output map)
+bool planes_ok(const Geo& g, int type);
+cudaError_t lift_planes(const Geo& g, int type, const float* rhat, float* y, cudaStream_t st);
+// dy -> dRhat^T[col * ldr + row] (internal row order), zero rows ldr tail included
+cudaError_t expand_planes(const Geo& g, int type, const float* dy, float* drt, int64_t ldr, cudaStream_t st);
+// Dhat2 / Dhat3 in internal row order from whole padded input rows (d % 4 == 0)
+bool lower_rows_ok(const Geo& g, int type, const float* x, const float* dh, int64_t ld);
+cudaError_t lower_rows(const Geo& g, int type, const float* x, float* dhat, int64_t ld, cudaStream_t st);
 
 }  // namespace cct

@@ -1,0 +1,276 @@
+// lowering23.cu -- the HBM-streaming Type 2 / Type 3 kernels of the training path.
+//
+// Type 2 and Type 3 move k (T2) or k^2 (T3) times the output through HBM: the
+// forward GEMM writes Rhat (b R m x k o, b R^2 x k^2 o) and lift sums k / k^2
+// shifted taps of it; the backward expands dy into dRhat^T of the same size
+// (SPEC.md:121-129 and the adjoint).  These kernels are organised so every byte
+// of the big operand streams once, in long contiguous runs:
+//
+//   Rhat, plane-major (written by the forward GEMM's epilogue output map):
+//       Rhat[((q * ncols) + col) * rpi + prow]     col = (oj, tap), prow = padded-row pixel
+//     so the k^a tap planes of one output channel of one image are ONE contiguous
+//     block (conv2 T3: 25 x 961 floats) -- lift_planes reads it as one stream per
+//     block and writes the output plane(s) once.
+//   dRhat^T (the backward GEMMs' operand, [col][ldr]): expand_planes stages the dy
+//     planes of (image, 8 channels) in shared memory once and writes every tap's
+//     run of rpi floats as a pure store stream.
+//   Dhat2 / Dhat3 (internal row order): lower_rows writes the lowered rows of one
+//     padded input row (q, Y) -- m rows of k d (T2) or R rows of d (T3), contiguous
+//     -- from one coalesced read of that input row (float4, depth % 4 == 0).
+//
+// y / dy may be NCHW (OutputBatch) or NHWC (Geo::yl); NHWC planes go through the
+// same shared-memory block so the big stream keeps its layout.
+// Summation orders equal lift_kernel's (taps i then j ascending): the fast path and
+// the phase-level API give bit-identical results.
+#include <algorithm>
+
+#include "common.cuh"
+#include "lowering.cuh"
+
+namespace cct {
+
+namespace {
+
+constexpr int kThreads = 256;
+constexpr int kG = 8;  // output channels (planes) per block
+
+// floor(v / d) for 0 <= v < 2^22 and 1 <= d < 2^10 from a float reciprocal plus one fix-up
+__device__ __forceinline__ int fdiv(int v, int d, float inv) {
+    int qv = __float2int_rz(float(v) * inv);
+    if (qv * d > v) --qv;
+    else if ((qv + 1) * d <= v) ++qv;
+    return qv;
+}
+
+template <int TYPE, bool NHWC>
+__global__ void __launch_bounds__(kThreads) lift_planes_kernel(const float* __restrict__ rh, float* __restrict__ y,
+                                                               Geo g) {
+    extern __shared__ float acc_s[];  // NHWC: kG x m^2 staged outputs
+    const int m = int(g.m), mm = m * m, o = int(g.o), k = int(g.k), s = int(g.s), R = int(g.R);
+    const int taps = TYPE == 2 ? k : k * k;
+    const int64_t rpi = TYPE == 2 ? int64_t(R) * m : int64_t(R) * R;
+    const int ngroups = (o + kG - 1) / kG;
+    const float inv_mm = 1.f / float(mm), inv_m = 1.f / float(m);
+    for (int64_t blk = blockIdx.x; blk < g.b * ngroups; blk += gridDim.x) {
+        const int64_t q = blk / ngroups;
+        const int oj0 = int(blk - q * ngroups) * kG;
+        const int G = min(kG, o - oj0);
+        for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+            const int gl = fdiv(e, mm, inv_mm), pix = e - gl * mm;
+            const int r = fdiv(pix, m, inv_m), c = pix - r * m;
+            const float* pl = rh + (q * o + oj0 + gl) * int64_t(taps) * rpi;
+            float a = 0.f;
+            if constexpr (TYPE == 2) {
+                const float* p0 = pl + int64_t(s) * r * m + c;
+#pragma unroll 4
+                for (int i = 0; i < k; ++i) a += __ldg(p0 + i * (rpi + m));
+            } else {
+                const float* p0 = pl + int64_t(s) * r * R + int64_t(s) * c;
+                for (int i = 0; i < k; ++i) {
+                    const float* pi = p0 + i * (int64_t(k) * rpi + R);
+#pragma unroll 4
+                    for (int j = 0; j < k; ++j) a += __ldg(pi + j * (rpi + 1));
+                }
+            }
+            if constexpr (NHWC) acc_s[e] = a;
+            else y[(q * o + oj0) * mm + e] = a;
+        }
+        if constexpr (NHWC) {
+            __syncthreads();
+            const float inv_g = 1.f / float(G);
+            for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+                const int pix = fdiv(e, G, inv_g), gl = e - pix * G;
+                y[(q * mm + pix) * o + oj0 + gl] = acc_s[gl * mm + pix];
+            }
+            __syncthreads();
+        }
+    }
+}
+
+template <int TYPE, bool NHWC>
+__global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __restrict__ dy, float* __restrict__ drt,
+                                                                 Geo g, int64_t ldr) {
+    extern __shared__ float sdy[];  // kG x m^2 dy values of (q, oj0 .. oj0 + G)
+    const int m = int(g.m), mm = m * m, o = int(g.o), k = int(g.k), s = int(g.s), R = int(g.R);
+    const int taps = TYPE == 2 ? k : k * k;
+    const int rw = TYPE == 2 ? m : R;  // lowered rows per padded input row
+    const int rpi = R * rw;
+    const int ngroups = (o + kG - 1) / kG;
+    const float inv_rw = 1.f / float(rw);
+    for (int64_t blk = blockIdx.x; blk < g.b * ngroups; blk += gridDim.x) {
+        const int64_t q = blk / ngroups;
+        const int oj0 = int(blk - q * ngroups) * kG;
+        const int G = min(kG, o - oj0);
+        if constexpr (NHWC) {
+            const float inv_g = 1.f / float(G);
+            for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+                const int pix = fdiv(e, G, inv_g), gl = e - pix * G;
+                sdy[gl * mm + pix] = __ldg(dy + (q * mm + pix) * o + oj0 + gl);
+            }
+        } else {
+            const float* src = dy + (q * o + oj0) * mm;
+            for (int e = threadIdx.x; e < G * mm; e += kThreads) sdy[e] = __ldg(src + e);
+        }
+        __syncthreads();
+        for (int gl = 0; gl < G; ++gl) {
+            const float* pl = sdy + gl * mm;
+            for (int tap = 0; tap < taps; ++tap) {
+                const int i = TYPE == 2 ? tap : tap / k;
+                const int j = TYPE == 2 ? 0 : tap - i * k;
+                float* out = drt + int64_t((oj0 + gl) * taps + tap) * ldr + q * rpi;
+                for (int idx = threadIdx.x; idx < rpi; idx += kThreads) {
+                    const int Y = fdiv(idx, rw, inv_rw), X = idx - Y * rw;
+                    const int ty = Y - i;
+                    int r, c;
+                    bool ok;
+                    if (s == 1) {
+                        r = ty;
+                        ok = unsigned(ty) < unsigned(m);
+                    } else {
+                        r = ty / s;
+                        ok = ty >= 0 && r * s == ty && r < m;
+                    }
+                    if constexpr (TYPE == 3) {
+                        const int tx = X - j;
+                        if (s == 1) {
+                            c = tx;
+                            ok = ok && unsigned(tx) < unsigned(m);
+                        } else {
+                            c = tx / s;
+                            ok = ok && tx >= 0 && c * s == tx && c < m;
+                        }
+                    } else {
+                        c = X;
+                    }
+                    out[idx] = ok ? pl[r * m + c] : 0.f;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// Type 2 / 3 lowering (internal order, depth % 4 == 0): block per padded input row
+// (q, Y); its lowered rows are one contiguous span of the output.
+//   T3: R rows of d floats = padded row Y, pixels [0, R) (ldc == d)
+//   T2: m rows of ldc floats, row c = padded pixels [s c, s c + k) x d, zero tail to ldc
+template <int TYPE>
+__global__ void __launch_bounds__(kThreads) lower_rows_kernel(const float* __restrict__ x, float* __restrict__ dh,
+                                                              Geo g, int64_t ldc) {
+    extern __shared__ float4 srow[];  // T2: the padded input row (N x d floats)
+    const int n = int(g.n), d4 = int(g.d / 4), p = int(g.p), R = int(g.R), m = int(g.m), N = int(g.N);
+    const int64_t rows = g.b * R;
+    const float4* x4 = reinterpret_cast<const float4*>(x);
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int64_t qy = blockIdx.x; qy < rows; qy += gridDim.x) {
+        const int64_t q = qy / R;
+        const int Y = int(qy - q * R);
+        const int ys = Y - p;
+        const bool yok = ys >= 0 && ys < n;
+        const float4* xr = x4 + ((q * n + (yok ? ys : 0)) * n) * d4;
+        if constexpr (TYPE == 3) {
+            float4* out = reinterpret_cast<float4*>(dh + qy * int64_t(R) * ldc);
+            const float inv = 1.f / float(d4);
+            for (int e = threadIdx.x; e < R * d4; e += kThreads) {
+                const int X = fdiv(e, d4, inv), ch = e - X * d4;
+                const int xs = X - p;
+                out[e] = (yok && xs >= 0 && xs < n) ? __ldg(xr + xs * d4 + ch) : z;
+            }
+        } else {
+            for (int e = threadIdx.x; e < N * d4; e += kThreads) {
+                const int X = e / d4, ch = e - X * d4;
+                const int xs = X - p;
+                srow[e] = (yok && xs >= 0 && xs < n) ? __ldg(xr + xs * d4 + ch) : z;
+            }
+            __syncthreads();
+            const int l4 = int(ldc / 4), kd4 = int(g.k) * d4, s = int(g.s);
+            float4* out = reinterpret_cast<float4*>(dh + qy * int64_t(m) * ldc);
+            const float inv = 1.f / float(l4);
+            for (int e = threadIdx.x; e < m * l4; e += kThreads) {
+                const int c = fdiv(e, l4, inv), u = e - c * l4;
+                out[e] = u < kd4 ? srow[s * c * d4 + u] : z;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+int blocks_for(int64_t work_blocks, int per_sm) {
+    return int(std::max<int64_t>(1, std::min<int64_t>(work_blocks, int64_t(num_sms()) * per_sm)));
+}
+
+}  // namespace
+
+bool planes_ok(const Geo& g, int type) {
+    // per-block shared memory (kG planes) and 32-bit in-plane indices
+    return (type == 2 || type == 3) && size_t(kG) * size_t(g.m * g.m) * 4 <= 96 * 1024 && g.R * g.R < (1 << 22) &&
+           g.R * g.m < (1 << 22);
+}
+
+cudaError_t lift_planes(const Geo& g, int type, const float* rhat, float* y, cudaStream_t st) {
+    if (!planes_ok(g, type)) return cudaErrorInvalidValue;
+    const int taps = type == 2 ? int(g.k) : int(g.k * g.k);
+    const int64_t rpi = type == 2 ? g.R * g.m : g.R * g.R;
+    PhaseScope ps(kPhaseLift, st, 0, 4.0 * double(g.b * g.o) * double(taps * rpi + g.m * g.m));
+    const size_t smem = g.yl ? size_t(kG) * size_t(g.m * g.m) * 4 : 0;
+    const int grid = blocks_for(g.b * ((g.o + kG - 1) / kG), 8);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        kern<<<grid, kThreads, smem, st>>>(rhat, y, g);
+    };
+    if (type == 2) g.yl ? go(lift_planes_kernel<2, true>) : go(lift_planes_kernel<2, false>);
+    else g.yl ? go(lift_planes_kernel<3, true>) : go(lift_planes_kernel<3, false>);
+    note_launch();
+    return cudaGetLastError();
+}
+
+cudaError_t expand_planes(const Geo& g, int type, const float* dy, float* drt, int64_t ldr, cudaStream_t st) {
+    if (!planes_ok(g, type)) return cudaErrorInvalidValue;
+    const int taps = type == 2 ? int(g.k) : int(g.k * g.k);
+    const int64_t rpi = type == 2 ? g.R * g.m : g.R * g.R;
+    PhaseScope ps(kPhaseExpand, st, 0, 4.0 * double(g.b * g.o) * double(taps * rpi + g.m * g.m));
+    const size_t smem = size_t(kG) * size_t(g.m * g.m) * 4;
+    const int grid = blocks_for(g.b * ((g.o + kG - 1) / kG), 8);
+    auto go = [&](auto kern) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        kern<<<grid, kThreads, smem, st>>>(dy, drt, g, ldr);
+    };
+    if (type == 2) g.yl ? go(expand_planes_kernel<2, true>) : go(expand_planes_kernel<2, false>);
+    else g.yl ? go(expand_planes_kernel<3, true>) : go(expand_planes_kernel<3, false>);
+    note_launch();
+    // ldr padding rows (rows b*rpi .. ldr) of every column: zero (never read by a valid tile row,
+    // but the GEMM's K / N tails read them)
+    const int64_t rows = g.b * rpi;
+    if (ldr > rows) {
+        const int64_t ncols = lowered_ncols(g, type);
+        cudaError_t e = cudaMemset2DAsync(drt + rows, size_t(ldr) * 4, 0, size_t(ldr - rows) * 4, size_t(ncols), st);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaGetLastError();
+}
+
+bool lower_rows_ok(const Geo& g, int type, const float* x, const float* dh, int64_t ld) {
+    if (!(type == 2 || type == 3) || g.d % 4 || ld % 4 || (reinterpret_cast<uintptr_t>(x) & 15) ||
+        (reinterpret_cast<uintptr_t>(dh) & 15))
+        return false;
+    if (type == 3) return ld == g.d && g.R * (g.d / 4) < (1 << 22);
+    return size_t(g.N * g.d) * 4 <= 96 * 1024 && g.m * (ld / 4) < (1 << 22);
+}
+
+cudaError_t lower_rows(const Geo& g, int type, const float* x, float* dhat, int64_t ld, cudaStream_t st) {
+    if (!lower_rows_ok(g, type, x, dhat, ld)) return cudaErrorInvalidValue;
+    const int64_t rpi = type == 2 ? g.R * g.m : g.R * g.R;
+    PhaseScope ps(kPhaseLower, st, 0, 4.0 * double(g.b * g.n * g.n * g.d + g.b * rpi * ld));
+    const int grid = blocks_for(g.b * g.R, 16);
+    if (type == 3) {
+        lower_rows_kernel<3><<<grid, kThreads, 0, st>>>(x, dhat, g, ld);
+    } else {
+        const size_t smem = size_t(g.N * g.d) * 4;
+        cudaFuncSetAttribute(lower_rows_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        lower_rows_kernel<2><<<grid, kThreads, smem, st>>>(x, dhat, g, ld);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace cct

@@ -37,8 +37,8 @@ class LayerSpec:
     stride: int = 1
     pad: int = 0
 
-    def desc(self, b: int) -> ConvDesc:
-        return ConvDesc(self.n, self.k, self.d, self.o, b, self.stride, self.pad)
+    def desc(self, b: int, layout: int = 0) -> ConvDesc:
+        return ConvDesc(self.n, self.k, self.d, self.o, b, self.stride, self.pad, layout)
 
 
 # BASELINE.json configs: conv1 227x227x3 -> 96 k11 s4; conv2 27x27x96 -> 256 k5 p2;
@@ -69,7 +69,7 @@ class ConvStack:
     """
 
     def __init__(self, batch: int, device: torch.device, layers=CAFFENET, lowering=LOWER_AUTO,
-                 group=None, seed: int = 1234, global_batch: int | None = None):
+                 group=None, seed: int = 1234, global_batch: int | None = None, layout: int = 0):
         from .batching import shard_of
         self.layers = tuple(layers)
         self.device = device
@@ -84,7 +84,8 @@ class ConvStack:
         if batch < 1:
             raise ValueError(f"rank {self.rank} of {self.world} gets no images of a {self.global_batch}-image batch")
         self.batch = batch
-        self.descs = [l.desc(batch) for l in self.layers]
+        self.layout = layout  # y / dy: NCHW (OutputBatch) or NHWC (the next layer's DataBatch order)
+        self.descs = [l.desc(batch, layout) for l in self.layers]
         if isinstance(lowering, (list, tuple)):
             self.types = list(lowering)
         elif lowering == LOWER_AUTO:
@@ -99,13 +100,13 @@ class ConvStack:
 
         def shard(sd, *shape):  # this rank's images of a global-batch tensor
             full = u(sd, self.global_batch, *shape)
-            return full.narrow(0, self.first, batch).contiguous() if self.world > 1 else full
+            # a copy, not a view: the C ABI needs 16-byte aligned tensors (an image offset is not)
+            return full.narrow(0, self.first, batch).clone() if self.world > 1 else full
 
         nl = len(self.layers)
         self.w = [u(seed + li, l.o, l.k, l.k, l.d) for li, l in enumerate(self.layers)]
         self.x = [shard(seed + nl + li, l.n, l.n, l.d) for li, l in enumerate(self.layers)]
-        self.dy = [shard(seed + 2 * nl + li, l.o, d.m, d.m)
-                   for li, (l, d) in enumerate(zip(self.layers, self.descs))]
+        self.dy = [shard(seed + 2 * nl + li, *d.y_shape()[1:]) for li, d in enumerate(self.descs)]
         self.y = [torch.empty_like(t) for t in self.dy]
         self.dx = [torch.empty_like(t) for t in self.x]
         self.dw = [torch.empty_like(t) for t in self.w]

@@ -111,9 +111,10 @@ def _rel(a, b):
 @pytest.mark.parametrize("gb", [6, 7])
 def test_convstack_two_ranks_match_full_batch(gb):
     """The all-reduced dW of two ConvStack ranks (CaffeNet conv1-5, global batch split
-    3/3 or 4/3) equals the single-rank full-batch dW (rel-L2 <= 1e-6: only the
-    summation order differs), identical on both ranks; each rank's y / dx are its
-    slice of the full-batch y / dx."""
+    3/3 or 4/3) equals the single-rank full-batch dW up to the summation order (rel-L2
+    <= 1e-5; conv1's 18k-term reduction differs by ~4e-6) and is identical on both
+    ranks; each rank's y / dx are its slice of the full-batch y / dx; and both dW agree
+    with fp64 torch (<= 1e-4, the north-star bar)."""
     from paper_1504_04343_b200.stack import CAFFENET, ConvStack
     mgr = mp.Manager()
     out = mgr.dict()
@@ -124,10 +125,14 @@ def test_convstack_two_ranks_match_full_batch(gb):
     torch.cuda.synchronize()
     assert (out[0]["first"], out[0]["batch"], out[1]["first"], out[1]["batch"]) == (0, (gb + 1) // 2, (gb + 1) // 2,
                                                                                       gb // 2)
-    for li in range(len(CAFFENET)):
+    for li, l in enumerate(CAFFENET):
         dwf = full.dw[li].cpu().numpy()
         assert np.array_equal(out[0]["dw"][li], out[1]["dw"][li])
-        assert _rel(out[0]["dw"][li], dwf) <= 1e-6, (li, _rel(out[0]["dw"][li], dwf))
-        for key, ref in (("y", full.y[li]), ("dx", full.dx[li])):
+        assert _rel(out[0]["dw"][li], dwf) <= 1e-5, (li, _rel(out[0]["dw"][li], dwf))
+        xd = full.x[li].double().permute(0, 3, 1, 2)
+        ref = torch.nn.grad.conv2d_weight(xd, (l.o, l.d, l.k, l.k), full.dy[li].double(), stride=l.stride,
+                                          padding=l.pad).permute(0, 2, 3, 1).cpu().numpy()
+        assert _rel(out[0]["dw"][li], ref) <= 1e-4 and _rel(dwf, ref) <= 1e-4
+        for key, r in (("y", full.y[li]), ("dx", full.dx[li])):
             got = np.concatenate([out[0][key][li], out[1][key][li]])
-            assert _rel(got, ref.cpu().numpy()) <= 1e-6, (key, li)
+            assert _rel(got, r.cpu().numpy()) <= 1e-5, (key, li)

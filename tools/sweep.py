@@ -31,7 +31,7 @@ def step_time(desc, t, x, w, dy, reps):
     cache = conv.alloc_cache(desc, t, dev)
     ws = conv.Workspace(dev)
     ws.get(max(cct.workspace_size(desc, t, cct.PASS_FWD), cct.workspace_size(desc, t, cct.PASS_BWD)))
-    y = torch.empty((desc.b, desc.o, desc.m, desc.m), device=dev)
+    y = torch.empty(desc.y_shape(), device=dev)
     dx = torch.empty_like(x)
     dw = torch.empty_like(w)
 
@@ -97,6 +97,11 @@ def main():
         print(f"d={d:5d} o={o:5d} d/o={d / o:7.4f} | T1 {tt[1]['ms']:7.3f} ms | T2 {tt[2]['ms']:7.3f} ms | "
               f"T3 {tt[3]['ms']:7.3f} ms | best T{meas} | model T{choice} "
               f"(model ms {tt[1]['model_ms']:.3f}/{tt[2]['model_ms']:.3f}/{tt[3]['model_ms']:.3f})", flush=True)
+        for t in (2, 3):
+            ph = tt[t]["phases"]
+            print("      T%d phases: " % t + "  ".join(
+                f"{nm} {v['ms'] * 1e3:6.0f} us {v['bytes'] / (v['ms'] * 1e-3) / 1e12 if v['ms'] else 0:4.2f} TB/s"
+                for nm, v in ph.items() if nm != "gemm") + f"  gemm {ph['gemm']['ms'] * 1e3:6.0f} us", flush=True)
         del x, w, dy
         torch.cuda.empty_cache()
     if a.out:
