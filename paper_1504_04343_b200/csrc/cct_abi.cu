@@ -22,6 +22,7 @@
 #include "reduce.cuh"
 #include "s2d.cuh"
 #include "epilogue.cuh"
+#include "gather.cuh"
 
 namespace cct {
 uint64_t launch_count();
@@ -179,6 +180,17 @@ bool t1_s2d(const Geo& g, int type) {
     return prefer_s2d(&d, t_pass);
 }
 
+// Small-channel Type 1 layers with d s % 4 == 0 (CaffeNet conv1) run fused: the lowered
+// matrix is gathered from staged input rows inside the GEMM (gather.cuh) -- no Dhat in
+// HBM, no separate lowering.  Takes precedence over the space-to-depth form (CCT_TUNE_GATHER
+// = 0 restores the earlier choices).
+bool t1_gather_fwd(const Geo& g, int type) {
+    return tuning(CCT_TUNE_GATHER) && implicit_enabled() && type == 1 && !im2col_ok(g.d, true) && gather_fwd_ok(g);
+}
+bool t1_gather_wgrad(const Geo& g, int type) {
+    return tuning(CCT_TUNE_GATHER) && implicit_enabled() && type == 1 && !im2col_ok(g.d, true) && gather_wgrad_ok(g);
+}
+
 // planning runs (no workspace) still need non-null, aligned operand pointers so
 // they follow the same decisions as the real call
 const float* kPlanPtr = reinterpret_cast<const float*>(uintptr_t(256));
@@ -189,6 +201,7 @@ T* or_plan(T* p, const Ws& ws) {
 
 // floats per image of the forward's lowered cache (the blocked input X' in s2d form)
 int64_t cache_per_image(const Geo& g, int type) {
+    if (t1_gather_fwd(g, type)) return 0;  // no Dhat: the backward gathers (or lowers) x itself
     if (t1_s2d(g, type)) {
         const Geo v = s2d_geo(g);
         return v.n * v.n * v.d;
@@ -367,6 +380,12 @@ cct_status run_fwd_one(const Geo& g, int type, const float* x, const float* w, f
     const bool strided = (opts.xcs && opts.xcs != g.d) || (opts.ycs && opts.ycs != g.o * g.m * g.m);
     if (strided && !(type == 1 && t1_implicit(g, type, x) && !t1_s2d(g, type)))
         return fail(CCT_ERR_UNSUPPORTED, "channel-group views need the implicit Type 1 path");
+    if (!strided && t1_gather_fwd(g, type) && aligned16(or_plan(x, ws))) {
+        float* w2 = ws.take(gather_fwd_ws_floats(g));
+        if (ws.base) CCT_TRY(gather_fwd(g, x, w, y, 0, opts.bias, opts.relu, w2, st), "fused gather forward");
+        if (opts.fused) *opts.fused = true;
+        return CCT_OK;
+    }
     if (t1_s2d(g, type)) {
         // blocked input (kept in the caller's lowered cache when given) and kernel bank
         const Geo v = s2d_geo(g);

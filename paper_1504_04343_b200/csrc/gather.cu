@@ -1,0 +1,580 @@
+// gather.cu -- fused small-channel Type 1 convolution: forward and backward-weight
+// without a materialised Dhat (see gather.cuh).
+//
+// Forward, one CTA per SM, persistent over 128-pixel tiles (a tile never crosses an
+// image), 768 threads:
+//   warp 0        TMA producer (one lane): kernel-bank k-blocks (big | small halves,
+//                 prepared once per call) -> smem ring stage s  [full / empty]
+//   warp 1        MMA issuer (one lane): per 16-wide k-block 6 x tcgen05.mma.kind::tf32,
+//                 A (the k-block of Dhat) from TMEM, B from smem
+//   warp 2        TMEM allocator, then the staging producer (one lane): the input rows a
+//                 tile touches -> a double-buffered row stage (1D bulk copies)  [xfull / xempty]
+//   warps 4-7     epilogue: tcgen05.ld -> y (NCHW: lanes = consecutive pixels, coalesced)
+//   warps 8-23    four gather groups (k-block gi -> group gi % 4): 128 pixels x 16 lowered columns
+//                 from the staged rows -> big / small -> tcgen05.st into TMEM A slot s
+// One barrier pair per ring position s covers both operands of a k-block: full[s] counts the
+// bank TMA (1 arrival + bytes) and the 4 gather warps, empty[s] is the MMA commit freeing the
+// bank stage and the A slot together (one wait and one commit per k-block on the MMA thread,
+// measured: the MMA issuer is the critical path of this narrow GEMM).
+// Lowered column order (this kernel's own; the kernel bank is repacked to match): filter
+// row i owns the window of columns [i segw, (i + 1) segw), its k d run placed at the shift
+// that makes every 4-column group of a k-block one aligned float4 of a staged row (the
+// float4 phase of an image's rows is uniform over the image since s d % 4 == 0): one
+// ld.shared.v4 per 4 lowered elements, no realignment (see variant_of).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "cct.h"
+#include "common.cuh"
+#include "gather.cuh"
+#include "ptx.cuh"
+
+namespace cct {
+namespace gth {
+
+constexpr int kGatherGroups = 4;            // gather groups of 4 warps, k-block gi -> group gi % 4
+constexpr int kThreads = 256 + 128 * kGatherGroups;
+constexpr int kTileM = 128;
+constexpr int kKB = 16;                   // k-block width (fp32 columns)
+constexpr int kSmemMax = 227 * 1024;      // opt-in dynamic shared memory per CTA
+constexpr int kMaxKGroups = 512;          // k-block groups of 4 columns in the table (K <= 2048)
+
+struct FwdParams {
+    const float* x;
+    float* y;
+    const float* bias;
+    int64_t y_sq, y_so, y_sp;  // y offset of (image q, channel o, pixel P)
+    int64_t x_total;           // floats in x (multiple of 4)
+    int b, n, d, k, s, p, m, o;
+    int seg, segw, kb_tile;    // lowered run per filter row, its window width, k-blocks per tile
+    int nvar;                  // kernel-bank variants (float4 phase of the image's rows, 1 or 4)
+    int tpi, tiles;            // tiles per image, total tiles
+    int pitch, lmargin;        // staged row slot: floats, and floats before the row data
+    int xr;                    // row slots per stage buffer
+    int stages;                // kernel-bank ring depth
+    int relu;
+};
+
+template <int NP>
+struct FwdCfg {
+    static constexpr int ACC_COLS = NP;                                // one accumulator buffer
+    static constexpr int A_COL = 2 * ACC_COLS;                         // double-buffered accumulators first
+    static constexpr int MAX_RING = (512 - A_COL) / 32 > 8 ? 8 : (512 - A_COL) / 32;  // A slots (big | small)
+    static constexpr uint32_t B_BYTES = NP * kKB * 4;                 // one half of a ring stage
+    static_assert(NP % 16 == 0 && NP <= 192, "tile width");
+};
+__host__ __device__ constexpr int max_ring(int np) { return (512 - 2 * np) / 32 > 8 ? 8 : (512 - 2 * np) / 32; }
+
+// dynamic smem layout (bytes): [ring stages][row stage x2][zero row][k tables][barriers]
+struct FwdLayout {
+    uint32_t ring, stage, zero, ktab, bars, total;
+};
+__host__ __device__ inline FwdLayout fwd_layout(int np, int stages, int xr, int pitch, int kgroups) {
+    FwdLayout L;
+    L.ring = 0;
+    L.stage = uint32_t(stages) * 2u * uint32_t(np) * kKB * 4u;
+    L.zero = L.stage + 2u * uint32_t(xr) * uint32_t(pitch) * 4u;
+    L.ktab = L.zero + uint32_t(pitch) * 4u;
+    L.bars = (L.ktab + 2u * 4u * uint32_t(kgroups) * 4u + 15u) & ~15u;  // ktab + etab, 4 variants
+    L.total = L.bars + uint32_t(2 * stages + 8) * 8u + 16u;
+    return L;
+}
+
+// Rows of image q start at float offset q n n d + y n d: their float4 phase is the same for
+// every output row of an image (s d % 4 == 0), (q n n d + (i - p) n d) mod 4 for filter row i.
+// The kernel bank is prepared in one variant per phase q n n d mod 4, each filter row's run
+// shifted inside its window so that every 4-column group is an aligned float4 of the stage.
+__host__ __device__ inline int variant_of(const FwdParams& p, int q) {
+    return p.nvar == 1 ? 0 : int((int64_t(q) * p.n * p.n * p.d) & 3);
+}
+// shift of filter row i's run inside its window, for variant phi
+__host__ __device__ inline int run_shift(int phi, int i, int n, int d, int pad) {
+    const int64_t delta = (int64_t(phi) + int64_t(i - pad) * n * d) & 3;  // row phase
+    return int((delta - int64_t(pad) * d) & 3);
+}
+
+struct TileGeo {
+    int q, P0, P1, ra, y0, nrows;
+};
+__device__ __forceinline__ TileGeo tile_geo(const FwdParams& p, int T) {
+    TileGeo t;
+    t.q = T / p.tpi;
+    t.P0 = (T - t.q * p.tpi) * kTileM;
+    t.P1 = min(t.P0 + kTileM, p.m * p.m);
+    t.ra = t.P0 / p.m;
+    const int rb = (t.P1 - 1) / p.m;
+    t.y0 = p.s * t.ra - p.p;
+    t.nrows = p.s * (rb - t.ra) + p.k;
+    return t;
+}
+
+template <int NP>
+__global__ void __launch_bounds__(kThreads, 1)
+    conv_fwd_gather_kernel(const __grid_constant__ CUtensorMap tmB, const FwdParams p) {
+    using C_ = FwdCfg<NP>;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int ngroups_k = p.kb_tile * 4;
+    const int R = p.stages;  // k-block ring: kernel-bank stage s and TMEM A slot s move together
+    const FwdLayout L = fwd_layout(NP, R, p.xr, p.pitch, ngroups_k);
+    float* zero_row = reinterpret_cast<float*>(smem + L.zero);
+    int* ktab = reinterpret_cast<int*>(smem + L.ktab);   // [variant][group]: row | zero mask | byte offset
+    int* etab = ktab + 4 * ngroups_k;                      // [variant][group]: run element of the group's column 0
+    // full[s]: the bank TMA (1 arrival + bytes) and the 4 gather warps of the k-block (4 arrivals)
+    // empty[s]: the MMA commit that frees bank stage s and A slot s together
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* empty = full + R;
+    uint64_t* xfull = empty + R;
+    uint64_t* xempty = xfull + 2;
+    uint64_t* tfull = xempty + 2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    // zero the stage buffers (their margins are never written by the row copies) and the
+    // zero row; build the k-block tables: group g of k-block kb -> (filter row, offset)
+    {
+        float4* z = reinterpret_cast<float4*>(smem + L.stage);
+        const int n4 = int((L.ktab - L.stage) / 16);
+        for (int i = threadIdx.x; i < n4; i += kThreads) z[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int idx = threadIdx.x; idx < p.nvar * ngroups_k; idx += kThreads) {
+            const int phi = idx / ngroups_k, gx = idx - phi * ngroups_k;
+            const int kc = gx * 4;
+            int i = kc / p.segw;
+            const int u0 = kc - i * p.segw;  // window column of the group's first element
+            int zmask = 0xF, boff = 0, e0 = 0;
+            if (i < p.k) {
+                const int sh = run_shift(phi, i, p.n, p.d, p.p);
+                const int delta = int((int64_t(phi) + int64_t(i - p.p) * p.n * p.d) & 3);
+                e0 = u0 - sh;
+                zmask = 0;
+                for (int u = 0; u < 4; ++u)
+                    if (e0 + u < 0 || e0 + u >= p.seg) zmask |= 1 << u;
+                boff = 4 * (p.lmargin + delta + e0);  // + 4 * col0 * d (per pixel) + the row slot
+            } else {
+                i = p.k;  // K padding: reads (and masks) the zero row, at an aligned offset
+                boff = 4 * (p.lmargin + ((p.p * p.d) & 3));
+            }
+            ktab[idx] = i | (zmask << 8) | (boff << 16);
+            etab[idx] = e0;
+        }
+    }
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < R; ++s) {
+            ptx::mbar_init(&full[s], 1 + 4);
+            ptx::mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&xfull[a], 1);
+            ptx::mbar_init(&xempty[a], 4 * kGatherGroups);  // every gather warp
+            ptx::mbar_init(&tfull[a], 1);
+            ptx::mbar_init(&tempty[a], 4);  // epilogue warps
+        }
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512, 1>(tmem_slot);
+    ptx::fence_proxy_async_smem();  // zeroed stage buffers -> later bulk-copy writes are ordered after
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nd = p.n * p.d;
+
+    if (warp == 0) {
+        // ===================== kernel-bank producer =====================
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            for (int T = blockIdx.x; T < p.tiles; T += gridDim.x) {
+                const int row0 = variant_of(p, T / p.tpi) * 2 * p.o;  // this image's bank variant
+                for (int kb = 0; kb < p.kb_tile; ++kb) {
+                    ptx::mbar_wait_sleep(&empty[st], ph ^ 1);
+                    ptx::mbar_arrive_expect_tx(&full[st], 2 * C_::B_BYTES);
+                    uint8_t* dst = smem + L.ring + uint32_t(st) * 2 * C_::B_BYTES;
+                    ptx::tma_load_2d(dst, &tmB, &full[st], kb * kKB, row0);                      // big
+                    ptx::tma_load_2d(dst + C_::B_BYTES, &tmB, &full[st], kb * kKB, row0 + p.o);  // small
+                    if (++st == R) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_tf32(kTileM, NP, 0, 0);
+            const uint32_t ring_u = ptx::smem_u32(smem + L.ring);
+            int st = 0;
+            uint32_t ph = 0;
+            int lt = 0;
+            for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
+                const int acc = lt & 1;
+                ptx::mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+                ptx::tc_fence_after();
+                const uint32_t d0 = tmem + uint32_t(acc * C_::ACC_COLS);
+                for (int kb = 0; kb < p.kb_tile; ++kb) {
+                    ptx::mbar_wait(&full[st], ph);
+                    ptx::tc_fence_after();
+                    const uint32_t bbig = ring_u + uint32_t(st) * 2 * C_::B_BYTES;
+                    const uint32_t bsml = bbig + C_::B_BYTES;
+                    const uint32_t abig = tmem + uint32_t(C_::A_COL) + uint32_t(st) * 32, asml = abig + kKB;
+                    const uint32_t first = kb ? 1u : 0u;
+                    // small products first, big * big last
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk)
+                        ptx::mma_tf32_ts(d0, asml + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc,
+                                         kk ? 1u : first);
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk)
+                        ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 32, 16, 512, 4), idesc, 1u);
+#pragma unroll
+                    for (int kk = 0; kk < 2; ++kk)
+                        ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc, 1u);
+                    ptx::mma_commit(&empty[st]);
+                    if (++st == R) { st = 0; ph ^= 1; }
+                }
+                ptx::mma_commit(&tfull[acc]);
+            }
+        }
+    } else if (warp == 2) {
+        // ===================== row-stage producer =====================
+        if (lane == 0) {
+            int lt = 0;
+            for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
+                const int buf = lt & 1;
+                ptx::mbar_wait_sleep(&xempty[buf], ((lt >> 1) & 1) ^ 1);
+                const TileGeo tg = tile_geo(p, T);
+                float* sb = reinterpret_cast<float*>(smem + L.stage) + int64_t(buf) * p.xr * p.pitch;
+                uint32_t bytes = 0;
+                // total bytes first (the barrier is armed before any copy is issued); the last
+                // 1-3 floats of x (when its size is not a multiple of 4) are stored directly
+                for (int rho = 0; rho < tg.nrows; ++rho) {
+                    const int yy = tg.y0 + rho;
+                    if (yy < 0 || yy >= p.n) continue;
+                    const int64_t off = (int64_t(tg.q) * p.n + yy) * nd;
+                    const int64_t a0 = off & ~int64_t(3);
+                    int64_t nfl = ((off - a0) + nd + 3) & ~int64_t(3);
+                    if (a0 + nfl > p.x_total) {
+                        nfl = (p.x_total - a0) & ~int64_t(3);
+                        for (int64_t u = a0 + nfl; u < p.x_total; ++u)
+                            sb[int64_t(rho) * p.pitch + p.lmargin + (u - a0)] = __ldg(p.x + u);
+                    }
+                    bytes += uint32_t(nfl) * 4u;
+                }
+                ptx::mbar_arrive_expect_tx(&xfull[buf], bytes);
+                for (int rho = 0; rho < tg.nrows; ++rho) {
+                    const int yy = tg.y0 + rho;
+                    if (yy < 0 || yy >= p.n) continue;
+                    const int64_t off = (int64_t(tg.q) * p.n + yy) * nd;
+                    const int64_t a0 = off & ~int64_t(3);
+                    int64_t nfl = ((off - a0) + nd + 3) & ~int64_t(3);
+                    if (a0 + nfl > p.x_total) nfl = (p.x_total - a0) & ~int64_t(3);
+                    if (nfl > 0)
+                        ptx::bulk_load(sb + int64_t(rho) * p.pitch + p.lmargin, p.x + a0, uint32_t(nfl) * 4u, &xfull[buf]);
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ===================== epilogue =====================
+        const int t = (warp & 3) * 32 + lane;
+        int lt = 0;
+        for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
+            const int acc = lt & 1;
+            ptx::mbar_wait_sleep(&tfull[acc], (lt >> 1) & 1);
+            ptx::tc_fence_after();
+            const TileGeo tg = tile_geo(p, T);
+            const int P = tg.P0 + t;
+            const bool ok = P < tg.P1;
+            float* yrow = p.y + int64_t(tg.q) * p.y_sq + int64_t(P) * p.y_sp;
+            const bool plain = !p.bias && !p.relu;
+#pragma unroll 1
+            for (int c0 = 0; c0 < NP; c0 += 32) {
+                uint32_t v[32];
+                const uint32_t tc = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(acc * C_::ACC_COLS + c0);
+                ptx::tmem_ld_32x32b_x32(tc, v);
+                ptx::tmem_ld_wait();
+                if (!ok) continue;
+                const int nj = min(32, p.o - c0);  // channels of this chunk that exist (uniform)
+                if (!plain) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        float f = __uint_as_float(v[j]);
+                        if (p.bias && j < nj) f += __ldg(p.bias + c0 + j);
+                        if (p.relu) f = fmaxf(f, 0.f);
+                        v[j] = __float_as_uint(f);
+                    }
+                }
+                float* yc = yrow + int64_t(c0) * p.y_so;
+                if (nj == 32 && p.y_so == 1 && (reinterpret_cast<uintptr_t>(yc) & 15) == 0) {
+                    // NHWC: 32 consecutive channels of this pixel
+                    float4* y4 = reinterpret_cast<float4*>(yc);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        y4[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                            __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                } else if (nj == 32) {
+                    // NCHW: lanes = consecutive pixels of one channel plane per store (coalesced)
+                    const int so = int(p.y_so);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        *yc = __uint_as_float(v[j]);
+                        yc += so;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (j < nj) yc[int64_t(j) * p.y_so] = __uint_as_float(v[j]);
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+        }
+    } else if (warp >= 8) {
+        // ===================== gather groups =====================
+        const int grp = (warp - 8) >> 2;
+        const int t = (warp & 3) * 32 + lane;
+        const uint32_t zero_u = ptx::smem_u32(zero_row);
+        const uint32_t stage_u = ptx::smem_u32(smem + L.stage);
+        const uint32_t pitch_b = uint32_t(p.pitch) * 4u;
+        uint32_t gi = 0;
+        int lt = 0;
+        for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
+            const int buf = lt & 1;
+            const TileGeo tg = tile_geo(p, T);
+            const int P = min(tg.P0 + t, tg.P1 - 1);
+            const int r = P / p.m, c = P - (P / p.m) * p.m;
+            const int yr = p.s * r - p.p;  // input row of filter row 0
+            const int col0 = p.s * c - p.p;  // input column of filter column 0
+            const bool border = col0 < 0 || col0 + p.k > p.n;
+            // filter rows whose input row exists (others read the zero row)
+            uint64_t rok = 0;
+            for (int i = 0; i < p.k; ++i)
+                if (unsigned(yr + i) < unsigned(p.n)) rok |= uint64_t(1) << i;
+            const uint32_t slot0 = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b + uint32_t(p.s * (r - tg.ra)) * pitch_b;
+            const int tb = col0 * p.d * 4;  // byte offset of this pixel's run within a staged row
+            const int* kt = ktab + variant_of(p, tg.q) * ngroups_k;
+            ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
+            for (int kb = 0; kb < p.kb_tile; ++kb, ++gi) {
+                if (int(gi % kGatherGroups) != grp) continue;
+                const uint32_t sl = gi % uint32_t(R);
+                if (gi >= uint32_t(R)) ptx::mbar_wait_sleep(&empty[sl], ((gi / uint32_t(R)) - 1) & 1);
+                uint32_t v[32];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    // group entry (uniform): filter row, zero mask, byte offset of the aligned float4
+                    const int ent = kt[kb * 4 + g];
+                    const int i = ent & 0xFF, zmask = (ent >> 8) & 0xF;
+                    const uint32_t slot = ((rok >> i) & 1) ? slot0 + uint32_t(i) * pitch_b : zero_u;
+                    float4 f = ptx::lds128(uint32_t(int(slot) + tb + (ent >> 16)));
+                    if (zmask) {  // window columns outside the filter row's k d run
+                        if (zmask & 1) f.x = 0.f;
+                        if (zmask & 2) f.y = 0.f;
+                        if (zmask & 4) f.z = 0.f;
+                        if (zmask & 8) f.w = 0.f;
+                    }
+                    if (border) {  // input columns outside [0, n): zero padding (edge pixels only)
+                        const int e0 = etab[variant_of(p, tg.q) * ngroups_k + kb * 4 + g];
+                        float fv[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int e = e0 + u;
+                            const int xc = col0 + (e >= 0 ? e / p.d : -1);
+                            if (xc < 0 || xc >= p.n) fv[u] = 0.f;
+                        }
+                        f = make_float4(fv[0], fv[1], fv[2], fv[3]);
+                    }
+                    const float fa[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const uint32_t big = __float_as_uint(fa[u]) & 0xFFFFE000u;
+                        v[4 * g + u] = big;
+                        v[16 + 4 * g + u] = __float_as_uint(fa[u] - __uint_as_float(big));
+                    }
+                }
+                ptx::tmem_st_32x32b_x32(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C_::A_COL) + sl * 32, v);
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&full[sl]);
+            }
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(&xempty[buf]);
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512, 1>(tmem);
+    }
+}
+
+// kernel bank (o, k, k, d) -> per variant phi: [big rows | small rows] x Kp, filter row i's
+// k d run at columns [i segw + shift, ...) of its window (run_shift), zeros elsewhere
+__global__ void prep_bank_kernel(const float* __restrict__ w, float* __restrict__ w2, int o, int k, int d, int n,
+                                 int pad, int segw, int kp, int nvar) {
+    const int64_t total = int64_t(nvar) * 2 * o * kp;
+    const int seg = k * d;
+    for (int64_t idx = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; idx < total; idx += int64_t(gridDim.x) * blockDim.x) {
+        const int row = int(idx / kp), col = int(idx - int64_t(row) * kp);
+        const int phi = row / (2 * o), hr = row - phi * 2 * o;
+        const int oc = hr < o ? hr : hr - o;
+        const int i = col / segw;
+        const int e = col - i * segw - (i < k ? run_shift(nvar == 1 ? 0 : phi, i, n, d, pad) : 0);
+        float v = 0.f;
+        if (i < k && e >= 0 && e < seg) {
+            v = w[(int64_t(oc) * k + i) * seg + e];
+            if (hr >= o) v -= __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        }
+        w2[idx] = v;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* ptr = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
+    }
+    return fn;
+}
+
+// K-major 2D map over rows x kp floats, box = 16 columns x box_rows rows, SWIZZLE_64B
+bool make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t kp, int box_rows) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {cuuint64_t(kp), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(kp) * 4};
+    cuuint32_t box[2] = {cuuint32_t(kKB), cuuint32_t(box_rows)};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct FwdPlan {
+    int np = 0, segw = 0, kp = 0, kb = 0, nvar = 1, xr = 0, pitch = 0, lmargin = 0, stages = 0;
+    uint32_t smem = 0;
+    bool ok = false;
+};
+
+FwdPlan fwd_plan(const Geo& g) {
+    FwdPlan P;
+    if (g.s * g.d % 4 != 0 || g.o > 192 || g.o < 1 || g.k > 48 || g.m < 1) return P;
+    if (g.b * g.n * g.n * g.d >= (int64_t(1) << 40) || g.b * g.o * g.m * g.m >= (int64_t(1) << 40) ||
+        g.n * g.n * g.d >= (int64_t(1) << 30) || g.b * ((g.m * g.m + kTileM - 1) / kTileM) >= (int64_t(1) << 31))
+        return P;
+    P.np = g.o <= 32 ? 32 : g.o <= 64 ? 64 : g.o <= 96 ? 96 : g.o <= 128 ? 128 : 192;
+    P.nvar = (g.n * g.n * g.d) % 4 == 0 ? 1 : 4;
+    const int seg = int(g.k * g.d);
+    bool shifted = false;
+    for (int phi = 0; phi < P.nvar; ++phi)
+        for (int i = 0; i < g.k; ++i) shifted = shifted || run_shift(phi, i, int(g.n), int(g.d), int(g.p)) != 0;
+    P.segw = (seg + (shifted ? 3 : 0) + 3) & ~3;
+    P.kp = int((g.k * P.segw + kKB - 1) / kKB * kKB);
+    P.kb = P.kp / kKB;
+    if (P.kb * 4 > kMaxKGroups || P.kb < 2) return P;
+    const int64_t rows_span = (kTileM - 1) / g.m + 2 > g.m ? g.m : (kTileM - 1) / g.m + 2;  // output rows per tile
+    P.xr = int(g.s * (rows_span - 1) + g.k);
+    P.lmargin = int((g.p * g.d + 4 + 3) & ~int64_t(3));
+    P.pitch = int((P.lmargin + 3 + (g.n + g.p) * g.d + P.segw + 8 + 3) & ~int64_t(3));
+    if (4 * (P.lmargin + 3 + P.segw) >= 32768) return P;  // byte offsets packed as int16
+    for (int st = max_ring(P.np); st >= 3; --st) {
+        const FwdLayout L = fwd_layout(P.np, st, P.xr, P.pitch, P.kb * 4);
+        if (L.total + 1024 <= uint32_t(kSmemMax)) {
+            P.stages = st;
+            P.smem = L.total + 1024;
+            break;
+        }
+    }
+    P.ok = P.stages > 0;
+    return P;
+}
+
+template <int NP>
+cudaError_t launch_fwd(const CUtensorMap& tm, const FwdParams& fp, uint32_t smem, cudaStream_t st) {
+    auto kern = conv_fwd_gather_kernel<NP>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    const int grid = std::min(num_sms(), fp.tiles);
+    PhaseScope ps(kPhaseGemm, st, 2.0 * double(fp.b) * fp.m * fp.m * double(fp.k) * fp.k * fp.d * fp.o, 0);
+    kern<<<grid, kThreads, smem, st>>>(tm, fp);
+    note_launch();
+    return cudaGetLastError();
+}
+
+}  // namespace gth
+
+using namespace gth;
+
+bool gather_fwd_ok(const Geo& g) { return fwd_plan(g).ok; }
+bool gather_wgrad_ok(const Geo&) { return false; }
+
+int64_t gather_fwd_ws_floats(const Geo& g) {
+    const FwdPlan P = fwd_plan(g);
+    return P.ok ? int64_t(P.nvar) * 2 * g.o * P.kp : 0;
+}
+int64_t gather_wgrad_ws_floats(const Geo&) { return 0; }
+
+cudaError_t gather_fwd(const Geo& g, const float* x, const float* w, float* y, int64_t ycs, const float* bias,
+                       int relu, float* ws, cudaStream_t st) {
+    const FwdPlan P = fwd_plan(g);
+    if (!P.ok) return cudaErrorInvalidValue;
+    {
+        const int64_t total = int64_t(P.nvar) * 2 * g.o * P.kp;
+        prep_bank_kernel<<<grid_for(total, 256), 256, 0, st>>>(w, ws, int(g.o), int(g.k), int(g.d), int(g.n),
+                                                               int(g.p), P.segw, P.kp, P.nvar);
+        note_launch();
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    CUtensorMap tm;
+    if (!make_kmajor_map(&tm, ws, int64_t(P.nvar) * 2 * g.o, P.kp, P.np)) return cudaErrorInvalidValue;
+    FwdParams fp{};
+    fp.x = x;
+    fp.y = y;
+    fp.bias = bias;
+    fp.relu = relu;
+    const int64_t mm = g.m * g.m;
+    if (g.yl) {  // NHWC
+        fp.y_sq = ycs ? ycs : mm * g.o;
+        fp.y_so = 1;
+        fp.y_sp = g.o;
+    } else {
+        fp.y_sq = ycs ? ycs : g.o * mm;
+        fp.y_so = mm;
+        fp.y_sp = 1;
+    }
+    fp.x_total = g.b * g.n * g.n * g.d;
+    fp.b = int(g.b); fp.n = int(g.n); fp.d = int(g.d); fp.k = int(g.k); fp.s = int(g.s); fp.p = int(g.p);
+    fp.m = int(g.m); fp.o = int(g.o);
+    fp.seg = int(g.k * g.d);
+    fp.segw = P.segw;
+    fp.nvar = P.nvar;
+    fp.kb_tile = P.kb;
+    fp.tpi = int((mm + kTileM - 1) / kTileM);
+    fp.tiles = int(g.b) * fp.tpi;
+    fp.pitch = P.pitch;
+    fp.lmargin = P.lmargin;
+    fp.xr = P.xr;
+    fp.stages = P.stages;
+    switch (P.np) {
+        case 32: return launch_fwd<32>(tm, fp, P.smem, st);
+        case 64: return launch_fwd<64>(tm, fp, P.smem, st);
+        case 96: return launch_fwd<96>(tm, fp, P.smem, st);
+        case 128: return launch_fwd<128>(tm, fp, P.smem, st);
+        default: return launch_fwd<192>(tm, fp, P.smem, st);
+    }
+}
+
+cudaError_t gather_wgrad(const Geo&, const float*, const float*, float*, float*, cudaStream_t) {
+    return cudaErrorNotSupported;
+}
+
+}  // namespace cct

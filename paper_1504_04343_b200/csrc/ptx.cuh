@@ -70,6 +70,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Same, with a suspend-time hint: a thread whose phase is not complete sleeps in hardware
+// (up to `ns`) instead of re-polling, so waiting warps do not steal issue slots and barrier
+// bandwidth from the critical ones (the MMA issuer) of the same SM.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns = 0x100000) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(ns)
+        : "memory");
+}
+
 // ---- clusters (CTA pairs for cta_group::2) ------------------------------------
 __device__ __forceinline__ uint32_t cluster_rank() {
     uint32_t r;

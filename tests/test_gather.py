@@ -1,0 +1,106 @@
+"""Fused small-channel Type 1 (csrc/gather.cu): the lowered matrix is gathered from staged
+input rows inside the tcgen05 GEMM (CaffeNet conv1 class: d * stride % 4 == 0).
+
+Parity against the oracle (direct_convolve restatement, tensor.cpp:77-106) at rel-L2
+<= 1e-4, the fused path proven to have run (no lowering phase recorded), and agreement
+with the materialised Type 1 path it replaces (CCT_TUNE_GATHER = 0).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle_py import rel_l2
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+# (n, k, d, o, b, stride, pad): conv1, torchvision AlexNet conv1, and geometries that
+# exercise padding, o not a multiple of 16, every tile width (32 / 64 / 96 / 128 / 192),
+# d = 1 / 2 / 4 / 6, tiles spanning up to 4 output rows, ragged last tiles
+GEOMS = [
+    (227, 11, 3, 96, 2, 4, 0),
+    (224, 11, 3, 64, 2, 4, 2),
+    (31, 5, 2, 96, 3, 2, 1),
+    (20, 3, 4, 128, 2, 1, 1),
+    (17, 7, 1, 40, 3, 4, 3),
+    (40, 4, 6, 192, 2, 2, 0),
+    (9, 9, 3, 16, 2, 4, 4),
+    (63, 11, 3, 96, 1, 4, 5),
+]
+
+
+def _phases(cct, fn):
+    L = cct.lib()
+    P = C.c_double * 7
+    ms, fl, by = P(), P(), P()
+    n = (C.c_uint64 * 7)()
+    L.cct_profile_read(None, None, None, None, 1)
+    L.cct_profile_enable(1)
+    out = fn()
+    L.cct_profile_enable(0)
+    L.cct_profile_read(ms, fl, by, n, 1)
+    return out, list(n)
+
+
+@pytest.mark.parametrize("geom", GEOMS, ids=[f"n{g[0]}k{g[1]}d{g[2]}o{g[3]}s{g[5]}p{g[6]}" for g in GEOMS])
+def test_gather_fwd_vs_oracle(cct, dev, orc, geom):
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = geom
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    x, w = orc.random_problem(7 + n, b, n, d, k, o)
+    ref = orc.conv_fwd(x, w, b, n, d, k, o, s, p)
+    xt = torch.from_numpy(x).to(dev).view(b, n, n, d)
+    wt = torch.from_numpy(w).to(dev).view(o, k, k, d)
+    y, launches = _phases(cct, lambda: conv.conv_fwd(xt, wt, desc, cct.LOWER_T1))
+    assert launches[0] == 0, "the fused path must not run a lowering kernel"
+    err = rel_l2(y.cpu().numpy().ravel(), ref)
+    assert err <= TOL, f"rel-L2 {err:.3e}"
+    with cct.tuning(gather=0):
+        y0 = conv.conv_fwd(xt, wt, desc, cct.LOWER_T1)
+    assert rel_l2(y.cpu().numpy().ravel(), y0.cpu().numpy().ravel()) <= TOL
+
+
+def test_gather_fwd_nhwc_and_repeatable(cct, dev, orc):
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = 227, 11, 3, 96, 3, 4, 0
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    dn = cct.ConvDesc(n, k, d, o, b, s, p, cct.NHWC)
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    y = conv.conv_fwd(x, w, desc, cct.LOWER_T1)
+    yn = conv.conv_fwd(x, w, dn, cct.LOWER_T1)
+    assert torch.equal(yn.view(b, desc.m, desc.m, o).permute(0, 3, 1, 2).contiguous(), y.view(b, o, desc.m, desc.m))
+    for _ in range(3):
+        assert torch.equal(conv.conv_fwd(x, w, desc, cct.LOWER_T1), y)
+
+
+def test_gather_fwd_full_batch_slices(cct, dev, orc):
+    """conv1 at b = 256 (BASELINE configs[2]): image slices against the oracle."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = 227, 11, 3, 96, 256, 4, 0
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    g = torch.Generator(device=dev).manual_seed(11)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    y = conv.conv_fwd(x, w, desc, cct.LOWER_T1).cpu().numpy()
+    wn = w.cpu().numpy().ravel()
+    for q in (0, 1, 127, 255):
+        ref = orc.conv_fwd(x[q].cpu().numpy().ravel(), wn, 1, n, d, k, o, s, p)
+        assert rel_l2(y[q].ravel(), ref) <= TOL
+
+
+def test_gather_fwd_bias_relu(cct, dev, orc):
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = 227, 11, 3, 96, 2, 4, 0
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    x, w = orc.random_problem(5, b, n, d, k, o)
+    bias = orc.uniform(6, o)
+    ref = orc.conv_fwd(x, w, b, n, d, k, o, s, p).reshape(b, o, -1) + bias[None, :, None]
+    ref = np.maximum(ref, 0).ravel()
+    xt = torch.from_numpy(x).to(dev).view(b, n, n, d)
+    wt = torch.from_numpy(w).to(dev).view(o, k, k, d)
+    y = conv.conv_fwd_ex(xt, wt, desc, cct.LOWER_T1, bias=torch.from_numpy(bias).to(dev), relu=True)
+    assert rel_l2(y.cpu().numpy().ravel(), ref) <= TOL

@@ -11,9 +11,9 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
-        if "cct" not in d["Kernel Name"] and "unnamed>" not in d["Kernel Name"] and "--all" not in sys.argv:
+        if not any(s in d["Kernel Name"] for s in ("cct", "unnamed>", "gk::", "_kernel")) and "--all" not in sys.argv:
             continue
-        key = (int(d["ID"]), d["Kernel Name"].split("(")[0].replace("void ", "").replace("cct::<unnamed>::", ""))
+        key = (int(d["ID"]), d["Kernel Name"].split("(")[0].replace("void ", "").replace("cct::<unnamed>::", "").replace("gk::", ""))
         agg.setdefault(key, {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
 tot = 0.0
 for (i, k), v in sorted(agg.items()):

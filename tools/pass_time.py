@@ -20,13 +20,18 @@ ap.add_argument("--pass", dest="pass_", default="fwd")
 ap.add_argument("--type", type=int, default=1)
 ap.add_argument("--batch", type=int, default=256)
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--tune", default="", help="comma list key=value of cct tuning switches")
+ap.add_argument("--layout", type=int, default=0, help="0 NCHW y / dy, 1 NHWC")
 a = ap.parse_args()
+for kv in filter(None, a.tune.split(",")):
+    k_, v_ = kv.split("=")
+    cct.set_tuning(k_, int(v_))
 n, k, d, o, s, p = LAYERS[a.layer]
-desc = cct.ConvDesc(n, k, d, o, a.batch, s, p)
+desc = cct.ConvDesc(n, k, d, o, a.batch, s, p, a.layout)
 dev = torch.device("cuda")
 x = torch.rand((a.batch, n, n, d), device=dev) * 2 - 1
 w = torch.rand((o, k, k, d), device=dev) * 2 - 1
-dy = torch.rand((a.batch, o, desc.m, desc.m), device=dev) * 2 - 1
+dy = torch.rand(desc.y_shape(), device=dev) * 2 - 1
 fn = {"fwd": lambda: conv.conv_fwd(x, w, desc, a.type), "dgrad": lambda: conv.conv_bwd_data(dy, w, desc, a.type),
       "wgrad": lambda: conv.conv_bwd_weight(x, dy, desc, a.type)}[a.pass_]
 for _ in range(3):
