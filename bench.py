@@ -61,6 +61,7 @@ def parse():
                     help="strong scaling (configs[4]): split this many images over the ranks "
                          "(0 = weak scaling, --batch images per GPU)")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs[0..2] device / CPU lines")
+    ap.add_argument("--tune", default="", help="A/B runs: comma list key=value of cct_set_tuning switches")
     return ap.parse_args()
 
 
@@ -363,6 +364,9 @@ def run_ours(a):
         group = dist.group.WORLD
         print(f"cct-bench rank {rank}/{world} on cuda:{local} backend {backend}", file=sys.stderr, flush=True)
     L = cct.lib()
+    for kv in filter(None, a.tune.split(",")):
+        k_, v_ = kv.split("=")
+        cct.set_tuning(k_, int(v_))
     if a.lowering == "auto":
         lowering = cct.LOWER_AUTO
     elif "," in a.lowering:
@@ -482,7 +486,8 @@ def run_ours(a):
                        "images_per_gpu": st.batch, "global_batch": images,
                        "lowering": {l.name: t for l, t in zip(st.layers, st.types)},
                        "parallelism": f"dp{world} (batch split, NCCL all-reduce of dW)" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (step working set > 2 GB)"},
+                       "l2": "inputs larger than L2 (step working set > 2 GB)",
+                       **({"tune": a.tune} if a.tune else {})},
             "tflops": tflops, "tflops_per_gpu": tflops / world,
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
             "clocks": clk, "phases": phase, "configs": cfg,

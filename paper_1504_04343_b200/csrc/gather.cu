@@ -132,7 +132,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     // zero the stage buffers (their margins are never written by the row copies) and the
     // zero row; build the k-block tables: group g of k-block kb -> (filter row, offset)
     {
@@ -184,25 +184,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int nd = p.n * p.d;
 
     if (warp == 0) {
-        // ===================== kernel-bank producer =====================
-        if (lane == 0) {
+        // ===================== kernel-bank producer (warp-uniform loop, elected issue) =====================
+        {
             int st = 0;
             uint32_t ph = 0;
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x) {
                 const int row0 = variant_of(p, T / p.tpi) * 2 * p.o;  // this image's bank variant
                 for (int kb = 0; kb < p.kb_tile; ++kb) {
                     ptx::mbar_wait_sleep(&empty[st], ph ^ 1);
-                    ptx::mbar_arrive_expect_tx(&full[st], 2 * C_::B_BYTES);
-                    uint8_t* dst = smem + L.ring + uint32_t(st) * 2 * C_::B_BYTES;
-                    ptx::tma_load_2d(dst, &tmB, &full[st], kb * kKB, row0);                      // big
-                    ptx::tma_load_2d(dst + C_::B_BYTES, &tmB, &full[st], kb * kKB, row0 + p.o);  // small
+                    if (ptx::elect_one()) {
+                        ptx::mbar_arrive_expect_tx(&full[st], 2 * C_::B_BYTES);
+                        uint8_t* dst = smem + L.ring + uint32_t(st) * 2 * C_::B_BYTES;
+                        ptx::tma_load_2d(dst, &tmB, &full[st], kb * kKB, row0);                      // big
+                        ptx::tma_load_2d(dst + C_::B_BYTES, &tmB, &full[st], kb * kKB, row0 + p.o);  // small
+                    }
+                    __syncwarp();
                     if (++st == R) { st = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
-        if (lane == 0) {
+        // the whole warp runs the loop (warp-uniform operands), one elected lane issues
+        {
             constexpr uint32_t idesc = ptx::idesc_tf32(kTileM, NP, 0, 0);
             const uint32_t ring_u = ptx::smem_u32(smem + L.ring);
             int st = 0;
@@ -220,21 +224,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t bsml = bbig + C_::B_BYTES;
                     const uint32_t abig = tmem + uint32_t(C_::A_COL) + uint32_t(st) * 32, asml = abig + kKB;
                     const uint32_t first = kb ? 1u : 0u;
-                    // small products first, big * big last
+                    if (ptx::elect_one()) {
+                        // small products first, big * big last
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk)
-                        ptx::mma_tf32_ts(d0, asml + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc,
-                                         kk ? 1u : first);
+                        for (int kk = 0; kk < 2; ++kk)
+                            ptx::mma_tf32_ts(d0, asml + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc,
+                                             kk ? 1u : first);
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk)
-                        ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 32, 16, 512, 4), idesc, 1u);
+                        for (int kk = 0; kk < 2; ++kk)
+                            ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 32, 16, 512, 4), idesc, 1u);
 #pragma unroll
-                    for (int kk = 0; kk < 2; ++kk)
-                        ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc, 1u);
-                    ptx::mma_commit(&empty[st]);
+                        for (int kk = 0; kk < 2; ++kk)
+                            ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc, 1u);
+                        ptx::mma_commit(&empty[st]);
+                    }
+                    __syncwarp();
                     if (++st == R) { st = 0; ph ^= 1; }
                 }
-                ptx::mma_commit(&tfull[acc]);
+                if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
+                __syncwarp();
             }
         }
     } else if (warp == 2) {
@@ -338,7 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t zero_u = ptx::smem_u32(zero_row);
         const uint32_t stage_u = ptx::smem_u32(smem + L.stage);
         const uint32_t pitch_b = uint32_t(p.pitch) * 4u;
-        uint32_t gi = 0;
+        // this group's k-blocks are gi = grp, grp + 4, ... (over all tiles): ring slot and
+        // pass over the ring walked incrementally (no division by the runtime ring depth)
+        uint32_t gbase = 0;  // gi of this tile's first k-block
+        int sl = grp, pass = 0;
+        while (sl >= R) { sl -= R; ++pass; }
         int lt = 0;
         for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
             const int buf = lt & 1;
@@ -356,10 +368,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int tb = col0 * p.d * 4;  // byte offset of this pixel's run within a staged row
             const int* kt = ktab + variant_of(p, tg.q) * ngroups_k;
             ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
-            for (int kb = 0; kb < p.kb_tile; ++kb, ++gi) {
-                if (int(gi % kGatherGroups) != grp) continue;
-                const uint32_t sl = gi % uint32_t(R);
-                if (gi >= uint32_t(R)) ptx::mbar_wait_sleep(&empty[sl], ((gi / uint32_t(R)) - 1) & 1);
+            for (int kb = int((uint32_t(grp) - gbase) & (kGatherGroups - 1)); kb < p.kb_tile; kb += kGatherGroups) {
+                if (pass > 0) ptx::mbar_wait_sleep(&empty[sl], (pass - 1) & 1);
                 uint32_t v[32];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
@@ -393,12 +403,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                         v[16 + 4 * g + u] = __float_as_uint(fa[u] - __uint_as_float(big));
                     }
                 }
-                ptx::tmem_st_32x32b_x32(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C_::A_COL) + sl * 32, v);
+                ptx::tmem_st_32x32b_x32(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C_::A_COL) + uint32_t(sl) * 32, v);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&full[sl]);
+                sl += kGatherGroups;
+                while (sl >= R) { sl -= R; ++pass; }
             }
+            gbase += uint32_t(p.kb_tile);
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(&xempty[buf]);
         }

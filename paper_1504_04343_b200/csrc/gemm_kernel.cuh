@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     int* sk_flag = reinterpret_cast<int*>(tmem_slot + 1);
     float* epi = reinterpret_cast<float*>(smem + STAGES * C_::STAGE_BYTES + ((C_::BAR_BYTES + 15) & ~15u));
 
-    const int warp = threadIdx.x >> 5;
+    const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0);  // warp-uniform (uniform registers)
     const int lane = threadIdx.x & 31;
     const uint32_t rank = (CG == 2) ? ptx::cluster_rank() : 0u;
     const bool leader = rank == 0;
@@ -255,7 +255,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         // both -- the split form intermittently hangs)
         const bool role_a = warp == 0;
         const bool role_b = (warp == 3) == (p.split_producer != 0);
-        if (lane == 0 && (role_a || role_b)) {
+        // the whole warp walks the loop (coordinates stay warp-uniform, in uniform registers);
+        // one elected lane arms the barrier and issues the copies
+        if (role_a || role_b) {
             int stage = 0;
             uint32_t phase = 0;
             uint32_t gi = 0;  // k-blocks issued by this CTA (selects the transform group's barrier)
@@ -313,17 +315,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 for (int kb = kb0; kb < kb1; ++kb, ++gi) {
                     ptx::mbar_wait(&empty[stage], phase ^ 1);
+                    const bool el = ptx::elect_one();
                     uint64_t* const fb = &full[int(gi % kTGroups) * STAGES + stage];
-                    if (role_a && role_b) ptx::mbar_arrive_expect_tx(fb, C_::RAW_BYTES);
-                    else if (role_a) ptx::mbar_arrive_expect_tx(fb, C_::A_BYTES);
-                    else ptx::mbar_arrive_expect_tx(fb, C_::B_BYTES);
+                    if (el) ptx::mbar_arrive_expect_tx(fb, (role_a && role_b) ? C_::RAW_BYTES : role_a ? C_::A_BYTES : C_::B_BYTES);
                     uint8_t* a_dst = smem + stage * C_::STAGE_BYTES;
                     uint8_t* b_dst = a_dst + C_::A_BYTES;
                     const int k0 = kb * kBK;
                     if (role_a) {
                         if constexpr (A_IM == 1 && !A_MN) {
                             // implicit lowering, forward: 128 pixels x 16 channels of filter tap (ti, tj)
-                            ptx::tma_load_im2col_4d(a_dst, &tmA, fb, cc * kBK, p.ic_s * px.c - p.ic_p,
+                            if (el) ptx::tma_load_im2col_4d(a_dst, &tmA, fb, cc * kBK, p.ic_s * px.c - p.ic_p,
                                                     p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
                             if (++cc == p.ic_cpt) {
                                 cc = 0;
@@ -333,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // implicit lowering, backward-weight: K rows = 16 pixels, M = (tap, ch)
 #pragma unroll
                             for (int c = 0; c < kBM / 32; ++c)
-                                ptx::tma_load_im2col_4d(a_dst + c * 32 * kBK * 4, &tmA, fb, bw_ch[c],
+                                if (el) ptx::tma_load_im2col_4d(a_dst + c * 32 * kBK * 4, &tmA, fb, bw_ch[c],
                                                         p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
                                                         uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
                             px.c += kBK;
@@ -342,17 +343,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 if (++px.r == p.ic_m) { px.r = 0; ++px.q; }
                             }
                         } else if constexpr (!A_MN) {
-                            ptx::tma_load_2d(a_dst, &tmA, fb, k0, m0);
+                            if (el) ptx::tma_load_2d(a_dst, &tmA, fb, k0, m0);
                         } else {
 #pragma unroll
                             for (int c = 0; c < kBM / 32; ++c)
-                                ptx::tma_load_2d(a_dst + c * 32 * kBK * 4, &tmA, fb, m0 + 32 * c, k0);
+                                if (el) ptx::tma_load_2d(a_dst + c * 32 * kBK * 4, &tmA, fb, m0 + 32 * c, k0);
                         }
                     }
                     if (role_b) {
                         if constexpr (A_IM == 2) {
                             // B: BNL pixels x 16 channels of tap (ti, tj)
-                            ptx::tma_load_im2col_4d(b_dst, &tmB, fb, cc * kBK, p.ic_s * px.c - p.ic_p,
+                            if (el) ptx::tma_load_im2col_4d(b_dst, &tmB, fb, cc * kBK, p.ic_s * px.c - p.ic_p,
                                                     p.ic_s * px.r - p.ic_p, px.q, uint16_t(tap_j), uint16_t(tap_i));
                             if (++cc == p.ic_cpt) {
                                 cc = 0;
@@ -362,7 +363,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             // swapped backward-weight: B = 16 pixels x (BNL/32 x 32 channels of a tap)
 #pragma unroll
                             for (int c = 0; c < NBW; ++c)
-                                ptx::tma_load_im2col_4d(b_dst + c * 32 * kBK * 4, &tmB, fb, bw_ch[c],
+                                if (el) ptx::tma_load_im2col_4d(b_dst + c * 32 * kBK * 4, &tmB, fb, bw_ch[c],
                                                         p.ic_s * px.c - p.ic_p, p.ic_s * px.r - p.ic_p, px.q,
                                                         uint16_t(bw_tj[c]), uint16_t(bw_ti[c]));
                             px.c += kBK;
@@ -375,38 +376,41 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const int nb = nt * BN;
 #pragma unroll
                             for (int c = 0; c < 8 / CG; ++c)
-                                ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, fb,
+                                if (el) ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, fb,
                                                  nb + int(rank) * (256 / CG) + 32 * c, k0);
 #pragma unroll
                             for (int c = 0; c < 4 / CG; ++c)
-                                ptx::tma_load_2d(b_dst + (8 / CG + c) * 32 * kBK * 4, &tmB, fb,
+                                if (el) ptx::tma_load_2d(b_dst + (8 / CG + c) * 32 * kBK * 4, &tmB, fb,
                                                  nb + 256 + int(rank) * (128 / CG) + 32 * c, k0);
                         } else if constexpr (BN == 384) {
                             // 64-row boxes: the CTA's rows of sub-tile 1 (256/CG), then of sub-tile 2 (128/CG)
                             const int nb = nt * BN;
 #pragma unroll
                             for (int c = 0; c < 4 / CG; ++c)
-                                ptx::tma_load_2d(b_dst + c * 64 * kBK * 4, &tmB, fb, k0,
+                                if (el) ptx::tma_load_2d(b_dst + c * 64 * kBK * 4, &tmB, fb, k0,
                                                  nb + int(rank) * (256 / CG) + 64 * c);
 #pragma unroll
                             for (int c = 0; c < 2 / CG; ++c)
-                                ptx::tma_load_2d(b_dst + (4 / CG + c) * 64 * kBK * 4, &tmB, fb, k0,
+                                if (el) ptx::tma_load_2d(b_dst + (4 / CG + c) * 64 * kBK * 4, &tmB, fb, k0,
                                                  nb + 256 + int(rank) * (128 / CG) + 64 * c);
                         } else if constexpr (!B_MN) {
-                            ptx::tma_load_2d(b_dst, &tmB, fb, k0, n0);
+                            if (el) ptx::tma_load_2d(b_dst, &tmB, fb, k0, n0);
                         } else {
 #pragma unroll
                             for (int c = 0; c < BNL / 32; ++c)
-                                ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, fb, n0 + 32 * c, k0);
+                                if (el) ptx::tma_load_2d(b_dst + c * 32 * kBK * 4, &tmB, fb, n0 + 32 * c, k0);
                         }
                     }
+                    __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
         // ===================== MMA issuer (leader CTA only) =====================
-        if (lane == 0 && leader) {
+        // the whole warp walks the loop (warp-uniform operands in uniform registers); one
+        // elected lane issues the MMAs and commits (ptx::elect_one)
+        if (leader) {
             // (BN = 384: two MMAs per step, N = 256 into columns [0, 256) and N = 128 into [256, 384))
             constexpr uint32_t idesc = ptx::idesc_tf32(kBM * CG, BN > 256 ? 256 : BN, A_MN, B_MN);
             constexpr uint32_t idesc2 = ptx::idesc_tf32(kBM * CG, BN > 256 ? BN - 256 : BN, A_MN, B_MN);
@@ -448,6 +452,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t b_raw = a_raw + C_::A_BYTES;
                     const uint32_t a_sml = a_raw + C_::RAW_BYTES;
                     const uint32_t b_sml = b_raw + C_::RAW_BYTES;
+                    if (ptx::elect_one()) {
                     if constexpr (A_TM) {
                         // A big | small for this k-block in TMEM slot gi % kASlots (16 + 16 columns)
                         const uint32_t a_big = tmem_base + A_COL + (gi % kASlots) * (2 * kBK);
@@ -551,10 +556,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     if constexpr (CG == 1) ptx::mma_commit(&empty[stage]);
                     else ptx::mma_commit_cg2(&empty[stage], 0x3);
+                    }  // elect_one
+                    __syncwarp();
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
-                if constexpr (CG == 1) ptx::mma_commit(&tfull[acc]);
-                else ptx::mma_commit_cg2(&tfull[acc], 0x3);
+                if (ptx::elect_one()) {
+                    if constexpr (CG == 1) ptx::mma_commit(&tfull[acc]);
+                    else ptx::mma_commit_cg2(&tfull[acc], 0x3);
+                }
+                __syncwarp();
             }
         }
     } else if (warp >= 4 && warp < 8) {

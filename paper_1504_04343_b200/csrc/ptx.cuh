@@ -246,6 +246,22 @@ __device__ __forceinline__ void mma_commit_cg2(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
+// One lane of a converged warp (elect.sync).  Issuing tcgen05.mma from a warp-uniform
+// loop under this predicate keeps its operands in uniform registers; issuing from a
+// `lane == 0` branch makes ptxas wrap every MMA in an ELECT / R2UR / BRA.U.ANY loop
+// (~10 dependent instructions per MMA: the issue-bound limit of narrow-N tiles).
+__device__ __forceinline__ bool elect_one() {
+    uint32_t pred = 0;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "elect.sync _|p, 0xffffffff;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(pred));
+    return pred != 0;
+}
+
 // Arrive on an mbarrier once every previously issued tcgen05.mma completed
 // (implicitly tcgen05.fence::before_thread_sync).
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
