@@ -61,6 +61,8 @@ def parse():
                     help="strong scaling (configs[4]): split this many images over the ranks "
                          "(0 = weak scaling, --batch images per GPU)")
     ap.add_argument("--no-configs", action="store_true", help="skip the configs[0..2] device / CPU lines")
+    ap.add_argument("--layout", default="nhwc", choices=["nchw", "nhwc"],
+                    help="y / dy layout of every layer (NHWC = the next layer's input order)")
     ap.add_argument("--tune", default="", help="A/B runs: comma list key=value of cct_set_tuning switches")
     return ap.parse_args()
 
@@ -374,7 +376,7 @@ def run_ours(a):
     else:
         lowering = int(a.lowering)
     strong = a.global_batch > 0
-    st = ConvStack(a.batch, dev, CAFFENET, lowering, group=group, seed=1234,
+    st = ConvStack(a.batch, dev, CAFFENET, lowering, group=group, seed=1234, layout=int(a.layout == "nhwc"),
                    global_batch=a.global_batch if strong else None)
     stream = torch.cuda.current_stream()
 
@@ -487,6 +489,7 @@ def run_ours(a):
                        "lowering": {l.name: t for l, t in zip(st.layers, st.types)},
                        "parallelism": f"dp{world} (batch split, NCCL all-reduce of dW)" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (step working set > 2 GB)",
+                       "layout": a.layout,
                        **({"tune": a.tune} if a.tune else {})},
             "tflops": tflops, "tflops_per_gpu": tflops / world,
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,

@@ -616,6 +616,21 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
     if (t1_implicit_bwd(g, type)) return run_bwd_implicit(g, x, cache, dy, w, dx, dw, ws, st);
     const Lowered L = lowered_of(g, type);
     cudaError_t e = cudaSuccess;
+    // small-channel Type 1: backward-weight gathers Dhat from x inside the GEMM (gather.cuh)
+    if (dw && t1_gather_wgrad(g, type) && aligned16(or_plan(x, ws))) {
+        const size_t mark = ws.off;
+        size_t hi = mark;
+        if (dx) {
+            cct_status s = run_bwd_one(g, type, x, cache, dy, w, dx, nullptr, ws, st);
+            if (s != CCT_OK) return s;
+            hi = ws.off;
+            ws.off = mark;  // stream order: the backward-weight may reuse the backward-data scratch
+        }
+        float* w2 = ws.take(gather_wgrad_ws_floats(g));
+        if (ws.base) CCT_TRY(gather_wgrad(g, x, dy, dw, w2, st), "fused gather backward-weight");
+        ws.off = std::max(hi, ws.off);
+        return CCT_OK;
+    }
     // Type 1 with an NHWC dy: dy IS dRhat (rows x o, row-major) -- the GEMMs read it in place
     // (K-major B of backward-data, MN-major operand of backward-weight); otherwise expand dRhat^T
     const bool dy_direct = type == 1 && g.yl && g.o % 4 == 0 && aligned16(dy);

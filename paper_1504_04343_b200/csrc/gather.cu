@@ -30,6 +30,7 @@
 #include "common.cuh"
 #include "gather.cuh"
 #include "ptx.cuh"
+#include "reduce.cuh"
 
 namespace cct {
 namespace gth {
@@ -360,42 +361,53 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int yr = p.s * r - p.p;  // input row of filter row 0
             const int col0 = p.s * c - p.p;  // input column of filter column 0
             const bool border = col0 < 0 || col0 + p.k > p.n;
-            // filter rows whose input row exists (others read the zero row)
-            uint64_t rok = 0;
+            // filter rows whose input row exists (others read the zero row); k <= 32
+            uint32_t rok = 0;
             for (int i = 0; i < p.k; ++i)
-                if (unsigned(yr + i) < unsigned(p.n)) rok |= uint64_t(1) << i;
+                if (unsigned(yr + i) < unsigned(p.n)) rok |= 1u << i;
             const uint32_t slot0 = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b + uint32_t(p.s * (r - tg.ra)) * pitch_b;
             const int tb = col0 * p.d * 4;  // byte offset of this pixel's run within a staged row
             const int* kt = ktab + variant_of(p, tg.q) * ngroups_k;
             ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
             for (int kb = int((uint32_t(grp) - gbase) & (kGatherGroups - 1)); kb < p.kb_tile; kb += kGatherGroups) {
                 if (pass > 0) ptx::mbar_wait_sleep(&empty[sl], (pass - 1) & 1);
-                uint32_t v[32];
+                // the k-block's 4 group entries (uniform): filter row | zero mask | byte offset of
+                // the aligned float4; all four loads issued before any use (no branches between)
+                const int4 e4 = *reinterpret_cast<const int4*>(kt + kb * 4);
+                const int ent[4] = {e4.x, e4.y, e4.z, e4.w};
+                float4 f[4];
 #pragma unroll
                 for (int g = 0; g < 4; ++g) {
-                    // group entry (uniform): filter row, zero mask, byte offset of the aligned float4
-                    const int ent = kt[kb * 4 + g];
-                    const int i = ent & 0xFF, zmask = (ent >> 8) & 0xF;
-                    const uint32_t slot = ((rok >> i) & 1) ? slot0 + uint32_t(i) * pitch_b : zero_u;
-                    float4 f = ptx::lds128(uint32_t(int(slot) + tb + (ent >> 16)));
-                    if (zmask) {  // window columns outside the filter row's k d run
-                        if (zmask & 1) f.x = 0.f;
-                        if (zmask & 2) f.y = 0.f;
-                        if (zmask & 4) f.z = 0.f;
-                        if (zmask & 8) f.w = 0.f;
-                    }
-                    if (border) {  // input columns outside [0, n): zero padding (edge pixels only)
+                    const int i = ent[g] & 0xFF;
+                    const uint32_t slot = ((rok >> i) & 1u) ? slot0 + uint32_t(i) * pitch_b : zero_u;
+                    f[g] = ptx::lds128(uint32_t(int(slot) + tb + (ent[g] >> 16)));
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {  // window columns outside the filter row's k d run
+                    const int zm = ent[g] >> 8;
+                    f[g].x = (zm & 1) ? 0.f : f[g].x;
+                    f[g].y = (zm & 2) ? 0.f : f[g].y;
+                    f[g].z = (zm & 4) ? 0.f : f[g].z;
+                    f[g].w = (zm & 8) ? 0.f : f[g].w;
+                }
+                if (border) {  // input columns outside [0, n): zero padding (edge pixels only)
+#pragma unroll
+                    for (int g = 0; g < 4; ++g) {
                         const int e0 = etab[variant_of(p, tg.q) * ngroups_k + kb * 4 + g];
-                        float fv[4] = {f.x, f.y, f.z, f.w};
+                        float fv[4] = {f[g].x, f[g].y, f[g].z, f[g].w};
 #pragma unroll
                         for (int u = 0; u < 4; ++u) {
                             const int e = e0 + u;
                             const int xc = col0 + (e >= 0 ? e / p.d : -1);
                             if (xc < 0 || xc >= p.n) fv[u] = 0.f;
                         }
-                        f = make_float4(fv[0], fv[1], fv[2], fv[3]);
+                        f[g] = make_float4(fv[0], fv[1], fv[2], fv[3]);
                     }
-                    const float fa[4] = {f.x, f.y, f.z, f.w};
+                }
+                uint32_t v[32];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const float fa[4] = {f[g].x, f[g].y, f[g].z, f[g].w};
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const uint32_t big = __float_as_uint(fa[u]) & 0xFFFFE000u;
@@ -479,7 +491,7 @@ struct FwdPlan {
 
 FwdPlan fwd_plan(const Geo& g) {
     FwdPlan P;
-    if (g.s * g.d % 4 != 0 || g.o > 192 || g.o < 1 || g.k > 48 || g.m < 1) return P;
+    if (g.s * g.d % 4 != 0 || g.o > 192 || g.o < 1 || g.k > 32 || g.m < 1) return P;
     if (g.b * g.n * g.n * g.d >= (int64_t(1) << 40) || g.b * g.o * g.m * g.m >= (int64_t(1) << 40) ||
         g.n * g.n * g.d >= (int64_t(1) << 30) || g.b * ((g.m * g.m + kTileM - 1) / kTileM) >= (int64_t(1) << 31))
         return P;
@@ -522,18 +534,438 @@ cudaError_t launch_fwd(const CUtensorMap& tm, const FwdParams& fp, uint32_t smem
     return cudaGetLastError();
 }
 
+
+// ===========================================================================
+// Backward-weight: dW (o x k k d) = sum over pixels of dy^T x lowered(x), computed
+// transposed, dW^T (k k d x o), so the gathered operand is the tcgen05 A operand in
+// TMEM: lanes = lowered columns (M-tile mt covers columns [128 mt, 128 mt + 128)),
+// TMEM columns = 16 pixels of a k-block.  B = dy (NHWC: pixels x o, MN-major) streams
+// through a TMA ring; 4 transform warps write its 3xTF32 small half next to it.  One
+// CTA computes all M-tiles of a k-block (the staged rows and the dy tile serve every
+// M-tile), accumulating M-tile mt in TMEM columns [mt NP, (mt + 1) NP).  Work = chains
+// of consecutive 128-pixel tiles (<= kWgChainKB k-blocks: the fp32 accumulation-chain
+// cap), each ending in a partial dW written to scratch; the partials are summed in
+// chain order afterwards (deterministic).
+//   warp 0        dy producer (TMA, MN-major 32-channel boxes)   [bfull / bempty]
+//   warp 1        MMA issuer                                       [btdone, afull -> aempty, bempty, tfull]
+//   warp 2        TMEM allocator, then the row-stage producer      [xfull / xempty]
+//   warps 4-7     epilogue: TMEM -> partial dW (lanes = consecutive lowered columns)
+//   warps 8-11    dy transform: small = dy - trunc(dy) in smem     [bfull -> btdone]
+//   warps 12-27   four gather groups: unit (k-block, M-tile) u -> group u % 4
+// ===========================================================================
+constexpr int kWgThreads = 256 + 128 + 128 * kGatherGroups;
+constexpr int kWgChainKB = 256;  // k-blocks per accumulation chain (= kMaxChainKB)
+constexpr int kWgMaxMT = 3;      // M-tiles (k k d <= 384)
+
+struct WgParams {
+    const float* x;
+    float* part;             // [chain][o][kkd]
+    int64_t x_total;
+    int b, n, d, k, s, p, m, o, kkd, kd;
+    int mt_tiles;            // M-tiles (ceil(kkd / 128))
+    int tpi, tiles, chains;  // 128-pixel tiles per image, total tiles, chains
+    int pitch, lmargin, xr;  // staged rows (as the forward)
+    int bstages, aslots;
+};
+
+__device__ __forceinline__ float4 small4(float4 v) {  // x - trunc_tf32(x), exact
+    v.x -= __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    v.y -= __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    v.z -= __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    v.w -= __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    return v;
+}
+
+__host__ __device__ inline uint32_t wg_bstage_bytes(int np) { return uint32_t(np) * kKB * 4u; }  // one half
+
+struct WgLayout {
+    uint32_t ring, stage, bars, total;
+};
+__host__ __device__ inline WgLayout wg_layout(int np, int bstages, int aslots, int xr, int pitch) {
+    WgLayout L;
+    L.ring = 0;
+    L.stage = uint32_t(bstages) * 2u * wg_bstage_bytes(np);
+    L.bars = (L.stage + 2u * uint32_t(xr) * uint32_t(pitch) * 4u + 15u) & ~15u;
+    L.total = L.bars + uint32_t(3 * bstages + 2 * aslots + 8) * 8u + 16u;
+    return L;
+}
+
+__device__ __forceinline__ void wg_chain(const WgParams& p, int c, int& t0, int& t1) {
+    t0 = int(int64_t(c) * p.tiles / p.chains);
+    t1 = int(int64_t(c + 1) * p.tiles / p.chains);
+}
+__device__ __forceinline__ int wg_tile_kb(const WgParams& p, int T) {
+    const int P0 = (T % p.tpi) * kTileM;
+    return (min(P0 + kTileM, p.m * p.m) - P0 + kKB - 1) / kKB;
+}
+
+template <int NP, bool PAD>
+__global__ void __launch_bounds__(kWgThreads, 1)
+    conv_wgrad_gather_kernel(const __grid_constant__ CUtensorMap tmB, const WgParams p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+    constexpr uint32_t HB = NP * kKB * 4;  // one half (raw or small) of a dy stage
+    const int RB = p.bstages, RA = p.aslots, MT = p.mt_tiles;
+    const WgLayout L = wg_layout(NP, RB, RA, p.xr, p.pitch);
+    uint64_t* bfull = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* btdone = bfull + RB;
+    uint64_t* bempty = btdone + RB;
+    uint64_t* afull = bempty + RB;
+    uint64_t* aempty = afull + RA;
+    uint64_t* xfull = aempty + RA;
+    uint64_t* xempty = xfull + 2;
+    uint64_t* tfull = xempty + 2;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+    const uint32_t A_COL = uint32_t(MT * NP);  // A slots after the accumulators
+
+    const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        ptx::prefetch_tmap(&tmB);
+        for (int s = 0; s < RB; ++s) {
+            ptx::mbar_init(&bfull[s], 1);
+            ptx::mbar_init(&btdone[s], 4);
+            ptx::mbar_init(&bempty[s], 1);
+        }
+        for (int a = 0; a < RA; ++a) {
+            ptx::mbar_init(&afull[a], 4);
+            ptx::mbar_init(&aempty[a], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            ptx::mbar_init(&xfull[a], 1);
+            ptx::mbar_init(&xempty[a], 4 * kGatherGroups);
+        }
+        ptx::mbar_init(tfull, 1);
+        ptx::mbar_init(tempty, 4);
+        ptx::fence_barrier_init();
+    }
+    if (warp == 2) ptx::tmem_alloc<512, 1>(tmem_slot);
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    const int nd = p.n * p.d;
+    const int mm = p.m * p.m;
+
+    if (warp == 0) {
+        // ===================== dy producer (warp-uniform loop, elected issue) =====================
+        int st = 0;
+        uint32_t ph = 0;
+        for (int c = blockIdx.x; c < p.chains; c += gridDim.x) {
+            int t0, t1;
+            wg_chain(p, c, t0, t1);
+            for (int T = t0; T < t1; ++T) {
+                const int q = T / p.tpi;
+                const int P0 = (T - q * p.tpi) * kTileM;
+                const int nkb = wg_tile_kb(p, T);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    ptx::mbar_wait_sleep(&bempty[st], ph ^ 1);
+                    if (ptx::elect_one()) {
+                        ptx::mbar_arrive_expect_tx(&bfull[st], HB);
+                        uint8_t* dst = smem + L.ring + uint32_t(st) * 2u * HB;
+                        const int pix = q * mm + P0 + kb * kKB;
+#pragma unroll
+                        for (int cc = 0; cc < NP / 32; ++cc)
+                            ptx::tma_load_2d(dst + cc * 32 * kKB * 4, &tmB, &bfull[st], 32 * cc, pix);
+                    }
+                    __syncwarp();
+                    if (++st == RB) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        constexpr uint32_t idesc = ptx::idesc_tf32(kTileM, NP, 0, 1);
+        const uint32_t ring_u = ptx::smem_u32(smem + L.ring);
+        int bs = 0, as = 0;
+        uint32_t bph = 0, aph = 0;
+        int lc = 0;
+        for (int c = blockIdx.x; c < p.chains; c += gridDim.x, ++lc) {
+            ptx::mbar_wait(tempty, (lc & 1) ^ 1);
+            ptx::tc_fence_after();
+            int t0, t1;
+            wg_chain(p, c, t0, t1);
+            bool first = true;
+            for (int T = t0; T < t1; ++T) {
+                const int nkb = wg_tile_kb(p, T);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    ptx::mbar_wait(&btdone[bs], bph);
+                    const uint32_t braw = ring_u + uint32_t(bs) * 2u * HB, bsml = braw + HB;
+                    for (int mt = 0; mt < MT; ++mt) {
+                        ptx::mbar_wait(&afull[as], aph);
+                        ptx::tc_fence_after();
+                        const uint32_t d0 = tmem + uint32_t(mt * NP);
+                        const uint32_t abig = tmem + A_COL + uint32_t(as) * 32, asml = abig + kKB;
+                        if (ptx::elect_one()) {
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                ptx::mma_tf32_ts(d0, asml + kk * 8, ptx::smem_desc(braw + kk * 1024, 2048, 512, 1), idesc,
+                                                 (first && kk == 0) ? 0u : 1u);
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 1024, 2048, 512, 1), idesc, 1u);
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(braw + kk * 1024, 2048, 512, 1), idesc, 1u);
+                            ptx::mma_commit(&aempty[as]);
+                        }
+                        __syncwarp();
+                        if (++as == RA) { as = 0; aph ^= 1; }
+                    }
+                    first = false;
+                    if (ptx::elect_one()) ptx::mma_commit(&bempty[bs]);
+                    __syncwarp();
+                    if (++bs == RB) { bs = 0; bph ^= 1; }
+                }
+            }
+            if (ptx::elect_one()) ptx::mma_commit(tfull);
+            __syncwarp();
+        }
+    } else if (warp == 2) {
+        // ===================== row-stage producer =====================
+        if (lane == 0) {
+            int lt = 0;
+            for (int c = blockIdx.x; c < p.chains; c += gridDim.x) {
+                int t0, t1;
+                wg_chain(p, c, t0, t1);
+                for (int T = t0; T < t1; ++T, ++lt) {
+                    const int buf = lt & 1;
+                    ptx::mbar_wait_sleep(&xempty[buf], ((lt >> 1) & 1) ^ 1);
+                    const int q = T / p.tpi;
+                    const int P0 = (T - q * p.tpi) * kTileM, P1 = min(P0 + kTileM, mm);
+                    const int ra = P0 / p.m, rb = (P1 - 1) / p.m;
+                    const int y0 = p.s * ra - p.p, nrows = p.s * (rb - ra) + p.k;
+                    float* sb = reinterpret_cast<float*>(smem + L.stage) + int64_t(buf) * p.xr * p.pitch;
+                    uint32_t bytes = 0;
+                    for (int rho = 0; rho < nrows; ++rho) {
+                        const int yy = y0 + rho;
+                        if (yy < 0 || yy >= p.n) continue;
+                        const int64_t off = (int64_t(q) * p.n + yy) * nd;
+                        const int64_t a0 = off & ~int64_t(3);
+                        int64_t nfl = ((off - a0) + nd + 3) & ~int64_t(3);
+                        if (a0 + nfl > p.x_total) {
+                            nfl = (p.x_total - a0) & ~int64_t(3);
+                            for (int64_t u = a0 + nfl; u < p.x_total; ++u)
+                                sb[int64_t(rho) * p.pitch + p.lmargin + (u - a0)] = __ldg(p.x + u);
+                        }
+                        bytes += uint32_t(nfl) * 4u;
+                    }
+                    ptx::mbar_arrive_expect_tx(&xfull[buf], bytes);
+                    for (int rho = 0; rho < nrows; ++rho) {
+                        const int yy = y0 + rho;
+                        if (yy < 0 || yy >= p.n) continue;
+                        const int64_t off = (int64_t(q) * p.n + yy) * nd;
+                        const int64_t a0 = off & ~int64_t(3);
+                        int64_t nfl = ((off - a0) + nd + 3) & ~int64_t(3);
+                        if (a0 + nfl > p.x_total) nfl = (p.x_total - a0) & ~int64_t(3);
+                        if (nfl > 0)
+                            ptx::bulk_load(sb + int64_t(rho) * p.pitch + p.lmargin, p.x + a0, uint32_t(nfl) * 4u,
+                                           &xfull[buf]);
+                    }
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        // ===================== epilogue: partial dW of each chain =====================
+        const int qd = warp & 3;
+        int lc = 0;
+        for (int c = blockIdx.x; c < p.chains; c += gridDim.x, ++lc) {
+            ptx::mbar_wait_sleep(tfull, lc & 1);
+            ptx::tc_fence_after();
+            float* part = p.part + int64_t(c) * p.o * p.kkd;
+            for (int mt = 0; mt < MT; ++mt) {
+                const int col = mt * kTileM + qd * 32 + lane;
+#pragma unroll 1
+                for (int c0 = 0; c0 < NP; c0 += 32) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + uint32_t(mt * NP + c0), v);
+                    ptx::tmem_ld_wait();
+                    if (col < p.kkd) {
+                        const int nj = min(32, p.o - c0);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (j < nj) __stcg(part + int64_t(c0 + j) * p.kkd + col, __uint_as_float(v[j]));
+                    }
+                }
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(tempty);
+        }
+    } else if (warp >= 8 && warp < 12) {
+        // ===================== dy transform: small half =====================
+        const int t = (warp - 8) * 32 + lane;
+        const uint32_t ring_u = ptx::smem_u32(smem + L.ring);
+        int st = 0;
+        uint32_t ph = 0;
+        for (int c = blockIdx.x; c < p.chains; c += gridDim.x) {
+            int t0, t1;
+            wg_chain(p, c, t0, t1);
+            for (int T = t0; T < t1; ++T) {
+                const int nkb = wg_tile_kb(p, T);
+                for (int kb = 0; kb < nkb; ++kb) {
+                    ptx::mbar_wait(&bfull[st], ph);
+                    const uint32_t braw = ring_u + uint32_t(st) * 2u * HB;
+#pragma unroll
+                    for (int i = t; i < int(HB / 16); i += 128) {
+                        const float4 v = ptx::lds128(braw + uint32_t(i) * 16u);
+                        ptx::sts128(braw + HB + uint32_t(i) * 16u, small4(v));
+                    }
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&btdone[st]);
+                    if (++st == RB) { st = 0; ph ^= 1; }
+                }
+            }
+        }
+    } else if (warp >= 12) {
+        // ===================== gather groups =====================
+        const int grp = (warp - 12) >> 2;
+        const int qd = warp & 3;
+        const uint32_t stage_u = ptx::smem_u32(smem + L.stage);
+        const uint32_t pitch_b = uint32_t(p.pitch) * 4u;
+        // per M-tile lane constants: lowered column -> filter row i, run element e, filter column j
+        int li[kWgMaxMT], le[kWgMaxMT], lj[kWgMaxMT], lph[kWgMaxMT];
+#pragma unroll
+        for (int mt = 0; mt < kWgMaxMT; ++mt) {
+            const int col = min(mt * kTileM + qd * 32 + lane, p.kkd - 1);
+            li[mt] = col / p.kd;
+            le[mt] = col - li[mt] * p.kd;
+            lj[mt] = le[mt] / p.d;
+            lph[mt] = int((int64_t(li[mt]) * nd) & 3);
+        }
+        int u = 0;                    // unit counter (k-block, M-tile) of this CTA
+        int sl = grp, pass = 0;       // A slot / pass of this group's next unit (unit grp first)
+        while (sl >= RA) { sl -= RA; ++pass; }
+        int lt = 0;
+        for (int c = blockIdx.x; c < p.chains; c += gridDim.x) {
+            int t0, t1;
+            wg_chain(p, c, t0, t1);
+            for (int T = t0; T < t1; ++T, ++lt) {
+                const int buf = lt & 1;
+                const int q = T / p.tpi;
+                const int P0 = (T - q * p.tpi) * kTileM, P1 = min(P0 + kTileM, mm);
+                const int ra = P0 / p.m;
+                const int nkb = (P1 - P0 + kKB - 1) / kKB;
+                const uint32_t sbase = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b;
+                ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
+                for (int kb = 0; kb < nkb; ++kb) {
+#pragma unroll
+                    for (int mt = 0; mt < kWgMaxMT; ++mt) {
+                        if (mt >= MT) break;
+                        if (((u++) & (kGatherGroups - 1)) != grp) continue;
+                        if (pass > 0) ptx::mbar_wait_sleep(&aempty[sl], (pass - 1) & 1);
+                        const int col = mt * kTileM + qd * 32 + lane;
+                        const bool cok = col < p.kkd;
+                        // lane part of the staged address: filter row i's slot, run element e
+                        const uint32_t lbase = sbase + uint32_t(li[mt]) * pitch_b + uint32_t(p.lmargin + le[mt]) * 4u;
+                        int P = P0 + kb * kKB;
+                        int r = P / p.m, cc = P - r * p.m;
+                        uint32_t v[32];
+#pragma unroll
+                        for (int jj = 0; jj < kKB; ++jj) {
+                            // pixel (r, cc): staged row s (r - ra) + i, row phase of input row s r - p + i
+                            const int ph4 = int(((int64_t(q) * p.n + p.s * r - p.p) * nd + lph[mt]) & 3);
+                            const uint32_t addr = lbase + uint32_t(p.s * (r - ra)) * pitch_b +
+                                                  uint32_t(((p.s * cc - p.p) * p.d + ph4) * 4);
+                            float f = ptx::lds32(addr);
+                            bool ok = cok && (P + jj < P1);
+                            if constexpr (PAD) {
+                                ok = ok && unsigned(p.s * r - p.p + li[mt]) < unsigned(p.n) &&
+                                     unsigned(p.s * cc - p.p + lj[mt]) < unsigned(p.n);
+                            }
+                            f = ok ? f : 0.f;
+                            const uint32_t big = __float_as_uint(f) & 0xFFFFE000u;
+                            v[jj] = big;
+                            v[kKB + jj] = __float_as_uint(f - __uint_as_float(big));
+                            if (++cc == p.m) { cc = 0; ++r; }
+                        }
+                        ptx::tmem_st_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + A_COL + uint32_t(sl) * 32, v);
+                        ptx::tmem_st_wait();
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(&afull[sl]);
+                        sl += kGatherGroups;
+                        while (sl >= RA) { sl -= RA; ++pass; }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&xempty[buf]);
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc<512, 1>(tmem);
+    }
+}
+
+// NHWC dy (pixels x o) as an MN-major operand: 32-channel x 16-pixel boxes, SWIZZLE_128B_ATOM_32B
+bool make_mnmajor_map(CUtensorMap* map, const float* base, int64_t pixels, int64_t o) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {cuuint64_t(o), cuuint64_t(pixels)};
+    cuuint64_t strides[1] = {cuuint64_t(o) * 4};
+    cuuint32_t box[2] = {32, cuuint32_t(kKB)};
+    cuuint32_t estr[2] = {1, 1};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+struct WgPlan {
+    int np = 0, mt = 0, bstages = 0, aslots = 0, xr = 0, pitch = 0, lmargin = 0, tpi = 0, tiles = 0, chains = 0, grid = 0;
+    uint32_t smem = 0;
+    bool ok = false;
+};
+
+WgPlan wg_plan(const Geo& g) {
+    WgPlan P;
+    const int64_t kkd = g.k * g.k * g.d, mm = g.m * g.m;
+    if (g.o < 1 || g.o > 128 || g.o % 4 != 0 || kkd > int64_t(kWgMaxMT) * kTileM || g.m < 1 || g.k > 32) return P;
+    if (g.b * g.n * g.n * g.d >= (int64_t(1) << 40) || g.b * mm >= (int64_t(1) << 31) - kTileM ||
+        g.n * g.n * g.d >= (int64_t(1) << 30) || g.o * kkd * 4096 >= (int64_t(1) << 40))
+        return P;
+    P.np = int((g.o + 31) / 32 * 32);
+    P.mt = int((kkd + kTileM - 1) / kTileM);
+    P.aslots = std::min(8, (512 - P.mt * P.np) / 32);
+    if (P.aslots < kGatherGroups) return P;
+    const int64_t rows_span = (kTileM - 1) / g.m + 2 > g.m ? g.m : (kTileM - 1) / g.m + 2;
+    P.xr = int(g.s * (rows_span - 1) + g.k);
+    P.lmargin = int((g.p * g.d + 4 + 3) & ~int64_t(3));
+    P.pitch = int((P.lmargin + (g.n + g.p) * g.d + 8 + 3) & ~int64_t(3));
+    if (int64_t(P.xr) * P.pitch * 4 * 2 >= (int64_t(1) << 31)) return P;
+    for (int st = 8; st >= 2; --st) {
+        const WgLayout L = wg_layout(P.np, st, P.aslots, P.xr, P.pitch);
+        if (L.total + 1024 <= uint32_t(kSmemMax)) {
+            P.bstages = st;
+            P.smem = L.total + 1024;
+            break;
+        }
+    }
+    if (!P.bstages) return P;
+    P.tpi = int((mm + kTileM - 1) / kTileM);
+    P.tiles = int(g.b * P.tpi);
+    const int kb_tile_max = kTileM / kKB;
+    const int cmin = (P.tiles * kb_tile_max + kWgChainKB - 1) / kWgChainKB;
+    P.grid = std::min(num_sms(), P.tiles);
+    P.chains = std::min(P.tiles, (cmin + P.grid - 1) / P.grid * P.grid);
+    P.ok = true;
+    return P;
+}
 }  // namespace gth
 
 using namespace gth;
 
 bool gather_fwd_ok(const Geo& g) { return fwd_plan(g).ok; }
-bool gather_wgrad_ok(const Geo&) { return false; }
 
 int64_t gather_fwd_ws_floats(const Geo& g) {
     const FwdPlan P = fwd_plan(g);
     return P.ok ? int64_t(P.nvar) * 2 * g.o * P.kp : 0;
 }
-int64_t gather_wgrad_ws_floats(const Geo&) { return 0; }
 
 cudaError_t gather_fwd(const Geo& g, const float* x, const float* w, float* y, int64_t ycs, const float* bias,
                        int relu, float* ws, cudaStream_t st) {
@@ -586,8 +1018,70 @@ cudaError_t gather_fwd(const Geo& g, const float* x, const float* w, float* y, i
     }
 }
 
-cudaError_t gather_wgrad(const Geo&, const float*, const float*, float*, float*, cudaStream_t) {
-    return cudaErrorNotSupported;
+
+bool gather_wgrad_ok(const Geo& g) { return wg_plan(g).ok; }
+
+int64_t gather_wgrad_ws_floats(const Geo& g) {
+    const WgPlan P = wg_plan(g);
+    if (!P.ok) return 0;
+    const int64_t nhwc = g.yl ? 0 : (g.b * g.m * g.m * g.o + 3) / 4 * 4;  // NCHW dy -> NHWC copy
+    return nhwc + int64_t(P.chains) * g.o * g.k * g.k * g.d;
+}
+
+cudaError_t gather_wgrad(const Geo& g, const float* x, const float* dy, float* dw, float* ws, cudaStream_t st) {
+    const WgPlan P = wg_plan(g);
+    if (!P.ok) return cudaErrorInvalidValue;
+    const int64_t mm = g.m * g.m, kkd = g.k * g.k * g.d;
+    const float* dyn = dy;
+    float* part = ws;
+    if (!g.yl) {  // NCHW dy -> NHWC (pixels x o), the MN-major B operand
+        float* t = ws;
+        part = ws + (g.b * mm * g.o + 3) / 4 * 4;
+        cudaError_t e = transpose_batched(dy, g.o, mm, mm, g.o * mm, t, g.o, mm * g.o, g.b, kPhaseExpand, st);
+        if (e != cudaSuccess) return e;
+        dyn = t;
+    }
+    CUtensorMap tm;
+    if (!make_mnmajor_map(&tm, dyn, g.b * mm, g.o)) return cudaErrorInvalidValue;
+    WgParams wp{};
+    wp.x = x;
+    wp.part = part;
+    wp.x_total = g.b * g.n * g.n * g.d;
+    wp.b = int(g.b); wp.n = int(g.n); wp.d = int(g.d); wp.k = int(g.k); wp.s = int(g.s); wp.p = int(g.p);
+    wp.m = int(g.m); wp.o = int(g.o);
+    wp.kkd = int(kkd);
+    wp.kd = int(g.k * g.d);
+    wp.mt_tiles = P.mt;
+    wp.tpi = P.tpi;
+    wp.tiles = P.tiles;
+    wp.chains = P.chains;
+    wp.pitch = P.pitch;
+    wp.lmargin = P.lmargin;
+    wp.xr = P.xr;
+    wp.bstages = P.bstages;
+    wp.aslots = P.aslots;
+    {
+        PhaseScope ps(kPhaseGemm, st, 2.0 * double(g.b) * double(mm) * double(kkd) * double(g.o), 0);
+        cudaError_t e = cudaSuccess;
+        auto go = [&](auto kern) {
+            e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.smem));
+            if (e == cudaSuccess) {
+                kern<<<P.grid, kWgThreads, P.smem, st>>>(tm, wp);
+                note_launch();
+                e = cudaGetLastError();
+            }
+        };
+        const bool pad = g.p > 0;
+        switch (P.np) {
+            case 32: pad ? go(conv_wgrad_gather_kernel<32, true>) : go(conv_wgrad_gather_kernel<32, false>); break;
+            case 64: pad ? go(conv_wgrad_gather_kernel<64, true>) : go(conv_wgrad_gather_kernel<64, false>); break;
+            case 96: pad ? go(conv_wgrad_gather_kernel<96, true>) : go(conv_wgrad_gather_kernel<96, false>); break;
+            default: pad ? go(conv_wgrad_gather_kernel<128, true>) : go(conv_wgrad_gather_kernel<128, false>); break;
+        }
+        if (e != cudaSuccess) return e;
+    }
+    const int64_t wsize = g.o * kkd;
+    return splitk_reduce(part, wsize, P.chains, 1, wsize, wsize, dw, wsize, st);
 }
 
 }  // namespace cct

@@ -104,3 +104,62 @@ def test_gather_fwd_bias_relu(cct, dev, orc):
     wt = torch.from_numpy(w).to(dev).view(o, k, k, d)
     y = conv.conv_fwd_ex(xt, wt, desc, cct.LOWER_T1, bias=torch.from_numpy(bias).to(dev), relu=True)
     assert rel_l2(y.cpu().numpy().ravel(), ref) <= TOL
+
+
+# ---------------------------------------------------------------------------
+# fused backward-weight (conv_wgrad_gather_kernel): dW^T = lowered(x)^T dy with the
+# lowered columns gathered into TMEM; o % 4 == 0, o <= 128, k k d <= 384
+WGEOMS = [g for g in GEOMS if g[3] % 4 == 0 and g[3] <= 128 and g[1] * g[1] * g[2] <= 384]
+
+
+@pytest.mark.parametrize("layout", [0, 1], ids=["nchw", "nhwc"])
+@pytest.mark.parametrize("geom", WGEOMS, ids=[f"n{g[0]}k{g[1]}d{g[2]}o{g[3]}s{g[5]}p{g[6]}" for g in WGEOMS])
+def test_gather_wgrad_vs_oracle(cct, dev, orc, geom, layout):
+    """dW against the oracle's backward-weight (tensor.cpp:77-106 adjoint) at rel-L2 <= 1e-4,
+    no lowering kernel launched, and agreement with the materialised Type 1 path."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = geom
+    desc = cct.ConvDesc(n, k, d, o, b, s, p, layout)
+    x, _ = orc.random_problem(17 + n, b, n, d, k, o)
+    m = desc.m
+    dy = orc.uniform(18 + n, b * o * m * m)  # NCHW order
+    ref = orc.conv_bwd_weight(x, dy, b, n, d, k, o, s, p)
+    xt = torch.from_numpy(x).to(dev).view(b, n, n, d)
+    dyt = torch.from_numpy(dy).to(dev).view(b, o, m, m)
+    if layout:
+        dyt = dyt.permute(0, 2, 3, 1).contiguous()
+    dw, launches = _phases(cct, lambda: conv.conv_bwd_weight(xt, dyt, desc, cct.LOWER_T1))
+    assert launches[0] == 0, "the fused path must not run a lowering kernel"
+    err = rel_l2(dw.cpu().numpy().ravel(), ref)
+    assert err <= TOL, f"rel-L2 {err:.3e}"
+    with cct.tuning(gather=0):
+        dw0 = conv.conv_bwd_weight(xt, dyt, desc, cct.LOWER_T1)
+    assert rel_l2(dw.cpu().numpy().ravel(), dw0.cpu().numpy().ravel()) <= TOL
+    # deterministic: fixed chains, fixed-order reduction
+    assert torch.equal(conv.conv_bwd_weight(xt, dyt, desc, cct.LOWER_T1), dw)
+
+
+def test_gather_wgrad_full_batch(cct, dev):
+    """conv1 at b = 256 (BASELINE configs[2]; 296 chains): against an fp64 torch reference
+    of the same lowered product, and the combined backward (dx + dW in one call)."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = 227, 11, 3, 96, 256, 4, 0
+    desc = cct.ConvDesc(n, k, d, o, b, s, p, cct.NHWC)
+    g = torch.Generator(device=dev).manual_seed(21)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    m = desc.m
+    dy = torch.rand((b, m, m, o), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    dw = conv.conv_bwd_weight(x, dy, desc, cct.LOWER_T1)
+    # fp64 reference: unfold x (NCHW view) into the lowered matrix, one image chunk at a time
+    ref = torch.zeros((o, d * k * k), dtype=torch.float64, device=dev)
+    for q0 in range(0, b, 32):
+        xc = x[q0:q0 + 32].permute(0, 3, 1, 2).double()
+        cols = torch.nn.functional.unfold(xc, k, stride=s, padding=p)          # (bq, d k k, m m)
+        dyc = dy[q0:q0 + 32].reshape(-1, m * m, o).double()                    # (bq, m m, o)
+        ref += torch.einsum("bcp,bpo->oc", cols, dyc)
+    ref = ref.view(o, d, k, k).permute(0, 2, 3, 1).reshape(o, k, k, d)
+    err = (torch.linalg.norm(dw.double() - ref) / torch.linalg.norm(ref)).item()
+    assert err <= TOL, f"rel-L2 {err:.3e}"
+    dx, dw2 = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x)
+    assert torch.equal(dw2, dw)
