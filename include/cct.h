@@ -162,7 +162,8 @@ typedef enum {
     CCT_TUNE_FWD_SWAP = 11,      /* 1: swapped forward for o < 128 (default 0: measured slower)          */
     CCT_TUNE_TRACE_PHASES = 12,  /* 1: one stderr line per kernel launch (diagnostics)                   */
     CCT_TUNE_GATHER = 13,        /* 1 (default): fused small-channel Type 1 (d s % 4 == 0, e.g. conv1):  */
-                                 /* Dhat gathered from staged input rows inside the GEMM, never in HBM   */
+                                 /* Dhat gathered from staged input rows inside the GEMM, never in HBM;  */
+                                 /* 2: same, forward without the merged N = 2 NP product (A/B)           */
     CCT_TUNE_COUNT = 14
 } cct_tuning;
 CCT_API cct_status cct_set_tuning(cct_tuning key, int value);

@@ -3,19 +3,18 @@
 //
 // Forward, one CTA per SM, persistent over 128-pixel tiles (a tile never crosses an
 // image), 768 threads:
-//   warp 0        TMA producer (one lane): kernel-bank k-blocks (big | small halves,
-//                 prepared once per call) -> smem ring stage s  [full / empty]
-//   warp 1        MMA issuer (one lane): per 16-wide k-block 6 x tcgen05.mma.kind::tf32,
+//   warp 0        TMA producer (elected lane): kernel-bank k-blocks ([small | big] halves,
+//                 prepared once per call) -> smem ring stage  [bfull / bempty]
+//   warp 1        MMA issuer (elected lane of a warp-uniform loop): per 16-wide k-block 4
+//                 (NP <= 96, merged N = 2 NP product, see FwdCfg) or 6 tcgen05.mma.kind::tf32,
 //                 A (the k-block of Dhat) from TMEM, B from smem
 //   warp 2        TMEM allocator, then the staging producer (one lane): the input rows a
 //                 tile touches -> a double-buffered row stage (1D bulk copies)  [xfull / xempty]
 //   warps 4-7     epilogue: tcgen05.ld -> y (NCHW: lanes = consecutive pixels, coalesced)
 //   warps 8-23    four gather groups (k-block gi -> group gi % 4): 128 pixels x 16 lowered columns
-//                 from the staged rows -> big / small -> tcgen05.st into TMEM A slot s
-// One barrier pair per ring position s covers both operands of a k-block: full[s] counts the
-// bank TMA (1 arrival + bytes) and the 4 gather warps, empty[s] is the MMA commit freeing the
-// bank stage and the A slot together (one wait and one commit per k-block on the MMA thread,
-// measured: the MMA issuer is the critical path of this narrow GEMM).
+//                 from the staged rows -> big / small -> tcgen05.st into TMEM A slot  [afull / aempty]
+// The bank ring (smem-sized) and the A slot ring (TMEM-sized) are independent; the MMA issuer
+// waits one barrier of each per k-block and commits both.
 // Lowered column order (this kernel's own; the kernel bank is repacked to match): filter
 // row i owns the window of columns [i segw, (i + 1) segw), its k d run placed at the shift
 // that makes every 4-column group of a k-block one aligned float4 of a staged row (the
@@ -54,32 +53,41 @@ struct FwdParams {
     int tpi, tiles;            // tiles per image, total tiles
     int pitch, lmargin;        // staged row slot: floats, and floats before the row data
     int xr;                    // row slots per stage buffer
-    int stages;                // kernel-bank ring depth
+    int stages;                // kernel-bank ring depth (smem)
+    int aslots;                // A slot ring depth (TMEM)
     int relu;
 };
 
-template <int NP>
+// MERGE (NP <= 96): the two products that share A_big run as ONE N = 2 NP MMA over the
+// stage's [small | big] bank rows into two accumulator halves, D[0, NP) = A_big B_small and
+// D[NP, 2 NP) = A_big B_big + A_small B_big, summed by the epilogue: 4 MMAs per k-block
+// instead of 6 (measured, tools/mma_rate.cu: an M = 128, K = 8 tf32 MMA costs ~77 cycles
+// at any N <= 128 and ~103 at N = 192).
+template <int NP, bool MG>
 struct FwdCfg {
-    static constexpr int ACC_COLS = NP;                                // one accumulator buffer
+    static constexpr bool MERGE = MG && NP <= 96;
+    static constexpr int ACC_COLS = MERGE ? 2 * NP : NP;               // one accumulator buffer
     static constexpr int A_COL = 2 * ACC_COLS;                         // double-buffered accumulators first
-    static constexpr int MAX_RING = (512 - A_COL) / 32 > 8 ? 8 : (512 - A_COL) / 32;  // A slots (big | small)
     static constexpr uint32_t B_BYTES = NP * kKB * 4;                 // one half of a ring stage
     static_assert(NP % 16 == 0 && NP <= 192, "tile width");
 };
-__host__ __device__ constexpr int max_ring(int np) { return (512 - 2 * np) / 32 > 8 ? 8 : (512 - 2 * np) / 32; }
+__host__ __device__ constexpr int acc_cols(int np, bool mg) { return (mg && np <= 96) ? 2 * np : np; }
+__host__ __device__ constexpr int max_aslots(int np, bool mg) {
+    return (512 - 2 * acc_cols(np, mg)) / 32 > 8 ? 8 : (512 - 2 * acc_cols(np, mg)) / 32;
+}
 
 // dynamic smem layout (bytes): [ring stages][row stage x2][zero row][k tables][barriers]
 struct FwdLayout {
     uint32_t ring, stage, zero, ktab, bars, total;
 };
-__host__ __device__ inline FwdLayout fwd_layout(int np, int stages, int xr, int pitch, int kgroups) {
+__host__ __device__ inline FwdLayout fwd_layout(int np, int stages, int aslots, int xr, int pitch, int kgroups) {
     FwdLayout L;
     L.ring = 0;
     L.stage = uint32_t(stages) * 2u * uint32_t(np) * kKB * 4u;
     L.zero = L.stage + 2u * uint32_t(xr) * uint32_t(pitch) * 4u;
     L.ktab = L.zero + uint32_t(pitch) * 4u;
     L.bars = (L.ktab + 2u * 4u * uint32_t(kgroups) * 4u + 15u) & ~15u;  // ktab + etab, 4 variants
-    L.total = L.bars + uint32_t(2 * stages + 8) * 8u + 16u;
+    L.total = L.bars + uint32_t(2 * stages + 2 * aslots + 8) * 8u + 16u;
     return L;
 }
 
@@ -111,23 +119,25 @@ __device__ __forceinline__ TileGeo tile_geo(const FwdParams& p, int T) {
     return t;
 }
 
-template <int NP>
+template <int NP, bool MG>
 __global__ void __launch_bounds__(kThreads, 1)
     conv_fwd_gather_kernel(const __grid_constant__ CUtensorMap tmB, const FwdParams p) {
-    using C_ = FwdCfg<NP>;
+    using C_ = FwdCfg<NP, MG>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int ngroups_k = p.kb_tile * 4;
-    const int R = p.stages;  // k-block ring: kernel-bank stage s and TMEM A slot s move together
-    const FwdLayout L = fwd_layout(NP, R, p.xr, p.pitch, ngroups_k);
+    const int RB = p.stages, RA = p.aslots;  // kernel-bank ring (smem), A slot ring (TMEM)
+    const FwdLayout L = fwd_layout(NP, RB, RA, p.xr, p.pitch, ngroups_k);
     float* zero_row = reinterpret_cast<float*>(smem + L.zero);
     int* ktab = reinterpret_cast<int*>(smem + L.ktab);   // [variant][group]: row | zero mask | byte offset
     int* etab = ktab + 4 * ngroups_k;                      // [variant][group]: run element of the group's column 0
-    // full[s]: the bank TMA (1 arrival + bytes) and the 4 gather warps of the k-block (4 arrivals)
-    // empty[s]: the MMA commit that frees bank stage s and A slot s together
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + L.bars);
-    uint64_t* empty = full + R;
-    uint64_t* xfull = empty + R;
+    // bfull / bempty: kernel-bank stage (TMA bytes / MMA commit); afull / aempty: A slot
+    // (the 4 gather warps of the k-block / MMA commit)
+    uint64_t* bfull = reinterpret_cast<uint64_t*>(smem + L.bars);
+    uint64_t* bempty = bfull + RB;
+    uint64_t* afull = bempty + RB;
+    uint64_t* aempty = afull + RA;
+    uint64_t* xfull = aempty + RA;
     uint64_t* xempty = xfull + 2;
     uint64_t* tfull = xempty + 2;
     uint64_t* tempty = tfull + 2;
@@ -164,9 +174,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (warp == 0 && lane == 0) {
         ptx::prefetch_tmap(&tmB);
-        for (int s = 0; s < R; ++s) {
-            ptx::mbar_init(&full[s], 1 + 4);
-            ptx::mbar_init(&empty[s], 1);
+        for (int s = 0; s < RB; ++s) {
+            ptx::mbar_init(&bfull[s], 1);
+            ptx::mbar_init(&bempty[s], 1);
+        }
+        for (int s = 0; s < RA; ++s) {
+            ptx::mbar_init(&afull[s], 4);
+            ptx::mbar_init(&aempty[s], 1);
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&xfull[a], 1);
@@ -192,15 +206,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x) {
                 const int row0 = variant_of(p, T / p.tpi) * 2 * p.o;  // this image's bank variant
                 for (int kb = 0; kb < p.kb_tile; ++kb) {
-                    ptx::mbar_wait_sleep(&empty[st], ph ^ 1);
+                    ptx::mbar_wait_sleep(&bempty[st], ph ^ 1);
                     if (ptx::elect_one()) {
-                        ptx::mbar_arrive_expect_tx(&full[st], 2 * C_::B_BYTES);
+                        ptx::mbar_arrive_expect_tx(&bfull[st], 2 * C_::B_BYTES);
                         uint8_t* dst = smem + L.ring + uint32_t(st) * 2 * C_::B_BYTES;
-                        ptx::tma_load_2d(dst, &tmB, &full[st], kb * kKB, row0);                      // big
-                        ptx::tma_load_2d(dst + C_::B_BYTES, &tmB, &full[st], kb * kKB, row0 + p.o);  // small
+                        ptx::tma_load_2d(dst, &tmB, &bfull[st], kb * kKB, row0);                      // small
+                        ptx::tma_load_2d(dst + C_::B_BYTES, &tmB, &bfull[st], kb * kKB, row0 + p.o);  // big
                     }
                     __syncwarp();
-                    if (++st == R) { st = 0; ph ^= 1; }
+                    if (++st == RB) { st = 0; ph ^= 1; }
                 }
             }
         }
@@ -209,9 +223,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // the whole warp runs the loop (warp-uniform operands), one elected lane issues
         {
             constexpr uint32_t idesc = ptx::idesc_tf32(kTileM, NP, 0, 0);
+            constexpr uint32_t idesc2 = ptx::idesc_tf32(kTileM, C_::MERGE ? 2 * NP : NP, 0, 0);
             const uint32_t ring_u = ptx::smem_u32(smem + L.ring);
-            int st = 0;
-            uint32_t ph = 0;
+            int bs = 0, as = 0;
+            uint32_t bph = 0, aph = 0;
             int lt = 0;
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
                 const int acc = lt & 1;
@@ -219,28 +234,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ptx::tc_fence_after();
                 const uint32_t d0 = tmem + uint32_t(acc * C_::ACC_COLS);
                 for (int kb = 0; kb < p.kb_tile; ++kb) {
-                    ptx::mbar_wait(&full[st], ph);
+                    ptx::mbar_wait(&bfull[bs], bph);
+                    ptx::mbar_wait(&afull[as], aph);
                     ptx::tc_fence_after();
-                    const uint32_t bbig = ring_u + uint32_t(st) * 2 * C_::B_BYTES;
-                    const uint32_t bsml = bbig + C_::B_BYTES;
-                    const uint32_t abig = tmem + uint32_t(C_::A_COL) + uint32_t(st) * 32, asml = abig + kKB;
+                    const uint32_t bsml = ring_u + uint32_t(bs) * 2 * C_::B_BYTES;  // [small | big] rows
+                    const uint32_t bbig = bsml + C_::B_BYTES;
+                    const uint32_t abig = tmem + uint32_t(C_::A_COL) + uint32_t(as) * 32, asml = abig + kKB;
                     const uint32_t first = kb ? 1u : 0u;
                     if (ptx::elect_one()) {
-                        // small products first, big * big last
+                        if constexpr (C_::MERGE) {
 #pragma unroll
-                        for (int kk = 0; kk < 2; ++kk)
-                            ptx::mma_tf32_ts(d0, asml + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc,
-                                             kk ? 1u : first);
+                            for (int kk = 0; kk < 2; ++kk) {
+                                // [A_big B_small | A_big B_big] (the first MMA of a tile clears both halves)
+                                ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 32, 16, 512, 4), idesc2,
+                                                 kk ? 1u : first);
+                                ptx::mma_tf32_ts(d0 + NP, asml + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4),
+                                                 idesc, 1u);
+                            }
+                        } else {
+                            // small products first, big * big last
 #pragma unroll
-                        for (int kk = 0; kk < 2; ++kk)
-                            ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 32, 16, 512, 4), idesc, 1u);
+                            for (int kk = 0; kk < 2; ++kk)
+                                ptx::mma_tf32_ts(d0, asml + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc,
+                                                 kk ? 1u : first);
 #pragma unroll
-                        for (int kk = 0; kk < 2; ++kk)
-                            ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc, 1u);
-                        ptx::mma_commit(&empty[st]);
+                            for (int kk = 0; kk < 2; ++kk)
+                                ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 32, 16, 512, 4), idesc, 1u);
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk)
+                                ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc, 1u);
+                        }
+                        ptx::mma_commit(&bempty[bs]);
+                        ptx::mma_commit(&aempty[as]);
                     }
                     __syncwarp();
-                    if (++st == R) { st = 0; ph ^= 1; }
+                    if (++bs == RB) { bs = 0; bph ^= 1; }
+                    if (++as == RA) { as = 0; aph ^= 1; }
                 }
                 if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
                 __syncwarp();
@@ -302,6 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 uint32_t v[32];
                 const uint32_t tc = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(acc * C_::ACC_COLS + c0);
                 ptx::tmem_ld_32x32b_x32(tc, v);
+                if constexpr (C_::MERGE) {
+                    uint32_t v2[32];
+                    ptx::tmem_ld_32x32b_x32(tc + NP, v2);
+                    ptx::tmem_ld_wait();
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] = __float_as_uint(__uint_as_float(v[j]) + __uint_as_float(v2[j]));
+                }
                 ptx::tmem_ld_wait();
                 if (!ok) continue;
                 const int nj = min(32, p.o - c0);  // channels of this chunk that exist (uniform)
@@ -351,7 +387,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // pass over the ring walked incrementally (no division by the runtime ring depth)
         uint32_t gbase = 0;  // gi of this tile's first k-block
         int sl = grp, pass = 0;
-        while (sl >= R) { sl -= R; ++pass; }
+        while (sl >= RA) { sl -= RA; ++pass; }
         int lt = 0;
         for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
             const int buf = lt & 1;
@@ -370,7 +406,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int* kt = ktab + variant_of(p, tg.q) * ngroups_k;
             ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
             for (int kb = int((uint32_t(grp) - gbase) & (kGatherGroups - 1)); kb < p.kb_tile; kb += kGatherGroups) {
-                if (pass > 0) ptx::mbar_wait_sleep(&empty[sl], (pass - 1) & 1);
+                // gather + split first; the slot is waited for only before the TMEM store
                 // the k-block's 4 group entries (uniform): filter row | zero mask | byte offset of
                 // the aligned float4; all four loads issued before any use (no branches between)
                 const int4 e4 = *reinterpret_cast<const int4*>(kt + kb * 4);
@@ -415,13 +451,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                         v[16 + 4 * g + u] = __float_as_uint(fa[u] - __uint_as_float(big));
                     }
                 }
+                if (pass > 0) ptx::mbar_wait_sleep(&aempty[sl], (pass - 1) & 1);
                 ptx::tmem_st_32x32b_x32(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C_::A_COL) + uint32_t(sl) * 32, v);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(&full[sl]);
+                if (lane == 0) ptx::mbar_arrive(&afull[sl]);
                 sl += kGatherGroups;
-                while (sl >= R) { sl -= R; ++pass; }
+                while (sl >= RA) { sl -= RA; ++pass; }
             }
             gbase += uint32_t(p.kb_tile);
             __syncwarp();
@@ -437,7 +474,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// kernel bank (o, k, k, d) -> per variant phi: [big rows | small rows] x Kp, filter row i's
+// kernel bank (o, k, k, d) -> per variant phi: [small rows | big rows] x Kp, filter row i's
 // k d run at columns [i segw + shift, ...) of its window (run_shift), zeros elsewhere
 __global__ void prep_bank_kernel(const float* __restrict__ w, float* __restrict__ w2, int o, int k, int d, int n,
                                  int pad, int segw, int kp, int nvar) {
@@ -452,7 +489,7 @@ __global__ void prep_bank_kernel(const float* __restrict__ w, float* __restrict_
         float v = 0.f;
         if (i < k && e >= 0 && e < seg) {
             v = w[(int64_t(oc) * k + i) * seg + e];
-            if (hr >= o) v -= __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+            if (hr < o) v -= __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);  // rows [0, o): small half
         }
         w2[idx] = v;
     }
@@ -484,7 +521,8 @@ bool make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t 
 }
 
 struct FwdPlan {
-    int np = 0, segw = 0, kp = 0, kb = 0, nvar = 1, xr = 0, pitch = 0, lmargin = 0, stages = 0;
+    int np = 0, segw = 0, kp = 0, kb = 0, nvar = 1, xr = 0, pitch = 0, lmargin = 0, stages = 0, aslots = 0;
+    bool merge = true;
     uint32_t smem = 0;
     bool ok = false;
 };
@@ -510,8 +548,11 @@ FwdPlan fwd_plan(const Geo& g) {
     P.lmargin = int((g.p * g.d + 4 + 3) & ~int64_t(3));
     P.pitch = int((P.lmargin + 3 + (g.n + g.p) * g.d + P.segw + 8 + 3) & ~int64_t(3));
     if (4 * (P.lmargin + 3 + P.segw) >= 32768) return P;  // byte offsets packed as int16
-    for (int st = max_ring(P.np); st >= 3; --st) {
-        const FwdLayout L = fwd_layout(P.np, st, P.xr, P.pitch, P.kb * 4);
+    P.merge = tuning(CCT_TUNE_GATHER) != 2;  // 2: the 6-MMA form (A/B)
+    P.aslots = max_aslots(P.np, P.merge);
+    if (P.aslots < kGatherGroups) return P;
+    for (int st = 12; st >= 3; --st) {
+        const FwdLayout L = fwd_layout(P.np, st, P.aslots, P.xr, P.pitch, P.kb * 4);
         if (L.total + 1024 <= uint32_t(kSmemMax)) {
             P.stages = st;
             P.smem = L.total + 1024;
@@ -522,9 +563,9 @@ FwdPlan fwd_plan(const Geo& g) {
     return P;
 }
 
-template <int NP>
+template <int NP, bool MG>
 cudaError_t launch_fwd(const CUtensorMap& tm, const FwdParams& fp, uint32_t smem, cudaStream_t st) {
-    auto kern = conv_fwd_gather_kernel<NP>;
+    auto kern = conv_fwd_gather_kernel<NP, MG>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
     const int grid = std::min(num_sms(), fp.tiles);
@@ -551,9 +592,10 @@ cudaError_t launch_fwd(const CUtensorMap& tm, const FwdParams& fp, uint32_t smem
 //   warp 2        TMEM allocator, then the row-stage producer      [xfull / xempty]
 //   warps 4-7     epilogue: TMEM -> partial dW (lanes = consecutive lowered columns)
 //   warps 8-11    dy transform: small = dy - trunc(dy) in smem     [bfull -> btdone]
-//   warps 12-27   four gather groups: unit (k-block, M-tile) u -> group u % 4
+//   warps 12-     one gather group (4 warps) per M-tile: group mt gathers unit (k-block, mt)
 // ===========================================================================
-constexpr int kWgThreads = 256 + 128 + 128 * kGatherGroups;
+template <int MT>
+constexpr int wg_threads() { return 256 + 128 + 128 * MT; }  // gather group mt owns M-tile mt
 constexpr int kWgChainKB = 256;  // k-blocks per accumulation chain (= kMaxChainKB)
 constexpr int kWgMaxMT = 3;      // M-tiles (k k d <= 384)
 
@@ -599,13 +641,13 @@ __device__ __forceinline__ int wg_tile_kb(const WgParams& p, int T) {
     return (min(P0 + kTileM, p.m * p.m) - P0 + kKB - 1) / kKB;
 }
 
-template <int NP, bool PAD>
-__global__ void __launch_bounds__(kWgThreads, 1)
+template <int NP, bool PAD, int MT>
+__global__ void __launch_bounds__(wg_threads<MT>(), 1)
     conv_wgrad_gather_kernel(const __grid_constant__ CUtensorMap tmB, const WgParams p) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr uint32_t HB = NP * kKB * 4;  // one half (raw or small) of a dy stage
-    const int RB = p.bstages, RA = p.aslots, MT = p.mt_tiles;
+    const int RB = p.bstages, RA = p.aslots;
     const WgLayout L = wg_layout(NP, RB, RA, p.xr, p.pitch);
     uint64_t* bfull = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* btdone = bfull + RB;
@@ -617,7 +659,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     uint64_t* tfull = xempty + 2;
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-    const uint32_t A_COL = uint32_t(MT * NP);  // A slots after the accumulators
+    constexpr uint32_t A_COL = uint32_t(MT * NP);  // A slots after the accumulators
 
     const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
@@ -633,7 +675,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         }
         for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&xfull[a], 1);
-            ptx::mbar_init(&xempty[a], 4 * kGatherGroups);
+            ptx::mbar_init(&xempty[a], 4 * MT);
         }
         ptx::mbar_init(tfull, 1);
         ptx::mbar_init(tempty, 4);
@@ -689,32 +731,42 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             for (int T = t0; T < t1; ++T) {
                 const int nkb = wg_tile_kb(p, T);
                 for (int kb = 0; kb < nkb; ++kb) {
-                    ptx::mbar_wait(&btdone[bs], bph);
-                    const uint32_t braw = ring_u + uint32_t(bs) * 2u * HB, bsml = braw + HB;
+                    // the k-block's MT units sit in consecutive A slots; one elected issue of all
+                    // 6 MT MMAs and the commits (few instructions per MMA: this warp's issue rate
+                    // bounded the kernel)
+                    int sl[MT];
+                    uint32_t sph[MT];
+#pragma unroll
                     for (int mt = 0; mt < MT; ++mt) {
-                        ptx::mbar_wait(&afull[as], aph);
-                        ptx::tc_fence_after();
-                        const uint32_t d0 = tmem + uint32_t(mt * NP);
-                        const uint32_t abig = tmem + A_COL + uint32_t(as) * 32, asml = abig + kKB;
-                        if (ptx::elect_one()) {
-#pragma unroll
-                            for (int kk = 0; kk < 2; ++kk)
-                                ptx::mma_tf32_ts(d0, asml + kk * 8, ptx::smem_desc(braw + kk * 1024, 2048, 512, 1), idesc,
-                                                 (first && kk == 0) ? 0u : 1u);
-#pragma unroll
-                            for (int kk = 0; kk < 2; ++kk)
-                                ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bsml + kk * 1024, 2048, 512, 1), idesc, 1u);
-#pragma unroll
-                            for (int kk = 0; kk < 2; ++kk)
-                                ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(braw + kk * 1024, 2048, 512, 1), idesc, 1u);
-                            ptx::mma_commit(&aempty[as]);
-                        }
-                        __syncwarp();
+                        sl[mt] = as;
+                        sph[mt] = aph;
                         if (++as == RA) { as = 0; aph ^= 1; }
                     }
-                    first = false;
-                    if (ptx::elect_one()) ptx::mma_commit(&bempty[bs]);
+                    ptx::mbar_wait(&btdone[bs], bph);
+#pragma unroll
+                    for (int mt = 0; mt < MT; ++mt) ptx::mbar_wait(&afull[sl[mt]], sph[mt]);
+                    ptx::tc_fence_after();
+                    const uint32_t braw = ring_u + uint32_t(bs) * 2u * HB;
+                    const uint64_t dr = ptx::smem_desc(braw, 2048, 512, 1);       // K step 0; step 1: +1024 B
+                    const uint64_t ds = ptx::smem_desc(braw + HB, 2048, 512, 1);
+                    if (ptx::elect_one()) {
+#pragma unroll
+                        for (int mt = 0; mt < MT; ++mt) {
+                            const uint32_t d0 = tmem + uint32_t(mt * NP);
+                            const uint32_t abig = tmem + A_COL + uint32_t(sl[mt]) * 32, asml = abig + kKB;
+                            // small products first, big * big last
+                            ptx::mma_tf32_ts(d0, asml, dr, idesc, first ? 0u : 1u);
+                            ptx::mma_tf32_ts(d0, asml + 8, dr + 64, idesc, 1u);
+                            ptx::mma_tf32_ts(d0, abig, ds, idesc, 1u);
+                            ptx::mma_tf32_ts(d0, abig + 8, ds + 64, idesc, 1u);
+                            ptx::mma_tf32_ts(d0, abig, dr, idesc, 1u);
+                            ptx::mma_tf32_ts(d0, abig + 8, dr + 64, idesc, 1u);
+                            ptx::mma_commit(&aempty[sl[mt]]);
+                        }
+                        ptx::mma_commit(&bempty[bs]);
+                    }
                     __syncwarp();
+                    first = false;
                     if (++bs == RB) { bs = 0; bph ^= 1; }
                 }
             }
@@ -804,7 +856,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             for (int T = t0; T < t1; ++T) {
                 const int nkb = wg_tile_kb(p, T);
                 for (int kb = 0; kb < nkb; ++kb) {
-                    ptx::mbar_wait(&bfull[st], ph);
+                    ptx::mbar_wait_sleep(&bfull[st], ph);
                     const uint32_t braw = ring_u + uint32_t(st) * 2u * HB;
 #pragma unroll
                     for (int i = t; i < int(HB / 16); i += 128) {
@@ -819,24 +871,22 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             }
         }
     } else if (warp >= 12) {
-        // ===================== gather groups =====================
-        const int grp = (warp - 12) >> 2;
+        // ===================== gather groups: group mt owns M-tile mt =====================
+        const int mt = (warp - 12) >> 2;
         const int qd = warp & 3;
         const uint32_t stage_u = ptx::smem_u32(smem + L.stage);
         const uint32_t pitch_b = uint32_t(p.pitch) * 4u;
-        // per M-tile lane constants: lowered column -> filter row i, run element e, filter column j
-        int li[kWgMaxMT], le[kWgMaxMT], lj[kWgMaxMT], lph[kWgMaxMT];
-#pragma unroll
-        for (int mt = 0; mt < kWgMaxMT; ++mt) {
-            const int col = min(mt * kTileM + qd * 32 + lane, p.kkd - 1);
-            li[mt] = col / p.kd;
-            le[mt] = col - li[mt] * p.kd;
-            lj[mt] = le[mt] / p.d;
-            lph[mt] = int((int64_t(li[mt]) * nd) & 3);
-        }
-        int u = 0;                    // unit counter (k-block, M-tile) of this CTA
-        int sl = grp, pass = 0;       // A slot / pass of this group's next unit (unit grp first)
+        // lane constants: lowered column -> filter row i, run element e, filter column j;
+        // loff = the lane's byte offset within the staged row of filter row i
+        const int col = min(mt * kTileM + qd * 32 + lane, p.kkd - 1);
+        const bool cok = mt * kTileM + qd * 32 + lane < p.kkd;
+        const int li = col / p.kd, le = col - li * p.kd, lj = le / p.d;
+        const uint32_t loff = uint32_t(li) * pitch_b + 4u * uint32_t(p.lmargin + le - p.p * p.d);
+        const uint32_t lph = uint32_t((int64_t(li) * nd) & 3);
+        // unit u = gk MT + mt (gk: the CTA's k-block counter) sits in A slot u % RA, pass u / RA
+        int sl = mt, pass = 0;
         while (sl >= RA) { sl -= RA; ++pass; }
+        int gk = 0;  // CTA k-block counter at the start of the current tile
         int lt = 0;
         for (int c = blockIdx.x; c < p.chains; c += gridDim.x) {
             int t0, t1;
@@ -849,46 +899,54 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int nkb = (P1 - P0 + kKB - 1) / kKB;
                 const uint32_t sbase = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b;
                 ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
+                int r0 = P0 / p.m, c0 = P0 - r0 * p.m;  // first pixel of k-block kb
                 for (int kb = 0; kb < nkb; ++kb) {
-#pragma unroll
-                    for (int mt = 0; mt < kWgMaxMT; ++mt) {
-                        if (mt >= MT) break;
-                        if (((u++) & (kGatherGroups - 1)) != grp) continue;
-                        if (pass > 0) ptx::mbar_wait_sleep(&aempty[sl], (pass - 1) & 1);
-                        const int col = mt * kTileM + qd * 32 + lane;
-                        const bool cok = col < p.kkd;
-                        // lane part of the staged address: filter row i's slot, run element e
-                        const uint32_t lbase = sbase + uint32_t(li[mt]) * pitch_b + uint32_t(p.lmargin + le[mt]) * 4u;
-                        int P = P0 + kb * kKB;
-                        int r = P / p.m, cc = P - r * p.m;
-                        uint32_t v[32];
-#pragma unroll
-                        for (int jj = 0; jj < kKB; ++jj) {
-                            // pixel (r, cc): staged row s (r - ra) + i, row phase of input row s r - p + i
-                            const int ph4 = int(((int64_t(q) * p.n + p.s * r - p.p) * nd + lph[mt]) & 3);
-                            const uint32_t addr = lbase + uint32_t(p.s * (r - ra)) * pitch_b +
-                                                  uint32_t(((p.s * cc - p.p) * p.d + ph4) * 4);
-                            float f = ptx::lds32(addr);
-                            bool ok = cok && (P + jj < P1);
-                            if constexpr (PAD) {
-                                ok = ok && unsigned(p.s * r - p.p + li[mt]) < unsigned(p.n) &&
-                                     unsigned(p.s * cc - p.p + lj[mt]) < unsigned(p.n);
-                            }
-                            f = ok ? f : 0.f;
-                            const uint32_t big = __float_as_uint(f) & 0xFFFFE000u;
-                            v[jj] = big;
-                            v[kKB + jj] = __float_as_uint(f - __uint_as_float(big));
-                            if (++cc == p.m) { cc = 0; ++r; }
-                        }
-                        ptx::tmem_st_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + A_COL + uint32_t(sl) * 32, v);
-                        ptx::tmem_st_wait();
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(&afull[sl]);
-                        sl += kGatherGroups;
-                        while (sl >= RA) { sl -= RA; ++pass; }
+                    // the k-block's 16 pixels lie in output row r0 (jj < split) and r0 + 1 (m >= 16);
+                    // pixel jj's staged address = row base + jj s d floats (uniform stride)
+                    const int split = p.m - c0;
+                    const int nval = P1 - (P0 + kb * kKB);
+                    const bool two = split < kKB && nval > split;  // row r0 + 1 is staged and used
+                    // float offset mod 4 of input row s r - p + i of image q
+                    const uint32_t ph0 = uint32_t(q * p.n + p.s * r0 - p.p) * uint32_t(nd) + lph;
+                    const uint32_t ph1 = ph0 + uint32_t(p.s * nd);
+                    const uint32_t sd4 = uint32_t(p.s * p.d) * 4u;
+                    const uint32_t rb0 = sbase + uint32_t(p.s * (r0 - ra)) * pitch_b + loff +
+                                         4u * ((ph0 & 3u) + uint32_t(p.s * c0 * p.d));
+                    const uint32_t rb1 = two ? sbase + uint32_t(p.s * (r0 + 1 - ra)) * pitch_b + loff +
+                                                   4u * (ph1 & 3u) - uint32_t(split) * sd4
+                                             : rb0;
+                    bool rv0 = true, rv1 = true;
+                    if constexpr (PAD) {
+                        rv0 = unsigned(p.s * r0 - p.p + li) < unsigned(p.n);
+                        rv1 = unsigned(p.s * (r0 + 1) - p.p + li) < unsigned(p.n);
                     }
+                    uint32_t v[32];
+#pragma unroll
+                    for (int jj = 0; jj < kKB; ++jj) {
+                        const bool second = jj >= split;
+                        float f = ptx::lds32((second ? rb1 : rb0) + uint32_t(jj) * sd4);
+                        bool ok = cok && jj < nval;
+                        if constexpr (PAD) {
+                            const int cc = second ? jj - split : c0 + jj;
+                            ok = ok && (second ? rv1 : rv0) && unsigned(p.s * cc - p.p + lj) < unsigned(p.n);
+                        }
+                        f = ok ? f : 0.f;
+                        const uint32_t big = __float_as_uint(f) & 0xFFFFE000u;
+                        v[jj] = big;
+                        v[kKB + jj] = __float_as_uint(f - __uint_as_float(big));
+                    }
+                    if (pass > 0) ptx::mbar_wait_sleep(&aempty[sl], (pass - 1) & 1);  // gathered before the wait
+                    ptx::tmem_st_32x32b_x32(tmem + (uint32_t(qd * 32) << 16) + A_COL + uint32_t(sl) * 32, v);
+                    ptx::tmem_st_wait();
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&afull[sl]);
+                    sl += MT;
+                    while (sl >= RA) { sl -= RA; ++pass; }
+                    c0 += kKB;
+                    if (c0 >= p.m) { c0 -= p.m; ++r0; }
                 }
+                gk += nkb;
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&xempty[buf]);
             }
@@ -925,14 +983,14 @@ struct WgPlan {
 WgPlan wg_plan(const Geo& g) {
     WgPlan P;
     const int64_t kkd = g.k * g.k * g.d, mm = g.m * g.m;
-    if (g.o < 1 || g.o > 128 || g.o % 4 != 0 || kkd > int64_t(kWgMaxMT) * kTileM || g.m < 1 || g.k > 32) return P;
+    if (g.o < 1 || g.o > 128 || g.o % 4 != 0 || kkd > int64_t(kWgMaxMT) * kTileM || g.m < kKB || g.k > 32) return P;
     if (g.b * g.n * g.n * g.d >= (int64_t(1) << 40) || g.b * mm >= (int64_t(1) << 31) - kTileM ||
         g.n * g.n * g.d >= (int64_t(1) << 30) || g.o * kkd * 4096 >= (int64_t(1) << 40))
         return P;
     P.np = int((g.o + 31) / 32 * 32);
     P.mt = int((kkd + kTileM - 1) / kTileM);
     P.aslots = std::min(8, (512 - P.mt * P.np) / 32);
-    if (P.aslots < kGatherGroups) return P;
+    if (P.aslots < 4) return P;
     const int64_t rows_span = (kTileM - 1) / g.m + 2 > g.m ? g.m : (kTileM - 1) / g.m + 2;
     P.xr = int(g.s * (rows_span - 1) + g.k);
     P.lmargin = int((g.p * g.d + 4 + 3) & ~int64_t(3));
@@ -1009,12 +1067,13 @@ cudaError_t gather_fwd(const Geo& g, const float* x, const float* w, float* y, i
     fp.lmargin = P.lmargin;
     fp.xr = P.xr;
     fp.stages = P.stages;
+    fp.aslots = P.aslots;
     switch (P.np) {
-        case 32: return launch_fwd<32>(tm, fp, P.smem, st);
-        case 64: return launch_fwd<64>(tm, fp, P.smem, st);
-        case 96: return launch_fwd<96>(tm, fp, P.smem, st);
-        case 128: return launch_fwd<128>(tm, fp, P.smem, st);
-        default: return launch_fwd<192>(tm, fp, P.smem, st);
+        case 32: return P.merge ? launch_fwd<32, true>(tm, fp, P.smem, st) : launch_fwd<32, false>(tm, fp, P.smem, st);
+        case 64: return P.merge ? launch_fwd<64, true>(tm, fp, P.smem, st) : launch_fwd<64, false>(tm, fp, P.smem, st);
+        case 96: return P.merge ? launch_fwd<96, true>(tm, fp, P.smem, st) : launch_fwd<96, false>(tm, fp, P.smem, st);
+        case 128: return launch_fwd<128, false>(tm, fp, P.smem, st);
+        default: return launch_fwd<192, false>(tm, fp, P.smem, st);
     }
 }
 
@@ -1066,17 +1125,23 @@ cudaError_t gather_wgrad(const Geo& g, const float* x, const float* dy, float* d
         auto go = [&](auto kern) {
             e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(P.smem));
             if (e == cudaSuccess) {
-                kern<<<P.grid, kWgThreads, P.smem, st>>>(tm, wp);
+                kern<<<P.grid, 384 + 128 * P.mt, P.smem, st>>>(tm, wp);
                 note_launch();
                 e = cudaGetLastError();
             }
         };
         const bool pad = g.p > 0;
-        switch (P.np) {
-            case 32: pad ? go(conv_wgrad_gather_kernel<32, true>) : go(conv_wgrad_gather_kernel<32, false>); break;
-            case 64: pad ? go(conv_wgrad_gather_kernel<64, true>) : go(conv_wgrad_gather_kernel<64, false>); break;
-            case 96: pad ? go(conv_wgrad_gather_kernel<96, true>) : go(conv_wgrad_gather_kernel<96, false>); break;
-            default: pad ? go(conv_wgrad_gather_kernel<128, true>) : go(conv_wgrad_gather_kernel<128, false>); break;
+        switch (P.np * 10 + P.mt) {
+#define CCT_WG_CASE(NP_, MT_)                                                                        \
+    case NP_ * 10 + MT_:                                                                             \
+        pad ? go(conv_wgrad_gather_kernel<NP_, true, MT_>) : go(conv_wgrad_gather_kernel<NP_, false, MT_>); \
+        break;
+            CCT_WG_CASE(32, 1) CCT_WG_CASE(32, 2) CCT_WG_CASE(32, 3)
+            CCT_WG_CASE(64, 1) CCT_WG_CASE(64, 2) CCT_WG_CASE(64, 3)
+            CCT_WG_CASE(96, 1) CCT_WG_CASE(96, 2) CCT_WG_CASE(96, 3)
+            CCT_WG_CASE(128, 1) CCT_WG_CASE(128, 2) CCT_WG_CASE(128, 3)
+#undef CCT_WG_CASE
+            default: return cudaErrorInvalidValue;
         }
         if (e != cudaSuccess) return e;
     }

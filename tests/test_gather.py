@@ -108,8 +108,9 @@ def test_gather_fwd_bias_relu(cct, dev, orc):
 
 # ---------------------------------------------------------------------------
 # fused backward-weight (conv_wgrad_gather_kernel): dW^T = lowered(x)^T dy with the
-# lowered columns gathered into TMEM; o % 4 == 0, o <= 128, k k d <= 384
-WGEOMS = [g for g in GEOMS if g[3] % 4 == 0 and g[3] <= 128 and g[1] * g[1] * g[2] <= 384]
+# lowered columns gathered into TMEM; o % 4 == 0, o <= 128, k k d <= 384, m >= 16
+WGEOMS = [g for g in GEOMS if g[3] % 4 == 0 and g[3] <= 128 and g[1] * g[1] * g[2] <= 384 and
+          (g[0] + 2 * g[6] - g[1]) // g[5] + 1 >= 16]
 
 
 @pytest.mark.parametrize("layout", [0, 1], ids=["nchw", "nhwc"])
