@@ -23,6 +23,7 @@
 #include "s2d.cuh"
 #include "epilogue.cuh"
 #include "gather.cuh"
+#include "dgrad.cuh"
 
 namespace cct {
 uint64_t launch_count();
@@ -189,6 +190,10 @@ bool t1_gather_fwd(const Geo& g, int type) {
 }
 bool t1_gather_wgrad(const Geo& g, int type) {
     return tuning(CCT_TUNE_GATHER) && implicit_enabled() && type == 1 && !im2col_ok(g.d, true) && gather_wgrad_ok(g);
+}
+// ... and backward-data folds the horizontal overlap of dDhat in the GEMM epilogue (dgrad.cuh)
+bool t1_hfold_dgrad(const Geo& g, int type) {
+    return tuning(CCT_TUNE_GATHER) && implicit_enabled() && type == 1 && !im2col_ok(g.d, true) && hfold_dgrad_ok(g);
 }
 
 // planning runs (no workspace) still need non-null, aligned operand pointers so
@@ -586,6 +591,17 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
 
 cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
                        float* dx, float* dw, Ws& ws, cudaStream_t st) {
+    if (dx && t1_hfold_dgrad(g, type) && aligned16(or_plan(dy, ws)) && aligned16(or_plan(dx, ws))) {
+        const size_t mark = ws.off;
+        float* w2 = ws.take(hfold_dgrad_ws_floats(g));
+        if (ws.base) CCT_TRY(hfold_dgrad(g, dy, w, dx, w2, st), "fused backward-data");
+        if (!dw) return CCT_OK;
+        const size_t hi = ws.off;
+        ws.off = mark;  // stream order: the backward-weight may reuse the backward-data scratch
+        cct_status s = run_bwd_one(g, type, x, cache, dy, w, nullptr, dw, ws, st);
+        ws.off = std::max(hi, ws.off);
+        return s;
+    }
     if (t1_s2d(g, type)) {
         // the stride-1 backward of the blocked layer, then the depth-to-space gathers
         const Geo v = s2d_geo(g);

@@ -164,3 +164,67 @@ def test_gather_wgrad_full_batch(cct, dev):
     assert err <= TOL, f"rel-L2 {err:.3e}"
     dx, dw2 = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x)
     assert torch.equal(dw2, dw)
+
+
+# ---------------------------------------------------------------------------
+# fused backward-data (conv_dgrad_hfold_kernel + vfold_kernel): dDhat never reaches HBM,
+# the horizontal overlap is folded in the GEMM epilogue, the vertical one by a streaming pass.
+# Instantiated fold geometries (k d, s d): (33, 12) conv1 / AlexNet conv1, (20, 8), (28, 16).
+DGEOMS = [
+    (227, 11, 3, 96, 2, 4, 0),   # CaffeNet conv1
+    (224, 11, 3, 64, 2, 4, 2),   # torchvision AlexNet conv1 (pad 2)
+    (63, 11, 3, 96, 1, 4, 5),    # pad > k / 2, m = 16
+    (31, 5, 4, 32, 2, 2, 1),     # k d = 20, s d = 8, ragged right edge
+    (40, 7, 4, 48, 3, 4, 3),     # k d = 28, s d = 16
+]
+
+
+@pytest.mark.parametrize("layout", [0, 1], ids=["nchw", "nhwc"])
+@pytest.mark.parametrize("geom", DGEOMS, ids=[f"n{g[0]}k{g[1]}d{g[2]}o{g[3]}s{g[5]}p{g[6]}" for g in DGEOMS])
+def test_hfold_dgrad_vs_oracle(cct, dev, orc, geom, layout):
+    """dx against the oracle's backward-data (the adjoint of tensor.cpp:77-106) at rel-L2 <=
+    1e-4, bitwise repeatable, and in agreement with the materialised Type 1 path."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = geom
+    desc = cct.ConvDesc(n, k, d, o, b, s, p, layout)
+    _, w = orc.random_problem(23 + n, b, n, d, k, o)
+    m = desc.m
+    dy = orc.uniform(24 + n, b * o * m * m)  # NCHW order
+    ref = orc.conv_bwd_data(dy, w, b, n, d, k, o, s, p)
+    wt = torch.from_numpy(w).to(dev).view(o, k, k, d)
+    dyt = torch.from_numpy(dy).to(dev).view(b, o, m, m)
+    if layout:
+        dyt = dyt.permute(0, 2, 3, 1).contiguous()
+    dx = conv.conv_bwd_data(dyt, wt, desc, cct.LOWER_T1)
+    err = rel_l2(dx.cpu().numpy().ravel(), ref)
+    assert err <= TOL, f"rel-L2 {err:.3e}"
+    assert torch.equal(conv.conv_bwd_data(dyt, wt, desc, cct.LOWER_T1), dx)
+    with cct.tuning(gather=0):
+        dx0 = conv.conv_bwd_data(dyt, wt, desc, cct.LOWER_T1)
+    assert rel_l2(dx.cpu().numpy().ravel(), dx0.cpu().numpy().ravel()) <= TOL
+
+
+def test_hfold_dgrad_full_batch(cct, dev):
+    """conv1 at b = 256 (BASELINE configs[2]): dx against an fp64 torch reference (fold of the
+    fp64 lowered product), and the combined backward (dx + dW in one call)."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = 227, 11, 3, 96, 256, 4, 0
+    desc = cct.ConvDesc(n, k, d, o, b, s, p, cct.NHWC)
+    g = torch.Generator(device=dev).manual_seed(31)
+    m = desc.m
+    dy = torch.rand((b, m, m, o), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    dx = conv.conv_bwd_data(dy, w, desc, cct.LOWER_T1)
+    wm = w.permute(0, 3, 1, 2).reshape(o, d * k * k).double()                  # (o, d k k) unfold order
+    num = den = 0.0
+    for q0 in range(0, b, 32):
+        cols = torch.einsum("bpo,oc->bcp", dy[q0:q0 + 32].reshape(-1, m * m, o).double(), wm)
+        ref = torch.nn.functional.fold(cols, (n, n), k, stride=s, padding=p)  # (bq, d, n, n)
+        got = dx[q0:q0 + 32].permute(0, 3, 1, 2).double()
+        num += float(((got - ref) ** 2).sum())
+        den += float((ref ** 2).sum())
+    err = (num / den) ** 0.5
+    assert err <= TOL, f"rel-L2 {err:.3e}"
+    dx2, _ = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x)
+    assert torch.equal(dx2, dx)
