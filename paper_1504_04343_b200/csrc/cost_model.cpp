@@ -17,6 +17,8 @@
 #include <cstdlib>
 
 #include "cct.h"
+#include "dgrad.cuh"
+#include "gather.cuh"
 
 namespace {
 
@@ -38,18 +40,18 @@ double rup(double v, double q) { return std::ceil(v / q) * q; }
 
 // Measured steady-state 3xTF32 GEMM rate (TF/s) of gemm3xtf32_kernel on B200 by
 // tile width BN (rows) and reduction length K (cols): tools/gemm_bench.py
-// --rate-table (M >= 16 tiles per CTA pair), profiles/r01/gemm_rate_table.json.
-// Longer K is chain-split at 4096.  Pipeline fill is added per launch.
+// --rate-table (M >= 16 tiles per CTA pair), re-measured on the round-2 build (warp-uniform
+// MMA / TMA issue): profiles/r02/gemm_rate_table.json.  Longer K is chain-split at 4096.
 const double kBN[5] = {64, 96, 128, 192, 256};
 const double kK[4] = {64, 256, 1024, 4096};
 const double kRate[5][4] = {
-    {64.4, 93.9, 106.5, 108.4},  // BN 64
-    {95.6, 138.0, 158.4, 161.9},  // BN 96
-    {111.0, 169.3, 196.2, 203.0},  // BN 128
-    {132.1, 214.8, 242.4, 250.8},  // BN 192
-    {128.2, 249.0, 281.7, 276.9},  // BN 256
+    {76.7, 147.5, 165.2, 170.4},   // BN 64
+    {98.2, 185.8, 208.4, 216.2},   // BN 96
+    {112.7, 193.2, 218.9, 226.6},  // BN 128
+    {119.6, 240.0, 278.8, 292.4},  // BN 192
+    {94.1, 193.7, 270.2, 300.1},   // BN 256
 };
-const double kRateRef = 276.9e12;  // table entry the calibration's gemm_flops_per_s scales
+const double kRateRef = 300.1e12;  // table entry the calibration's gemm_flops_per_s scales
 
 double interp_rate(double bn, double k) {
     auto pos = [](const double* xs, int n, double v, int* i0, double* f) {
@@ -149,24 +151,73 @@ G s2d_of(const G& g) {
 }
 
 void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* secs, double* bytes,
-              bool allow_s2d = true);
+              bool allow_s2d = true, bool allow_fused = true);
 
 // model seconds of a strided Type 1 pass with (true) / without the space-to-depth form
 double t1_form_seconds(const G& g, int pass, bool s2d, const cct_calibration* c) {
     double secs = 0, bytes = 0;
-    one_pass(g, 1, pass, c, &secs, &bytes, s2d);
+    one_pass(g, 1, pass, c, &secs, &bytes, s2d, false);  // (the unfused forms)
     return secs;
 }
 
 // counts + model for one pass.  pass: 0 fwd, 1 bwd-data, 2 bwd-weight, 3 training step.
 // A strided Type 1 layer takes the faster of its direct and space-to-depth forms,
 // as the launcher does (cct::prefer_s2d).
+// Small-channel Type 1 layers the launcher runs fused (cct_abi.cu t1_gather_fwd /
+// t1_gather_wgrad / t1_hfold_dgrad: d % 16 != 0 and the fused kernels' geometry limits).
+cct::Geo geo_cct(const G& g) {
+    cct::Geo v;
+    v.b = int64_t(g.b); v.n = int64_t(g.n); v.d = int64_t(g.d); v.k = int64_t(g.k); v.o = int64_t(g.o);
+    v.s = int64_t(g.s); v.p = int64_t(g.p); v.N = int64_t(g.N); v.m = int64_t(g.m); v.R = int64_t(g.R);
+    v.yl = 1;
+    return v;
+}
+bool fused_small(const G& g) {
+    return cct_get_tuning(CCT_TUNE_GATHER) != 0 && cct_get_implicit_lowering() && std::fmod(g.d, 16) != 0;
+}
+
 void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* secs, double* bytes,
-              bool allow_s2d) {
+              bool allow_s2d, bool allow_fused) {
     const double f = 4.0;  // bytes per float
+    // fused small-channel Type 1 passes (gather.cuh, dgrad.cuh): executed flops at the rates
+    // measured on B200 for CaffeNet conv1 (b = 256, profiles/r02): forward 0.65, backward-weight
+    // 0.59, backward-data GEMM 0.57 of the table GEMM rate; the backward-data's vertical fold
+    // streams its partial rows at 1.15 x the lowering copy rate
+    if (type == 1 && allow_fused && fused_small(g)) {
+        const cct::Geo v = geo_cct(g);
+        const bool fw = cct::gather_fwd_ok(v), wg = cct::gather_wgrad_ok(v), dg = cct::hfold_dgrad_ok(v);
+        if (fw || wg || dg) {
+            double t = 0, by = 0, launches = 0;
+            const double flops = 2.0 * g.b * g.m * g.m * g.k * g.k * g.d * g.o;
+            const double xin = g.b * g.n * g.n * g.d * f, yout = g.b * g.o * g.m * g.m * f;
+            const double rate = c->gemm_flops_per_s;
+            double sf = 0, bf = 0, sw = 0, bw = 0, sd = 0, bd = 0;
+            if (fw) { sf = flops / (0.65 * rate); bf = xin + yout; }
+            else one_pass(g, 1, 0, c, &sf, &bf, allow_s2d, false);
+            if (wg) { sw = flops / (0.59 * rate); bw = xin + yout; }
+            else one_pass(g, 1, 2, c, &sw, &bw, allow_s2d, false);
+            if (dg) {
+                const double xp = std::ceil((g.s * g.d * (g.m - 1) + g.k * g.d + 6) / 4) * 4;
+                const double h = g.b * g.m * g.k * xp * f;
+                sd = flops / (0.57 * rate) + (h + xin) / (1.15 * c->hbm_bytes_per_s);
+                bd = 2 * yout + 2 * h + xin;
+                launches += 1;
+            } else {
+                one_pass(g, 1, 1, c, &sd, &bd, allow_s2d, false);
+            }
+            launches += 2;
+            if (pass == 0) { t = sf; by = bf; }
+            else if (pass == 1) { t = sd; by = bd; }
+            else if (pass == 2) { t = sw; by = bw; }
+            else { t = sf + sd + sw; by = bf + bd + bw; }
+            *secs = t + (pass == 3 ? 3 : 1) * launches / 3 * c->launch_s;
+            *bytes = by;
+            return;
+        }
+    }
     if (type == 1 && allow_s2d && s2d_possible(g)) {
         double s0 = 0, b0 = 0, s1 = 0, b1 = 0;
-        one_pass(g, 1, pass, c, &s0, &b0, false);
+        one_pass(g, 1, pass, c, &s0, &b0, false, allow_fused);
         const G v = s2d_of(g);
         one_pass(v, 1, pass, c, &s1, &b1, false);
         const double xin = g.b * g.n * g.n * g.d * f, xs = v.b * v.n * v.n * v.d * f;
@@ -205,9 +256,9 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
         return wg_swap ? gemm_seconds(g.o, wg_cols, rows, c) * 1.46 : gemm_seconds(wg_cols, ncols, rows, c) * wg_slow;
     };
     double t = 0, by = 0, launches = 0;
-    // measured class rates (sweep, profiles/r01): lift and expand gather, so they
-    // run below the copy-like lower / col2im kernels
-    const double lift_bw = c->hbm_bytes_per_s * 0.64, expand_bw = c->hbm_bytes_per_s * 0.42;
+    // measured class rates (configs[1] sweep on the round-2 build, profiles/r02): the staged
+    // lift streams at ~0.88 and the plane expand at ~0.77 of the lower / col2im copy rate
+    const double lift_bw = c->hbm_bytes_per_s * 0.88, expand_bw = c->hbm_bytes_per_s * 0.77;
     auto hbm = [&](double b) { by += b; t += b / c->hbm_bytes_per_s; launches += 1; };
     auto hbm_at = [&](double b, double bw) { by += b; t += b / bw; launches += 1; };
     const double a_in = t1_implicit ? xin : dhat;         // bytes of the A operand stream
@@ -312,7 +363,7 @@ extern "C" {
 void cct_calibration_default(cct_calibration* cal) {
     if (!cal) return;
     cal->hbm_bytes_per_s = 4.15e12;  // measured lower / col2im rate (sweep, profiles/r01)
-    cal->gemm_flops_per_s = 276.9e12; // measured 3xTF32 rate at BN 256, K 4096 (rate table)
+    cal->gemm_flops_per_s = 300.1e12; // measured 3xTF32 rate at BN 256, K 4096 (rate table, round 2)
     cal->launch_s = 5e-6;
     cal->alpha = 4.0 / cal->hbm_bytes_per_s * 2.0;  // one element read + written
     cal->beta = 1.0 / cal->gemm_flops_per_s;

@@ -42,6 +42,10 @@ __device__ __forceinline__ int fdiv(int v, int d, float inv) {
     return qv;
 }
 
+// One block per (image, kG output channels).  A thread owns output pixels (pix, pix + kThreads,
+// ...) and, for each, walks the kG channels and their k^a taps: its (row, column) split is done
+// once per pixel, and the kG x k^a loads of a pixel are independent (memory-level parallelism;
+// consecutive threads read consecutive floats of a tap plane).
 template <int TYPE, bool NHWC>
 __global__ void __launch_bounds__(kThreads) lift_planes_kernel(const float* __restrict__ rh, float* __restrict__ y,
                                                                Geo g) {
@@ -50,30 +54,51 @@ __global__ void __launch_bounds__(kThreads) lift_planes_kernel(const float* __re
     const int taps = TYPE == 2 ? k : k * k;
     const int64_t rpi = TYPE == 2 ? int64_t(R) * m : int64_t(R) * R;
     const int ngroups = (o + kG - 1) / kG;
-    const float inv_mm = 1.f / float(mm), inv_m = 1.f / float(m);
+    const float inv_m = 1.f / float(m);
+    // tap strides within a channel's plane block: i (row tap), j (column tap, T3)
+    const int64_t si = TYPE == 2 ? rpi + m : int64_t(k) * rpi + R, sj = rpi + 1;
     for (int64_t blk = blockIdx.x; blk < g.b * ngroups; blk += gridDim.x) {
         const int64_t q = blk / ngroups;
         const int oj0 = int(blk - q * ngroups) * kG;
         const int G = min(kG, o - oj0);
-        for (int e = threadIdx.x; e < G * mm; e += kThreads) {
-            const int gl = fdiv(e, mm, inv_mm), pix = e - gl * mm;
+        const float* pl0 = rh + (q * o + oj0) * int64_t(taps) * rpi;
+        for (int pix = threadIdx.x; pix < mm; pix += kThreads) {
             const int r = fdiv(pix, m, inv_m), c = pix - r * m;
-            const float* pl = rh + (q * o + oj0 + gl) * int64_t(taps) * rpi;
-            float a = 0.f;
+            const int64_t off = TYPE == 2 ? int64_t(s) * r * m + c : int64_t(s) * r * R + int64_t(s) * c;
+            float a[kG];
+#pragma unroll
+            for (int gl = 0; gl < kG; ++gl) a[gl] = 0.f;
+            const float* p0 = pl0 + off;
+            const int64_t sg = int64_t(taps) * rpi;  // channel stride
+            // taps i then j ascending per channel (lift_kernel's order); the kG channels' loads
+            // of a tap are independent
+            // (measured: T2 fastest with the channels innermost, T3 with each channel's k x k
+            // taps innermost -- 2.0 vs 0.4 TB/s and 2.2 vs 1.2 TB/s)
             if constexpr (TYPE == 2) {
-                const float* p0 = pl + int64_t(s) * r * m + c;
-#pragma unroll 4
-                for (int i = 0; i < k; ++i) a += __ldg(p0 + i * (rpi + m));
-            } else {
-                const float* p0 = pl + int64_t(s) * r * R + int64_t(s) * c;
                 for (int i = 0; i < k; ++i) {
-                    const float* pi = p0 + i * (int64_t(k) * rpi + R);
-#pragma unroll 4
-                    for (int j = 0; j < k; ++j) a += __ldg(pi + j * (rpi + 1));
+#pragma unroll
+                    for (int gl = 0; gl < kG; ++gl)
+                        if (gl < G) a[gl] += __ldg(p0 + gl * sg + i * si);
+                }
+            } else {
+#pragma unroll
+                for (int gl = 0; gl < kG; ++gl) {
+                    if (gl < G) {
+                        for (int i = 0; i < k; ++i) {
+                            const float* pi = p0 + gl * sg + i * si;
+#pragma unroll 3
+                            for (int j = 0; j < k; ++j) a[gl] += __ldg(pi + j * sj);
+                        }
+                    }
                 }
             }
-            if constexpr (NHWC) acc_s[e] = a;
-            else y[(q * o + oj0) * mm + e] = a;
+#pragma unroll
+            for (int gl = 0; gl < kG; ++gl) {
+                if (gl < G) {
+                    if constexpr (NHWC) acc_s[gl * mm + pix] = a[gl];
+                    else y[(q * o + oj0 + gl) * mm + pix] = a[gl];
+                }
+            }
         }
         if constexpr (NHWC) {
             __syncthreads();
@@ -87,6 +112,63 @@ __global__ void __launch_bounds__(kThreads) lift_planes_kernel(const float* __re
     }
 }
 
+// Staged variant: the block's contiguous run of tap planes (G channels x k^a planes of rpi
+// floats) is streamed into shared memory with coalesced loads first, so the HBM read is one
+// sequential stream per block; the k^a-tap sums then read shared memory (same summation order).
+template <int TYPE, bool NHWC>
+__global__ void __launch_bounds__(kThreads) lift_staged_kernel(const float* __restrict__ rh, float* __restrict__ y,
+                                                               Geo g, int gmax) {
+    extern __shared__ float sm[];  // gmax x taps x rpi staged planes [+ NHWC: gmax x m^2 outputs]
+    const int m = int(g.m), mm = m * m, o = int(g.o), k = int(g.k), s = int(g.s), R = int(g.R);
+    const int taps = TYPE == 2 ? k : k * k;
+    const int rpi = TYPE == 2 ? R * m : R * R;
+    const int blk_floats = taps * rpi;
+    const int ngroups = (o + gmax - 1) / gmax;
+    const float inv_mm = 1.f / float(mm), inv_m = 1.f / float(m);
+    float* acc_s = sm + gmax * blk_floats;
+    for (int64_t blk = blockIdx.x; blk < g.b * ngroups; blk += gridDim.x) {
+        const int64_t q = blk / ngroups;
+        const int oj0 = int(blk - q * ngroups) * gmax;
+        const int G = min(gmax, o - oj0);
+        const float* src = rh + (q * o + oj0) * int64_t(blk_floats);
+        const int total = G * blk_floats;
+#pragma unroll 4
+        for (int e = threadIdx.x; e < total; e += kThreads) sm[e] = __ldg(src + e);
+        __syncthreads();
+        for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+            const int gl = fdiv(e, mm, inv_mm), pix = e - gl * mm;
+            const int r = fdiv(pix, m, inv_m), c = pix - r * m;
+            const float* pl = sm + gl * blk_floats;
+            float a = 0.f;
+            if constexpr (TYPE == 2) {
+                const float* p0 = pl + s * r * m + c;
+                for (int i = 0; i < k; ++i) a += p0[i * (rpi + m)];
+            } else {
+                const float* p0 = pl + s * r * R + s * c;
+                for (int i = 0; i < k; ++i) {
+                    const float* pi = p0 + i * (k * rpi + R);
+                    for (int j = 0; j < k; ++j) a += pi[j * (rpi + 1)];
+                }
+            }
+            if constexpr (NHWC) acc_s[gl * mm + pix] = a;
+            else y[(q * o + oj0) * mm + e] = a;
+        }
+        if constexpr (NHWC) {
+            __syncthreads();
+            const float inv_g = 1.f / float(G);
+            for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+                const int pix = fdiv(e, G, inv_g), gl = e - pix * G;
+                y[(q * mm + pix) * o + oj0 + gl] = acc_s[gl * mm + pix];
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// One block per (image, kG channels): the dy planes are staged in shared memory once; a thread
+// owns lowered rows (idx, idx + kThreads, ...) of an image's run, splits idx once, and writes
+// that row of every (channel, tap) column -- kG k^a independent stores per row, each warp a
+// contiguous run.
 template <int TYPE, bool NHWC>
 __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __restrict__ dy, float* __restrict__ drt,
                                                                  Geo g, int64_t ldr) {
@@ -112,37 +194,28 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
             for (int e = threadIdx.x; e < G * mm; e += kThreads) sdy[e] = __ldg(src + e);
         }
         __syncthreads();
-        for (int gl = 0; gl < G; ++gl) {
-            const float* pl = sdy + gl * mm;
-            for (int tap = 0; tap < taps; ++tap) {
-                const int i = TYPE == 2 ? tap : tap / k;
-                const int j = TYPE == 2 ? 0 : tap - i * k;
-                float* out = drt + int64_t((oj0 + gl) * taps + tap) * ldr + q * rpi;
-                for (int idx = threadIdx.x; idx < rpi; idx += kThreads) {
-                    const int Y = fdiv(idx, rw, inv_rw), X = idx - Y * rw;
-                    const int ty = Y - i;
-                    int r, c;
-                    bool ok;
-                    if (s == 1) {
-                        r = ty;
-                        ok = unsigned(ty) < unsigned(m);
-                    } else {
-                        r = ty / s;
-                        ok = ty >= 0 && r * s == ty && r < m;
-                    }
-                    if constexpr (TYPE == 3) {
+        float* out0 = drt + int64_t(oj0) * taps * ldr + q * rpi;
+        for (int idx = threadIdx.x; idx < rpi; idx += kThreads) {
+            const int Y = fdiv(idx, rw, inv_rw), X = idx - Y * rw;
+            float* out = out0 + idx;
+            for (int i = 0; i < k; ++i) {
+                const int ty = Y - i;
+                const int r = s == 1 ? ty : (ty >= 0 ? ty / s : -1);
+                const bool rok = ty >= 0 && r * s == ty && r < m;
+                if constexpr (TYPE == 2) {
+#pragma unroll
+                    for (int gl = 0; gl < kG; ++gl)
+                        if (gl < G) out[(int64_t(gl) * taps + i) * ldr] = rok ? sdy[gl * mm + r * m + X] : 0.f;
+                } else {
+                    for (int j = 0; j < k; ++j) {
                         const int tx = X - j;
-                        if (s == 1) {
-                            c = tx;
-                            ok = ok && unsigned(tx) < unsigned(m);
-                        } else {
-                            c = tx / s;
-                            ok = ok && tx >= 0 && c * s == tx && c < m;
-                        }
-                    } else {
-                        c = X;
+                        const int c = s == 1 ? tx : (tx >= 0 ? tx / s : -1);
+                        const bool ok = rok && tx >= 0 && c * s == tx && c < m;
+                        const int src = r * m + c;
+#pragma unroll
+                        for (int gl = 0; gl < kG; ++gl)
+                            if (gl < G) out[(int64_t(gl) * taps + i * k + j) * ldr] = ok ? sdy[gl * mm + src] : 0.f;
                     }
-                    out[idx] = ok ? pl[r * m + c] : 0.f;
                 }
             }
         }
@@ -212,6 +285,24 @@ cudaError_t lift_planes(const Geo& g, int type, const float* rhat, float* y, cud
     const int taps = type == 2 ? int(g.k) : int(g.k * g.k);
     const int64_t rpi = type == 2 ? g.R * g.m : g.R * g.R;
     PhaseScope ps(kPhaseLift, st, 0, 4.0 * double(g.b * g.o) * double(taps * rpi + g.m * g.m));
+    // staged form: up to kG channels' planes in 24 KB of shared memory per block (several blocks
+    // per SM keep the load phase of one overlapping the sums of another)
+    const int64_t blk_bytes = int64_t(taps) * rpi * 4;
+    const int gmax = int(std::min<int64_t>(kG, (24 * 1024) / std::max<int64_t>(1, blk_bytes)));
+    if (gmax >= 1) {
+        const size_t smem = size_t(gmax) * size_t(blk_bytes) + (g.yl ? size_t(gmax) * size_t(g.m * g.m) * 4 : 0);
+        if (smem <= 96 * 1024) {
+            const int grid = blocks_for(g.b * ((g.o + gmax - 1) / gmax), 8);
+            auto go = [&](auto kern) {
+                cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+                kern<<<grid, kThreads, smem, st>>>(rhat, y, g, gmax);
+            };
+            if (type == 2) g.yl ? go(lift_staged_kernel<2, true>) : go(lift_staged_kernel<2, false>);
+            else g.yl ? go(lift_staged_kernel<3, true>) : go(lift_staged_kernel<3, false>);
+            note_launch();
+            return cudaGetLastError();
+        }
+    }
     const size_t smem = g.yl ? size_t(kG) * size_t(g.m * g.m) * 4 : 0;
     const int grid = blocks_for(g.b * ((g.o + kG - 1) / kG), 8);
     auto go = [&](auto kern) {

@@ -1,0 +1,6 @@
+# round-2 call V: full GPU test suite, smoke, bench (x2), launch list of the step
+O=gpurun_out/r2v; mkdir -p $O
+timeout 1500 python -m pytest tests -m gpu -q --timeout 600 > $O/tests.log 2>&1; echo "tests rc $?" >> $O/tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
+for i in 1 2; do timeout 300 python bench.py --no-cpu --no-e2e --no-configs --steps 20 >> $O/bench.jsonl 2>> $O/bench.err; done
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-configs > $O/ncu_bench.log 2>&1; echo "ncu rc $?" >> $O/ncu_bench.log
