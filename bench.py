@@ -243,9 +243,9 @@ def measured_peaks():
 
 
 def gemm_traffic():
-    """DRAM bytes per GEMM launch from the committed ncu launch list of this
-    command (profiles/r01/gemm_traffic.json), or None."""
-    p = os.path.join(ROOT, "profiles", "r01", "gemm_traffic.json")
+    """DRAM bytes per GEMM-phase launch from the committed ncu launch list of this
+    command (profiles/r02/gemm_traffic.json), or None."""
+    p = os.path.join(ROOT, "profiles", "r02", "gemm_traffic.json")
     try:
         return json.load(open(p))["avg_dram_bytes_per_launch"]
     except (OSError, ValueError, KeyError):
@@ -443,7 +443,7 @@ def run_ours(a):
     peak = peaks.get("bf16_tflops") / 2.0 / 3.0
     peak_sus = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops")) / 2.0 / 3.0
     roofline = {
-        "bound": "tensor", "kernel": "gemm3xtf32_kernel (tcgen05 kind::tf32, 3 products per K step)",
+        "bound": "tensor", "kernel": "gemm3xtf32_kernel + the fused conv1 gather / hfold GEMMs (tcgen05 kind::tf32, 3 products per K step)",
         "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": (achieved / peak) if achieved else None,
         "peak_source": f"{peak_src} bf16_tflops (burst) / 2 (TF32 rate) / 3 (3xTF32 products)",

@@ -1,5 +1,6 @@
 """profiles/rNN/gemm_traffic.json from an ncu launch list of `bench.py --steps 1 --warmup 1`:
-average DRAM bytes (read + write) per gemm3xtf32 launch over the last (timed) step."""
+average DRAM bytes (read + write) per tensor-core GEMM launch (gemm3xtf32 and the fused conv1
+gather / hfold kernels: the GEMM phase of the step) over the last (timed) step."""
 import csv
 import json
 import sys
@@ -14,12 +15,13 @@ for r in rows:
         continue
     if hdr and len(r) == len(hdr):
         d = dict(zip(hdr, r))
-        if "gemm3xtf32" in d["Kernel Name"]:
+        if any(t in d["Kernel Name"] for t in ("gemm3xtf32", "gather_kernel", "hfold_kernel")):
             agg.setdefault(int(d["ID"]), {})[d["Metric Name"]] = float(d["Metric Value"].replace(",", ""))
 last = [agg[i] for i in sorted(agg)][-per_step:]
 by = [v.get("dram__bytes_read.sum", 0) + v.get("dram__bytes_write.sum", 0) for v in last]
 ns = [v.get("gpu__time_duration.sum", 0) for v in last]
-json.dump({"kernel": f"gemm3xtf32_kernel (the {len(last)} launches of one conv1-5 fwd+bwd step, b=256)",
+json.dump({"kernel": f"gemm3xtf32_kernel + fused conv1 gather / hfold kernels (the {len(last)} launches of one "
+                     f"conv1-5 fwd+bwd step, b=256)",
            "launches": len(last), "avg_dram_bytes_per_launch": sum(by) / len(by),
            "avg_duration_ns_under_ncu": sum(ns) / len(ns),
            "source": f"ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "

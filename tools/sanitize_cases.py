@@ -102,6 +102,11 @@ def main():
     conv_case("a_smem", 9, 3, 32, 64, 2, 1, 1, types=(1,), a_tmem=0, a_tmem_wide=0); n += 1
     conv_case("a_ring", 9, 3, 32, 64, 2, 1, 1, types=(1,), a_tmem=2); n += 1
     conv_case("fwd_swap", 19, 3, 16, 64, 4, 1, 1, types=(1,), fwd_swap=1); n += 1
+    # fused small-channel Type 1 (gather forward / backward-weight, hfold backward-data) at a
+    # batch whose tiles wrap every ring (> 148 tiles: CTAs with several tiles and chains)
+    conv_case("gather_conv1", 227, 11, 3, 96, 8, 4, 0, types=(1,)); n += 1
+    conv_case("gather_6mma", 227, 11, 3, 96, 8, 4, 0, types=(1,), gather=2); n += 1
+    conv_case("gather_pad", 71, 11, 3, 64, 3, 4, 2, types=(1,)); n += 1
     print(f"SANITIZE_CASES_OK {n}", flush=True)
 
 
