@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the configs[0..2] device / CPU lines")
     ap.add_argument("--layout", default="nhwc", choices=["nchw", "nhwc"],
                     help="y / dy layout of every layer (NHWC = the next layer's input order)")
+    ap.add_argument("--copy-streams", type=int, default=2, help="e2e: copy streams per direction")
     ap.add_argument("--tune", default="", help="A/B runs: comma list key=value of cct_set_tuning switches")
     return ap.parse_args()
 
@@ -520,15 +521,18 @@ def run_e2e(a, st, torch, world, group, dev):
     for h, t in zip(hx + hdy, st.x + st.dy):
         h.copy_(t.cpu())
     comp = torch.cuda.current_stream()
-    up = torch.cuda.Stream(device=dev)
-    down = torch.cuda.Stream(device=dev)
+    # several copy streams per direction: independent DMA queues keep both PCIe directions
+    # busier than one stream each
+    ncs = max(1, a.copy_streams)
+    ups = [torch.cuda.Stream(device=dev) for _ in range(ncs)]
+    downs = [torch.cuda.Stream(device=dev) for _ in range(ncs)]
     h2d = sum(t.numel() * 4 for t in hx + hdy)
     d2h = sum(t.numel() * 4 for t in hy + hdx + hdw)
     ins = [(st.x, st.dy), ([torch.empty_like(t) for t in st.x], [torch.empty_like(t) for t in st.dy])]
     outs = [(st.y, st.dx, st.dw), ([torch.empty_like(t) for t in st.y], [torch.empty_like(t) for t in st.dx],
                                    [torch.empty_like(t) for t in st.dw])]
     in_free = [None, None]   # comp event: the last step that read input set s is done
-    out_free = [None, None]  # down event: the downloads of output set s are done
+    out_free = [None, None]  # down events: the downloads of output set s are done
     step = [0]
 
     def ev(s):
@@ -542,46 +546,49 @@ def run_e2e(a, st, torch, world, group, dev):
         xs, dys = ins[s]
         ys, dxs, dws = outs[s]
         evx, evdy = [None] * nl, [None] * nl
-        with torch.cuda.stream(up):
-            if in_free[s] is not None:
-                up.wait_event(in_free[s])
-            for i in range(nl):
+        if in_free[s] is not None:
+            for u in ups:
+                u.wait_event(in_free[s])
+        for i in range(nl):
+            u = ups[i % ncs]
+            with torch.cuda.stream(u):
                 xs[i].copy_(hx[i], non_blocking=True)
-                evx[i] = ev(up)
-            for i in reversed(range(nl)):
+                evx[i] = ev(u)
+        for i in reversed(range(nl)):
+            u = ups[(i + 1) % ncs]
+            with torch.cuda.stream(u):
                 dys[i].copy_(hdy[i], non_blocking=True)
-                evdy[i] = ev(up)
+                evdy[i] = ev(u)
         if out_free[s] is not None:
-            comp.wait_event(out_free[s])
+            for e in out_free[s]:
+                comp.wait_event(e)
+
+        def download(j, host, dev_t):
+            e = ev(comp)
+            dn = downs[j % ncs]
+            with torch.cuda.stream(dn):
+                dn.wait_event(e)
+                host.copy_(dev_t, non_blocking=True)
+
         for i, d in enumerate(st.descs):
             comp.wait_event(evx[i])
             conv_fwd_cached(xs[i], st.w[i], d, st.types[i], cache=st.cache[i], out=ys[i], ws=st.ws)
-            e = ev(comp)
-            with torch.cuda.stream(down):
-                down.wait_event(e)
-                hy[i].copy_(ys[i], non_blocking=True)
+            download(i, hy[i], ys[i])
         handles = []
         for i in reversed(range(nl)):
             d, t = st.descs[i], st.types[i]
             comp.wait_event(evdy[i])
             conv_bwd(dys[i], st.w[i], d, t, x=xs[i], cache=st.cache[i], dx=dxs[i], dw=dws[i], ws=st.ws)
-            e = ev(comp)
-            with torch.cuda.stream(down):
-                down.wait_event(e)
-                hdx[i].copy_(dxs[i], non_blocking=True)
+            download(i + 1, hdx[i], dxs[i])
             if group is not None:
                 handles.append((i, dist.all_reduce(dws[i], group=group, async_op=True)))
             else:
-                with torch.cuda.stream(down):
-                    hdw[i].copy_(dws[i], non_blocking=True)
+                download(i, hdw[i], dws[i])
         for i, h in handles:
             h.wait()
-            e = ev(comp)
-            with torch.cuda.stream(down):
-                down.wait_event(e)
-                hdw[i].copy_(dws[i], non_blocking=True)
+            download(i, hdw[i], dws[i])
         in_free[s] = ev(comp)
-        out_free[s] = ev(down)
+        out_free[s] = [ev(dn) for dn in downs]
 
     for _ in range(2):
         one()
@@ -592,7 +599,8 @@ def run_e2e(a, st, torch, world, group, dev):
     e0.record(comp)
     for _ in range(a.steps):
         one()
-    comp.wait_stream(down)  # the last step's results are on the host
+    for dn in downs:
+        comp.wait_stream(dn)  # the last step's results are on the host
     e1.record(comp)
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
@@ -604,7 +612,7 @@ def run_e2e(a, st, torch, world, group, dev):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "h2d_gb_per_s": h2d / (ms * 1e-3) / 1e9, "d2h_gb_per_s": d2h / (ms * 1e-3) / 1e9,
             "path": "C ABI (cct_conv_fwd_cached / cct_conv_bwd) on double-buffered device buffers: pinned-host "
-                    "H2D of x, dy and D2H of y, dx, dW on two copy streams overlapping compute"}
+                    f"H2D of x, dy and D2H of y, dx, dW on {ncs} + {ncs} copy streams overlapping compute"}
 
 
 if __name__ == "__main__":
