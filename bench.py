@@ -63,7 +63,8 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the configs[0..2] device / CPU lines")
     ap.add_argument("--layout", default="nhwc", choices=["nchw", "nhwc"],
                     help="y / dy layout of every layer (NHWC = the next layer's input order)")
-    ap.add_argument("--copy-streams", type=int, default=2, help="e2e: copy streams per direction")
+    ap.add_argument("--copy-streams", type=int, default=1,
+                    help="e2e: copy streams per direction (measured: 2-3 no faster than 1)")
     ap.add_argument("--tune", default="", help="A/B runs: comma list key=value of cct_set_tuning switches")
     return ap.parse_args()
 
