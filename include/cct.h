@@ -149,7 +149,8 @@ CCT_API int cct_get_implicit_lowering(void);
  * CCT_ERR_CONFIG for an unknown key or an out-of-range value. */
 typedef enum {
     CCT_TUNE_SPLIT_PRODUCER = 0, /* 1 (default): A and B TMA tiles issued by two producer threads       */
-    CCT_TUNE_A_TMEM = 1,         /* N <= 96 tiles: 0 A from smem, 1 A in TMEM (default), 2 deeper A ring */
+    CCT_TUNE_A_TMEM = 1,         /* N <= 96 tiles: 0 A from smem, 1 A in TMEM (default), 2 deeper A ring, */
+                                 /* 3 A in TMEM + merged N = 2 BN product (single CTAs, K-major B)       */
     CCT_TUNE_A_TMEM_WIDE = 2,    /* 1 (default): 192/256/384-wide CTA-pair tiles keep A in TMEM          */
     CCT_TUNE_CTA_PAIRS = 3,      /* 0 auto (default), 1 single CTAs only, 2 CTA pairs whenever legal     */
     CCT_TUNE_BN384 = 4,          /* 1 (default): one 256 + 128 composite tile for N = 384                */
@@ -158,7 +159,7 @@ typedef enum {
     CCT_TUNE_S2D = 7,            /* strided Type 1: 0 never space-to-depth, 1 cost model (default), 2 always */
     CCT_TUNE_IMPLICIT_BWD = 8,   /* implicit Type 1 backward-data: 0 never, 1 cost model (default), 2 always */
     CCT_TUNE_WGRAD_SWAP = 9,     /* 1 (default): swapped implicit backward-weight for o < 128            */
-    CCT_TUNE_DGRAD_SWAP = 10,    /* swapped implicit backward-data: 0 never, 1 d < 128 (default), 2 d <= 128 */
+    CCT_TUNE_DGRAD_SWAP = 10,    /* swapped implicit backward-data: 0 never (default), 1 d < 128, 2 d <= 128 */
     CCT_TUNE_FWD_SWAP = 11,      /* 1: swapped forward for o < 128 (default 0: measured slower)          */
     CCT_TUNE_TRACE_PHASES = 12,  /* 1: one stderr line per kernel launch (diagnostics)                   */
     CCT_TUNE_GATHER = 13,        /* 1 (default): fused small-channel Type 1 (d s % 4 == 0, e.g. conv1):  */

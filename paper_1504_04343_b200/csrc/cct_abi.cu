@@ -299,7 +299,11 @@ const float* dhat_of(const Geo& g, int type, const Lowered& L, const float* x, f
 cct_status gemm_capped(GemmProblem gp, float* out, int64_t span, Ws& ws, cudaStream_t st, const char* what,
                        bool* fused = nullptr) {
     const int64_t kb = (gp.K + kBK - 1) / kBK;
-    int splits = effective_splits(kb, int((kb + kMaxChainKB - 1) / kMaxChainKB));
+    // narrow tiles (N <= 128) accumulate alternate 8-wide K steps into two sub-accumulators
+    // (gemm_kernel.cuh Cfg::NACC): each TMEM chain holds half the K terms, so the accuracy cap
+    // allows twice the k-blocks per tile (not for the one-accumulator A ring or the merged form)
+    const int64_t cap = kMaxChainKB * ((tile_n(gp) <= 128 && tuning(CCT_TUNE_A_TMEM) < 2) ? 2 : 1);
+    int splits = effective_splits(kb, int((kb + cap - 1) / cap));
     // a 2-way accuracy split of a wide-tile K-major GEMM runs as two TMEM chains of one tile
     // (no partial tiles, no reduce kernel); CCT_TUNE_CHAIN2 = 0 keeps the split-K form (A/B)
     const int chain2_env = tuning(CCT_TUNE_CHAIN2);

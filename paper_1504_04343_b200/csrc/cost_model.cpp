@@ -103,9 +103,10 @@ double dgrad_seconds(const G& g, bool implicit, double rows, double cols, double
     double t = 0;
     if (implicit) {
         const double K = g.k * g.k * g.o, M = g.b * g.n * g.n;
-        // d < 128 runs swapped (cct_abi.cu dgrad_swapped): a 128-row tile of d useful rows,
-        // pixels 256 wide, without CTA pairs (measured ~8% below the paired rate)
-        const double gt = g.d < 128 ? gemm_seconds(g.d, M, K, c) * 1.08 : gemm_seconds(M, g.d, K, c);
+        // pixels x d tiles (CTA pairs; the swapped d-row form is opt-in, CCT_TUNE_DGRAD_SWAP,
+        // measured 8 % slower on conv2 after the warp-uniform issue fix)
+        const double gt = cct_get_tuning(CCT_TUNE_DGRAD_SWAP) && g.d < 128 ? gemm_seconds(g.d, M, K, c) * 1.08
+                                                                           : gemm_seconds(M, g.d, K, c);
         const double gb = rhat + xin;
         t += std::max(gt, gb / c->hbm_bytes_per_s);
         *by += gb;

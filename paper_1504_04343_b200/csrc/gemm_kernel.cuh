@@ -182,7 +182,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr int STAGES = C_::STAGES;
     constexpr int BNL = C_::BNL;
     // A_TM == 2: one accumulator per tile, the freed TMEM columns deepen the A ring
+    // A_TM == 3 (MG): A in TMEM, and the two products sharing A_big run as ONE N = 2 BN MMA over
+    // the stage's B rows laid out [small | raw]: D[0, BN) = A_big B_small, D[BN, 2 BN) = A_big B_big
+    // + A_small B_big, summed by the epilogue like two sub-accumulators (4 MMAs per k-block
+    // instead of 6; an N <= 128 tf32 MMA costs ~77 cycles at any N, N = 192 ~103: tools/mma_rate.cu)
+    constexpr bool MG = A_TM == 3;
+    static_assert(!MG || (CG == 1 && !B_MN && !A_MN && BN <= 96 && !CH2 && !TRO), "A_TM 3 config");
     constexpr int NACC = CH2 ? 2 : (A_TM == 2) ? 1 : C_::NACC;
+    // stage layout: [A raw | B raw | A small | B small]; MG: [A raw | B small | B raw | A small]
+    constexpr uint32_t B_OFF = MG ? C_::A_BYTES + C_::B_BYTES : C_::A_BYTES;       // B raw
+    constexpr uint32_t BS_OFF = MG ? C_::A_BYTES : C_::RAW_BYTES + C_::A_BYTES;    // B small
     static_assert(!CH2 || (!A_TM && BN > 128), "CH2 config");
     // single-buffered accumulator: CH2 (two chains), the 384-wide tile (256 + 128 columns), and
     // a 256-wide tile with A in TMEM (the A ring takes the second accumulator's columns)
@@ -319,7 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     uint64_t* const fb = &full[int(gi % kTGroups) * STAGES + stage];
                     if (el) ptx::mbar_arrive_expect_tx(fb, (role_a && role_b) ? C_::RAW_BYTES : role_a ? C_::A_BYTES : C_::B_BYTES);
                     uint8_t* a_dst = smem + stage * C_::STAGE_BYTES;
-                    uint8_t* b_dst = a_dst + C_::A_BYTES;
+                    uint8_t* b_dst = a_dst + B_OFF;
                     const int k0 = kb * kBK;
                     if (role_a) {
                         if constexpr (A_IM == 1 && !A_MN) {
@@ -414,6 +423,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // (BN = 384: two MMAs per step, N = 256 into columns [0, 256) and N = 128 into [256, 384))
             constexpr uint32_t idesc = ptx::idesc_tf32(kBM * CG, BN > 256 ? 256 : BN, A_MN, B_MN);
             constexpr uint32_t idesc2 = ptx::idesc_tf32(kBM * CG, BN > 256 ? BN - 256 : BN, A_MN, B_MN);
+            constexpr uint32_t idesc_mg = ptx::idesc_tf32(kBM, MG ? 2 * BN : BN, 0, 0);
             int stage = 0;
             uint32_t phase = 0;
             int local = 0;
@@ -449,9 +459,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ptx::mbar_wait(&tdone[stage], phase);
                     ptx::tc_fence_after();
                     const uint32_t a_raw = ptx::smem_u32(smem + stage * C_::STAGE_BYTES);
-                    const uint32_t b_raw = a_raw + C_::A_BYTES;
+                    const uint32_t b_raw = a_raw + B_OFF;
                     const uint32_t a_sml = a_raw + C_::RAW_BYTES;
-                    const uint32_t b_sml = b_raw + C_::RAW_BYTES;
+                    const uint32_t b_sml = a_raw + BS_OFF;
                     if (ptx::elect_one()) {
                     if constexpr (A_TM) {
                         // A big | small for this k-block in TMEM slot gi % kASlots (16 + 16 columns)
@@ -476,6 +486,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int kk = 0; kk < 2; ++kk) {
                                 mma_ts(d_tmem, a_big + kk * 8, tile_desc<B_MN>(b_raw, kk), 1u);
                                 mma2_ts(d_tmem + 256, a_big + kk * 8, tile_desc<B_MN>(b_raw + SUB2, kk), 1u);
+                            }
+                        } else if constexpr (MG) {
+                            // [A_big B_small | A_big B_big] over the 2 BN rows [small | raw] (the first
+                            // MMA of a tile clears both halves), then A_small B_big into the upper half
+#pragma unroll
+                            for (int kk = 0; kk < 2; ++kk) {
+                                ptx::mma_tf32_ts(d_tmem, a_big + kk * 8, tile_desc<false>(b_sml, kk), idesc_mg,
+                                                 kk ? 1u : first);
+                                ptx::mma_tf32_ts(d_tmem + BN, a_small + kk * 8, tile_desc<false>(b_raw, kk), idesc, 1u);
                             }
                         } else {
 #pragma unroll
@@ -783,10 +802,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                                             v);
                     ptx::tmem_st_wait();
                     // B small part in smem as usual
-                    constexpr int b0 = C_::A_BYTES / 16, b1 = C_::RAW_BYTES / 16;
-                    for (int i = b0 + t; i < b1; i += 128) {
-                        const float4 x = ptx::lds128(raw + i * 16);
-                        ptx::sts128(raw + C_::RAW_BYTES + i * 16, small_part(x));
+                    for (int i = t; i < int(C_::B_BYTES / 16); i += 128) {
+                        const float4 x = ptx::lds128(raw + B_OFF + i * 16);
+                        ptx::sts128(raw + BS_OFF + i * 16, small_part(x));
                     }
                     ptx::fence_proxy_async_smem();
                     ptx::tc_fence_before();
@@ -906,11 +924,15 @@ cudaError_t dispatch_std(const GemmProblem& g, const CUtensorMap& ta, const CUte
     }
     if constexpr (BN <= 96) {
         const int atm = g.im2col.operand >= 1 ? 0 : a_in_tmem_mode();
+        if constexpr (CG == 1) {
+            if (!amn && !bmn && g.passes == 3 && atm == 3)
+                return g.im2col.x ? launch<BN, 0, 0, 1, 1, 3>(ta, tb, kp, st) : launch<BN, 0, 0, 1, 0, 3>(ta, tb, kp, st);
+        }
         if (!amn && g.passes == 3 && atm == 2) {
             if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 2>(ta, tb, kp, st);
             return bmn ? launch<BN, 0, 1, CG, 0, 2>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 2>(ta, tb, kp, st);
         }
-        if (!amn && g.passes == 3 && atm) {
+        if (!amn && g.passes == 3 && atm) {  // (atm 3 on a CTA pair or MN-major B: the two-sub-accumulator form)
             if (g.im2col.x) return bmn ? cudaErrorInvalidValue : launch<BN, 0, 0, CG, 1, 1>(ta, tb, kp, st);
             return bmn ? launch<BN, 0, 1, CG, 0, 1>(ta, tb, kp, st) : launch<BN, 0, 0, CG, 0, 1>(ta, tb, kp, st);
         }
