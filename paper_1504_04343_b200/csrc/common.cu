@@ -33,8 +33,8 @@ int num_sms() {
 // environment variables, so results and tile choices depend only on the caller's calls.
 namespace {
 constexpr int kTuneDefaults[CCT_TUNE_COUNT] = {
-    /* SPLIT_PRODUCER */ 1, /* A_TMEM */ 1,     /* A_TMEM_WIDE */ 1, /* CTA_PAIRS */ 0,
-    /* BN384 */ 1,          /* STREAMK */ 1,    /* CHAIN2 */ 1,      /* S2D */ 1,
+    /* SPLIT_PRODUCER */ 0, /* A_TMEM */ 1,     /* A_TMEM_WIDE */ 1, /* CTA_PAIRS */ 0,
+    /* BN384 */ 0,          /* STREAMK */ 1,    /* CHAIN2 */ 1,      /* S2D */ 1,
     /* IMPLICIT_BWD */ 1,   /* WGRAD_SWAP */ 1, /* DGRAD_SWAP */ 0,  /* FWD_SWAP */ 0,
     /* TRACE_PHASES */ 0,   /* GATHER */ 1};
 constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 3, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1, 2};

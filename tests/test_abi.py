@@ -174,9 +174,9 @@ def test_tuning_switches_are_explicit():
     L = cct.lib()
     cct.reset_tuning()
     defaults = {k: cct.get_tuning(k) for k in cct.TUNE}
-    assert defaults["split_producer"] == 1 and defaults["fwd_swap"] == 0 and defaults["s2d"] == 1
-    with cct.tuning(s2d=2, split_producer=0):
-        assert cct.get_tuning("s2d") == 2 and cct.get_tuning("split_producer") == 0
+    assert defaults["split_producer"] == 0 and defaults["fwd_swap"] == 0 and defaults["s2d"] == 1
+    with cct.tuning(s2d=2, split_producer=1):
+        assert cct.get_tuning("s2d") == 2 and cct.get_tuning("split_producer") == 1
     assert {k: cct.get_tuning(k) for k in cct.TUNE} == defaults
     assert L.cct_set_tuning(7, 3) == 1          # out of range -> CCT_ERR_CONFIG
     assert b"out of range" in L.cct_last_error()

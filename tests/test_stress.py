@@ -44,8 +44,9 @@ def test_training_step_bitwise_repeatable(cct, dev, split_producer):
 
 
 @pytest.mark.timeout(900, method="thread")
-@pytest.mark.parametrize("tune", [{}, {"bn384": 0}, {"streamk": 0}, {"chain2": 0}, {"a_tmem_wide": 0},
-                                  {"cta_pairs": 1}, {"implicit_bwd": 2}, {"s2d": 2}],
+@pytest.mark.parametrize("tune", [{}, {"bn384": 1}, {"streamk": 0}, {"chain2": 0}, {"a_tmem_wide": 0},
+                                  {"cta_pairs": 1}, {"implicit_bwd": 2}, {"s2d": 2}, {"dgrad_swap": 1},
+                                  {"gather": 0}, {"gather": 2}],
                          ids=lambda d: ",".join(f"{k}={v}" for k, v in d.items()) or "default")
 def test_gemm_variants_repeatable(cct, dev, tune):
     """Every kernel form the tuning keys select (odd and even ring depths, CTA pairs,
