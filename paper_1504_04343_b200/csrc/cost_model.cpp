@@ -84,7 +84,7 @@ double gemm_seconds(double M, double N, double K, const cct_calibration* c) {
         const double pad = rup(N, x);
         if (pad < best) { best = pad; bn = x; }
     }
-    const bool wide384 = std::fmod(N, 384.0) == 0;
+    const bool wide384 = cct_get_tuning(CCT_TUNE_BN384) && std::fmod(N, 384.0) == 0;
     const double rate = interp_rate(wide384 ? 256.0 : bn, std::min(K, 4096.0)) * (c->gemm_flops_per_s / kRateRef);
     return 2.0 * rup(M, 128) * rup(N, bn) * K / rate;
 }
