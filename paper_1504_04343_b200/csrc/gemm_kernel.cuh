@@ -902,6 +902,7 @@ cudaError_t dispatch_std(const GemmProblem& g, const CUtensorMap& ta, const CUte
                 if (!amn && !bmn) return launch<BN, 0, 0, CG, 0, 0, 0, 1>(ta, tb, kp, st);
                 if (amn && !bmn) return launch<BN, 1, 0, CG, 0, 0, 0, 1>(ta, tb, kp, st);  // materialised wgrad
                 if (!amn && bmn) return launch<BN, 0, 1, CG, 0, 0, 0, 1>(ta, tb, kp, st);  // swapped (narrow bank)
+                if (amn && bmn) return launch<BN, 1, 1, CG, 0, 0, 0, 1>(ta, tb, kp, st);   // swapped, dy NHWC
             }
         }
         return cudaErrorInvalidValue;

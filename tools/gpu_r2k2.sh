@@ -1,0 +1,7 @@
+# round-2 call K2: new defaults -- full GPU tests, smoke, full bench + reference arm, launch list
+O=gpurun_out/r2k2; mkdir -p $O
+timeout 1800 python -m pytest tests -m gpu -q --timeout 900 > $O/tests.log 2>&1; echo "tests rc $?" >> $O/tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc $?" >> $O/smoke.log
+timeout 900 python bench.py > $O/bench_full.json 2> $O/bench_full.err; echo "bench rc $?" >> $O/bench_full.err
+timeout 900 python bench.py --impl reference > $O/bench_reference.json 2> $O/bench_reference.err; echo "ref rc $?" >> $O/bench_reference.err
+timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e --no-configs > $O/ncu_bench.log 2>&1; echo "ncu rc $?" >> $O/ncu_bench.log
