@@ -228,3 +228,31 @@ def test_hfold_dgrad_full_batch(cct, dev):
     assert err <= TOL, f"rel-L2 {err:.3e}"
     dx2, _ = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x)
     assert torch.equal(dx2, dx)
+
+
+def test_fused_conv1_under_workspace_limit(cct, dev):
+    """The fused conv1 passes under a workspace limit that forces batch chunks (SPEC batching
+    module): forward, backward-data and backward-weight agree with the unchunked call."""
+    from paper_1504_04343_b200 import conv
+    L = cct.lib()
+    n, k, d, o, b, s, p = 227, 11, 3, 96, 12, 4, 0
+    desc = cct.ConvDesc(n, k, d, o, b, s, p, cct.NHWC)
+    g = torch.Generator(device=dev).manual_seed(41)
+    x = torch.rand((b, n, n, d), generator=g, device=dev) * 2 - 1
+    w = torch.rand((o, k, k, d), generator=g, device=dev) * 2 - 1
+    dy = torch.rand((b, desc.m, desc.m, o), generator=g, device=dev) * 2 - 1
+    full = (conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_data(dy, w, desc, 1), conv.conv_bwd_weight(x, dy, desc, 1))
+    old = L.cct_get_workspace_limit()
+    unlimited = cct.workspace_size(desc, 1, cct.PASS_BWD)
+    try:
+        L.cct_set_workspace_limit(24 << 20)
+        assert cct.workspace_size(desc, 1, cct.PASS_BWD) < unlimited  # the batch is chunked
+        ch = (conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_data(dy, w, desc, 1), conv.conv_bwd_weight(x, dy, desc, 1))
+        dx2, dw2 = conv.conv_bwd(dy, w, desc, 1, x=x)
+    finally:
+        L.cct_set_workspace_limit(old)
+
+    def close(a, ref):
+        return float(torch.linalg.norm(a - ref) / torch.linalg.norm(ref)) < 1e-5
+    assert torch.equal(ch[0], full[0]) and torch.equal(ch[1], full[1])  # per-image passes: same bits
+    assert close(ch[2], full[2]) and close(dw2, full[2]) and torch.equal(dx2, full[1])
