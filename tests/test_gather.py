@@ -245,7 +245,7 @@ def test_fused_conv1_under_workspace_limit(cct, dev):
     old = L.cct_get_workspace_limit()
     unlimited = cct.workspace_size(desc, 1, cct.PASS_BWD)
     try:
-        L.cct_set_workspace_limit(24 << 20)
+        L.cct_set_workspace_limit(8 << 20)
         assert cct.workspace_size(desc, 1, cct.PASS_BWD) < unlimited  # the batch is chunked
         ch = (conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_data(dy, w, desc, 1), conv.conv_bwd_weight(x, dy, desc, 1))
         dx2, dw2 = conv.conv_bwd(dy, w, desc, 1, x=x)
