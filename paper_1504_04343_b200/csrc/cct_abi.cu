@@ -595,7 +595,7 @@ cct_status run_bwd_implicit(const Geo& g, const float* x, const float* cache, co
 
 cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cache, const float* dy, const float* w,
                        float* dx, float* dw, Ws& ws, cudaStream_t st) {
-    if (dx && t1_hfold_dgrad(g, type) && aligned16(or_plan(dy, ws)) && aligned16(or_plan(dx, ws))) {
+    if (dx && t1_hfold_dgrad(g, type) && aligned16(or_plan(dy, ws))) {  // (dx: plain stores)
         const size_t mark = ws.off;
         float* w2 = ws.take(hfold_dgrad_ws_floats(g));
         if (ws.base) CCT_TRY(hfold_dgrad(g, dy, w, dx, w2, st), "fused backward-data");
@@ -766,7 +766,10 @@ int64_t chunk_images(const Geo& g, int type, int pass) {
     const size_t one = plan_bytes(g, type, pass, 1), two = plan_bytes(g, type, pass, 2);
     const size_t per = two > one ? two - one : one;
     const size_t fixed = one > per ? one - per : 0;
-    const int64_t cb = ws_limit() > fixed ? int64_t((ws_limit() - fixed) / std::max<size_t>(per, 1)) : 1;
+    int64_t cb = ws_limit() > fixed ? int64_t((ws_limit() - fixed) / std::max<size_t>(per, 1)) : 1;
+    // chunks start at 16-byte aligned image offsets (the TMA / bulk-copy paths need aligned x):
+    // with an image size not a multiple of 4 floats (conv1: 227 x 227 x 3), whole groups of 4
+    if ((g.n * g.n * g.d) % 4 != 0 && cb >= 4) cb &= ~int64_t(3);
     return std::max<int64_t>(1, std::min<int64_t>(cb, g.b));
 }
 

@@ -195,7 +195,7 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
             double sf = 0, bf = 0, sw = 0, bw = 0, sd = 0, bd = 0;
             if (fw) { sf = flops / (0.65 * rate); bf = xin + yout; }
             else one_pass(g, 1, 0, c, &sf, &bf, allow_s2d, false);
-            if (wg) { sw = flops / (0.59 * rate); bw = xin + yout; }
+            if (wg) { sw = flops / (0.63 * rate); bw = xin + yout; }
             else one_pass(g, 1, 2, c, &sw, &bw, allow_s2d, false);
             if (dg) {
                 const double xp = std::ceil((g.s * g.d * (g.m - 1) + g.k * g.d + 6) / 4) * 4;

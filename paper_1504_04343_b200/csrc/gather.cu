@@ -605,8 +605,9 @@ struct WgParams {
     int64_t x_total;
     int b, n, d, k, s, p, m, o, kkd, kd;
     int mt_tiles;            // M-tiles (ceil(kkd / 128))
-    int tpi, tiles, chains;  // 128-pixel tiles per image, total tiles, chains
+    int tpi, tpx, tiles, chains;  // tiles per image, pixels per tile (whole output rows when m <= 128), total tiles, chains
     int pitch, lmargin, xr;  // staged rows (as the forward)
+    int xb;                  // row-stage buffers (2 or 3)
     int bstages, aslots;
 };
 
@@ -623,12 +624,12 @@ __host__ __device__ inline uint32_t wg_bstage_bytes(int np) { return uint32_t(np
 struct WgLayout {
     uint32_t ring, stage, bars, total;
 };
-__host__ __device__ inline WgLayout wg_layout(int np, int bstages, int aslots, int xr, int pitch) {
+__host__ __device__ inline WgLayout wg_layout(int np, int bstages, int aslots, int xr, int pitch, int xb) {
     WgLayout L;
     L.ring = 0;
     L.stage = uint32_t(bstages) * 2u * wg_bstage_bytes(np);
-    L.bars = (L.stage + 2u * uint32_t(xr) * uint32_t(pitch) * 4u + 15u) & ~15u;
-    L.total = L.bars + uint32_t(3 * bstages + 2 * aslots + 8) * 8u + 16u;
+    L.bars = (L.stage + uint32_t(xb) * uint32_t(xr) * uint32_t(pitch) * 4u + 15u) & ~15u;
+    L.total = L.bars + uint32_t(3 * bstages + 2 * aslots + 2 * xb + 4) * 8u + 16u;
     return L;
 }
 
@@ -636,9 +637,17 @@ __device__ __forceinline__ void wg_chain(const WgParams& p, int c, int& t0, int&
     t0 = int(int64_t(c) * p.tiles / p.chains);
     t1 = int(int64_t(c + 1) * p.tiles / p.chains);
 }
+// tile T: image q, pixels [P0, P1) (whole output rows when m <= 128: the staged rows of a tile
+// are then s (rows - 1) + k, and no tile restages a partial output row)
+__device__ __forceinline__ void wg_tile(const WgParams& p, int T, int& q, int& P0, int& P1) {
+    q = T / p.tpi;
+    P0 = (T - q * p.tpi) * p.tpx;
+    P1 = min(P0 + p.tpx, p.m * p.m);
+}
 __device__ __forceinline__ int wg_tile_kb(const WgParams& p, int T) {
-    const int P0 = (T % p.tpi) * kTileM;
-    return (min(P0 + kTileM, p.m * p.m) - P0 + kKB - 1) / kKB;
+    int q, P0, P1;
+    wg_tile(p, T, q, P0, P1);
+    return (P1 - P0 + kKB - 1) / kKB;
 }
 
 template <int NP, bool PAD, int MT>
@@ -648,15 +657,15 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr uint32_t HB = NP * kKB * 4;  // one half (raw or small) of a dy stage
     const int RB = p.bstages, RA = p.aslots;
-    const WgLayout L = wg_layout(NP, RB, RA, p.xr, p.pitch);
+    const WgLayout L = wg_layout(NP, RB, RA, p.xr, p.pitch, p.xb);
     uint64_t* bfull = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* btdone = bfull + RB;
     uint64_t* bempty = btdone + RB;
     uint64_t* afull = bempty + RB;
     uint64_t* aempty = afull + RA;
     uint64_t* xfull = aempty + RA;
-    uint64_t* xempty = xfull + 2;
-    uint64_t* tfull = xempty + 2;
+    uint64_t* xempty = xfull + p.xb;
+    uint64_t* tfull = xempty + p.xb;
     uint64_t* tempty = tfull + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
     constexpr uint32_t A_COL = uint32_t(MT * NP);  // A slots after the accumulators
@@ -673,7 +682,7 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
             ptx::mbar_init(&afull[a], 4);
             ptx::mbar_init(&aempty[a], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < p.xb; ++a) {
             ptx::mbar_init(&xfull[a], 1);
             ptx::mbar_init(&xempty[a], 4 * MT);
         }
@@ -697,9 +706,9 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
             int t0, t1;
             wg_chain(p, c, t0, t1);
             for (int T = t0; T < t1; ++T) {
-                const int q = T / p.tpi;
-                const int P0 = (T - q * p.tpi) * kTileM;
-                const int nkb = wg_tile_kb(p, T);
+                int q, P0, P1;
+                wg_tile(p, T, q, P0, P1);
+                const int nkb = (P1 - P0 + kKB - 1) / kKB;
                 for (int kb = 0; kb < nkb; ++kb) {
                     ptx::mbar_wait_sleep(&bempty[st], ph ^ 1);
                     if (ptx::elect_one()) {
@@ -781,10 +790,10 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
                 int t0, t1;
                 wg_chain(p, c, t0, t1);
                 for (int T = t0; T < t1; ++T, ++lt) {
-                    const int buf = lt & 1;
-                    ptx::mbar_wait_sleep(&xempty[buf], ((lt >> 1) & 1) ^ 1);
-                    const int q = T / p.tpi;
-                    const int P0 = (T - q * p.tpi) * kTileM, P1 = min(P0 + kTileM, mm);
+                    const int buf = lt % p.xb;
+                    ptx::mbar_wait_sleep(&xempty[buf], ((lt / p.xb) & 1) ^ 1);
+                    int q, P0, P1;
+                    wg_tile(p, T, q, P0, P1);
                     const int ra = P0 / p.m, rb = (P1 - 1) / p.m;
                     const int y0 = p.s * ra - p.p, nrows = p.s * (rb - ra) + p.k;
                     float* sb = reinterpret_cast<float*>(smem + L.stage) + int64_t(buf) * p.xr * p.pitch;
@@ -892,13 +901,13 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
             int t0, t1;
             wg_chain(p, c, t0, t1);
             for (int T = t0; T < t1; ++T, ++lt) {
-                const int buf = lt & 1;
-                const int q = T / p.tpi;
-                const int P0 = (T - q * p.tpi) * kTileM, P1 = min(P0 + kTileM, mm);
+                const int buf = lt % p.xb;
+                int q, P0, P1;
+                wg_tile(p, T, q, P0, P1);
                 const int ra = P0 / p.m;
                 const int nkb = (P1 - P0 + kKB - 1) / kKB;
                 const uint32_t sbase = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b;
-                ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
+                ptx::mbar_wait_sleep(&xfull[buf], (lt / p.xb) & 1);
                 int r0 = P0 / p.m, c0 = P0 - r0 * p.m;  // first pixel of k-block kb
                 for (int kb = 0; kb < nkb; ++kb) {
                     // the k-block's 16 pixels lie in output row r0 (jj < split) and r0 + 1 (m >= 16);
@@ -975,7 +984,8 @@ bool make_mnmajor_map(CUtensorMap* map, const float* base, int64_t pixels, int64
 }
 
 struct WgPlan {
-    int np = 0, mt = 0, bstages = 0, aslots = 0, xr = 0, pitch = 0, lmargin = 0, tpi = 0, tiles = 0, chains = 0, grid = 0;
+    int np = 0, mt = 0, bstages = 0, aslots = 0, xr = 0, xb = 0, pitch = 0, lmargin = 0, tpi = 0, tpx = 0, tiles = 0,
+        chains = 0, grid = 0;
     uint32_t smem = 0;
     bool ok = false;
 };
@@ -991,23 +1001,30 @@ WgPlan wg_plan(const Geo& g) {
     P.mt = int((kkd + kTileM - 1) / kTileM);
     P.aslots = std::min(8, (512 - P.mt * P.np) / 32);
     if (P.aslots < 4) return P;
-    const int64_t rows_span = (kTileM - 1) / g.m + 2 > g.m ? g.m : (kTileM - 1) / g.m + 2;
+    // tiles of whole output rows when m <= 128 (the pixels are this GEMM's K: at most one partly
+    // filled k-block per tile), else 128-pixel tiles
+    const int64_t tr = g.m <= kTileM ? kTileM / g.m : 0;
+    P.tpx = int(tr ? tr * g.m : kTileM);
+    const int64_t rows_span = tr ? tr : ((kTileM - 1) / g.m + 2 > g.m ? g.m : (kTileM - 1) / g.m + 2);
     P.xr = int(g.s * (rows_span - 1) + g.k);
     P.lmargin = int((g.p * g.d + 4 + 3) & ~int64_t(3));
     P.pitch = int((P.lmargin + (g.n + g.p) * g.d + 8 + 3) & ~int64_t(3));
-    if (int64_t(P.xr) * P.pitch * 4 * 2 >= (int64_t(1) << 31)) return P;
-    for (int st = 8; st >= 2; --st) {
-        const WgLayout L = wg_layout(P.np, st, P.aslots, P.xr, P.pitch);
-        if (L.total + 1024 <= uint32_t(kSmemMax)) {
-            P.bstages = st;
-            P.smem = L.total + 1024;
-            break;
+    if (int64_t(P.xr) * P.pitch * 4 * 3 >= (int64_t(1) << 31)) return P;
+    // three row-stage buffers when they fit next to >= 6 dy stages, else two
+    for (int xb = 3; xb >= 2 && !P.bstages; --xb)
+        for (int st = 8; st >= (xb == 3 ? 6 : 2); --st) {
+            const WgLayout L = wg_layout(P.np, st, P.aslots, P.xr, P.pitch, xb);
+            if (L.total + 1024 <= uint32_t(kSmemMax)) {
+                P.bstages = st;
+                P.xb = xb;
+                P.smem = L.total + 1024;
+                break;
+            }
         }
-    }
     if (!P.bstages) return P;
-    P.tpi = int((mm + kTileM - 1) / kTileM);
+    P.tpi = int((mm + P.tpx - 1) / P.tpx);
     P.tiles = int(g.b * P.tpi);
-    const int kb_tile_max = kTileM / kKB;
+    const int kb_tile_max = (P.tpx + kKB - 1) / kKB;
     const int cmin = (P.tiles * kb_tile_max + kWgChainKB - 1) / kWgChainKB;
     P.grid = std::min(num_sms(), P.tiles);
     P.chains = std::min(P.tiles, (cmin + P.grid - 1) / P.grid * P.grid);
@@ -1112,6 +1129,8 @@ cudaError_t gather_wgrad(const Geo& g, const float* x, const float* dy, float* d
     wp.kd = int(g.k * g.d);
     wp.mt_tiles = P.mt;
     wp.tpi = P.tpi;
+    wp.tpx = P.tpx;
+    wp.xb = P.xb;
     wp.tiles = P.tiles;
     wp.chains = P.chains;
     wp.pitch = P.pitch;
