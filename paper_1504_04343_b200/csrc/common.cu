@@ -37,7 +37,7 @@ constexpr int kTuneDefaults[CCT_TUNE_COUNT] = {
     /* BN384 */ 0,          /* STREAMK */ 1,    /* CHAIN2 */ 1,      /* S2D */ 1,
     /* IMPLICIT_BWD */ 1,   /* WGRAD_SWAP */ 1, /* DGRAD_SWAP */ 0,  /* FWD_SWAP */ 0,
     /* TRACE_PHASES */ 0,   /* GATHER */ 1};
-constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 3, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1, 2};
+constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 3, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1, 3};
 std::atomic<int> g_tune[CCT_TUNE_COUNT] = {
     {kTuneDefaults[0]}, {kTuneDefaults[1]}, {kTuneDefaults[2]},  {kTuneDefaults[3]},  {kTuneDefaults[4]},
     {kTuneDefaults[5]}, {kTuneDefaults[6]}, {kTuneDefaults[7]},  {kTuneDefaults[8]},  {kTuneDefaults[9]},

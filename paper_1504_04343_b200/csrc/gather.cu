@@ -50,7 +50,8 @@ struct FwdParams {
     int b, n, d, k, s, p, m, o;
     int seg, segw, kb_tile;    // lowered run per filter row, its window width, k-blocks per tile
     int nvar;                  // kernel-bank variants (float4 phase of the image's rows, 1 or 4)
-    int tpi, tiles;            // tiles per image, total tiles
+    int tpi, tpx, tiles;       // tiles per image, pixels per tile, total tiles
+    int xb;                    // row-stage buffers
     int pitch, lmargin;        // staged row slot: floats, and floats before the row data
     int xr;                    // row slots per stage buffer
     int stages;                // kernel-bank ring depth (smem)
@@ -80,14 +81,15 @@ __host__ __device__ constexpr int max_aslots(int np, bool mg) {
 struct FwdLayout {
     uint32_t ring, stage, zero, ktab, bars, total;
 };
-__host__ __device__ inline FwdLayout fwd_layout(int np, int stages, int aslots, int xr, int pitch, int kgroups) {
+__host__ __device__ inline FwdLayout fwd_layout(int np, int stages, int aslots, int xr, int pitch, int kgroups,
+                                                int xb) {
     FwdLayout L;
     L.ring = 0;
     L.stage = uint32_t(stages) * 2u * uint32_t(np) * kKB * 4u;
-    L.zero = L.stage + 2u * uint32_t(xr) * uint32_t(pitch) * 4u;
+    L.zero = L.stage + uint32_t(xb) * uint32_t(xr) * uint32_t(pitch) * 4u;
     L.ktab = L.zero + uint32_t(pitch) * 4u;
     L.bars = (L.ktab + 2u * 4u * uint32_t(kgroups) * 4u + 15u) & ~15u;  // ktab + etab, 4 variants
-    L.total = L.bars + uint32_t(2 * stages + 2 * aslots + 8) * 8u + 16u;
+    L.total = L.bars + uint32_t(2 * stages + 2 * aslots + 2 * xb + 4) * 8u + 16u;
     return L;
 }
 
@@ -110,8 +112,8 @@ struct TileGeo {
 __device__ __forceinline__ TileGeo tile_geo(const FwdParams& p, int T) {
     TileGeo t;
     t.q = T / p.tpi;
-    t.P0 = (T - t.q * p.tpi) * kTileM;
-    t.P1 = min(t.P0 + kTileM, p.m * p.m);
+    t.P0 = (T - t.q * p.tpi) * p.tpx;
+    t.P1 = min(t.P0 + p.tpx, p.m * p.m);
     t.ra = t.P0 / p.m;
     const int rb = (t.P1 - 1) / p.m;
     t.y0 = p.s * t.ra - p.p;
@@ -127,7 +129,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     const int ngroups_k = p.kb_tile * 4;
     const int RB = p.stages, RA = p.aslots;  // kernel-bank ring (smem), A slot ring (TMEM)
-    const FwdLayout L = fwd_layout(NP, RB, RA, p.xr, p.pitch, ngroups_k);
+    const FwdLayout L = fwd_layout(NP, RB, RA, p.xr, p.pitch, ngroups_k, p.xb);
     float* zero_row = reinterpret_cast<float*>(smem + L.zero);
     int* ktab = reinterpret_cast<int*>(smem + L.ktab);   // [variant][group]: row | zero mask | byte offset
     int* etab = ktab + 4 * ngroups_k;                      // [variant][group]: run element of the group's column 0
@@ -138,8 +140,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t* afull = bempty + RB;
     uint64_t* aempty = afull + RA;
     uint64_t* xfull = aempty + RA;
-    uint64_t* xempty = xfull + 2;
-    uint64_t* tfull = xempty + 2;
+    uint64_t* xempty = xfull + p.xb;
+    uint64_t* tfull = xempty + p.xb;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -182,9 +184,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             ptx::mbar_init(&afull[s], 4);
             ptx::mbar_init(&aempty[s], 1);
         }
-        for (int a = 0; a < 2; ++a) {
+        for (int a = 0; a < p.xb; ++a) {
             ptx::mbar_init(&xfull[a], 1);
             ptx::mbar_init(&xempty[a], 4 * kGatherGroups);  // every gather warp
+        }
+        for (int a = 0; a < 2; ++a) {
             ptx::mbar_init(&tfull[a], 1);
             ptx::mbar_init(&tempty[a], 4);  // epilogue warps
         }
@@ -280,8 +284,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             int lt = 0;
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
-                const int buf = lt & 1;
-                ptx::mbar_wait_sleep(&xempty[buf], ((lt >> 1) & 1) ^ 1);
+                const int buf = lt % p.xb;
+                ptx::mbar_wait_sleep(&xempty[buf], ((lt / p.xb) & 1) ^ 1);
                 const TileGeo tg = tile_geo(p, T);
                 float* sb = reinterpret_cast<float*>(smem + L.stage) + int64_t(buf) * p.xr * p.pitch;
                 uint32_t bytes = 0;
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (sl >= RA) { sl -= RA; ++pass; }
         int lt = 0;
         for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
-            const int buf = lt & 1;
+            const int buf = lt % p.xb;
             const TileGeo tg = tile_geo(p, T);
             const int P = min(tg.P0 + t, tg.P1 - 1);
             const int r = P / p.m, c = P - (P / p.m) * p.m;
@@ -404,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t slot0 = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b + uint32_t(p.s * (r - tg.ra)) * pitch_b;
             const int tb = col0 * p.d * 4;  // byte offset of this pixel's run within a staged row
             const int* kt = ktab + variant_of(p, tg.q) * ngroups_k;
-            ptx::mbar_wait_sleep(&xfull[buf], (lt >> 1) & 1);
+            ptx::mbar_wait_sleep(&xfull[buf], (lt / p.xb) & 1);
             for (int kb = int((uint32_t(grp) - gbase) & (kGatherGroups - 1)); kb < p.kb_tile; kb += kGatherGroups) {
                 // gather + split first; the slot is waited for only before the TMEM store
                 // the k-block's 4 group entries (uniform): filter row | zero mask | byte offset of
@@ -522,7 +526,8 @@ bool make_kmajor_map(CUtensorMap* map, const float* base, int64_t rows, int64_t 
 
 struct FwdPlan {
     int np = 0, segw = 0, kp = 0, kb = 0, nvar = 1, xr = 0, pitch = 0, lmargin = 0, stages = 0, aslots = 0;
-    bool merge = true;
+    int tpx = 0, xb = 2;
+    bool merge = true, rows_tiles = false;
     uint32_t smem = 0;
     bool ok = false;
 };
@@ -543,8 +548,13 @@ FwdPlan fwd_plan(const Geo& g) {
     P.kp = int((g.k * P.segw + kKB - 1) / kKB * kKB);
     P.kb = P.kp / kKB;
     if (P.kb * 4 > kMaxKGroups || P.kb < 2) return P;
-    const int64_t rows_span = (kTileM - 1) / g.m + 2 > g.m ? g.m : (kTileM - 1) / g.m + 2;  // output rows per tile
+    // CCT_TUNE_GATHER = 3 (A/B): tiles of whole output rows (m <= 128) with three row buffers
+    P.rows_tiles = tuning(CCT_TUNE_GATHER) == 3 && g.m <= kTileM;
+    const int64_t tr = P.rows_tiles ? kTileM / g.m : 0;
+    P.tpx = int(tr ? tr * g.m : kTileM);
+    const int64_t rows_span = tr ? tr : ((kTileM - 1) / g.m + 2 > g.m ? g.m : (kTileM - 1) / g.m + 2);  // output rows per tile
     P.xr = int(g.s * (rows_span - 1) + g.k);
+    P.xb = P.rows_tiles ? 3 : 2;
     P.lmargin = int((g.p * g.d + 4 + 3) & ~int64_t(3));
     P.pitch = int((P.lmargin + 3 + (g.n + g.p) * g.d + P.segw + 8 + 3) & ~int64_t(3));
     if (4 * (P.lmargin + 3 + P.segw) >= 32768) return P;  // byte offsets packed as int16
@@ -552,7 +562,7 @@ FwdPlan fwd_plan(const Geo& g) {
     P.aslots = max_aslots(P.np, P.merge);
     if (P.aslots < kGatherGroups) return P;
     for (int st = 12; st >= 3; --st) {
-        const FwdLayout L = fwd_layout(P.np, st, P.aslots, P.xr, P.pitch, P.kb * 4);
+        const FwdLayout L = fwd_layout(P.np, st, P.aslots, P.xr, P.pitch, P.kb * 4, P.xb);
         if (L.total + 1024 <= uint32_t(kSmemMax)) {
             P.stages = st;
             P.smem = L.total + 1024;
@@ -1078,7 +1088,9 @@ cudaError_t gather_fwd(const Geo& g, const float* x, const float* w, float* y, i
     fp.segw = P.segw;
     fp.nvar = P.nvar;
     fp.kb_tile = P.kb;
-    fp.tpi = int((mm + kTileM - 1) / kTileM);
+    fp.tpx = P.tpx;
+    fp.xb = P.xb;
+    fp.tpi = int((mm + P.tpx - 1) / P.tpx);
     fp.tiles = int(g.b) * fp.tpi;
     fp.pitch = P.pitch;
     fp.lmargin = P.lmargin;
