@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--no-configs", action="store_true", help="skip the configs[0..2] device / CPU lines")
     ap.add_argument("--layout", default="nhwc", choices=["nchw", "nhwc"],
                     help="y / dy layout of every layer (NHWC = the next layer's input order)")
+    ap.add_argument("--h2d-wc", type=int, default=0, help="e2e: write-combined pinned H2D source buffers (1)")
     ap.add_argument("--copy-streams", type=int, default=1,
                     help="e2e: copy streams per direction (measured: 2-3 no faster than 1)")
     ap.add_argument("--tune", default="", help="A/B runs: comma list key=value of cct_set_tuning switches")
@@ -517,7 +518,25 @@ def run_e2e(a, st, torch, world, group, dev):
     from paper_1504_04343_b200.conv import conv_bwd, conv_fwd_cached
     nl = len(st.layers)
     pin = lambda ts: [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in ts]  # noqa: E731
-    hx, hdy = pin(st.x), pin(st.dy)
+    keep = []
+
+    def pin_wc(ts):
+        """Page-locked write-combined host buffers (cudaHostAllocWriteCombined) for the H2D
+        sources: the DMA engine reads them without snooping the CPU caches."""
+        import ctypes
+        from cuda.bindings import runtime as cudart
+        out = []
+        for t in ts:
+            nbytes = t.numel() * t.element_size()
+            err, ptr = cudart.cudaHostAlloc(nbytes, cudart.cudaHostAllocWriteCombined)
+            if int(err) != 0:
+                return pin(ts)
+            buf = (ctypes.c_char * nbytes).from_address(int(ptr))
+            keep.append((ptr, buf))
+            out.append(torch.frombuffer(buf, dtype=t.dtype).view(t.shape))
+        return out
+
+    hx, hdy = (pin_wc(st.x), pin_wc(st.dy)) if a.h2d_wc else (pin(st.x), pin(st.dy))
     hy, hdx, hdw = pin(st.y), pin(st.dx), pin(st.dw)
     for h, t in zip(hx + hdy, st.x + st.dy):
         h.copy_(t.cpu())
@@ -613,7 +632,8 @@ def run_e2e(a, st, torch, world, group, dev):
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
             "h2d_gb_per_s": h2d / (ms * 1e-3) / 1e9, "d2h_gb_per_s": d2h / (ms * 1e-3) / 1e9,
             "path": "C ABI (cct_conv_fwd_cached / cct_conv_bwd) on double-buffered device buffers: pinned-host "
-                    f"H2D of x, dy and D2H of y, dx, dW on {ncs} + {ncs} copy streams overlapping compute"}
+                    f"H2D of x, dy{' (write-combined)' if a.h2d_wc else ''} and D2H of y, dx, dW on {ncs} + {ncs} "
+                    "copy streams overlapping compute"}
 
 
 if __name__ == "__main__":

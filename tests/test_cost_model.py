@@ -56,3 +56,15 @@ def test_ratio_crossover_direction(cct):
         return min(est[1].model_seconds, est[2].model_seconds) / est[0].model_seconds
     lo, hi = rel(64, 1024), rel(1024, 64)
     assert lo > 1.5 and hi < 1.15 and hi < lo
+
+
+def test_fused_conv1_passes_modelled(cct):
+    """CaffeNet conv1 (b = 256) runs the fused small-channel kernels (gather forward /
+    backward-weight, hfold backward-data); the model prices those passes within 25 % of
+    their B200 times (profiles/r02: forward 0.33, backward-data 0.45, backward-weight
+    0.31 ms) and picks Type 1."""
+    desc = cct.ConvDesc(227, 11, 3, 96, 256, 4, 0)
+    for p, ms in ((0, 0.33), (1, 0.45), (2, 0.31)):
+        choice, est = cct.select_lowering(desc, p)
+        assert choice == 1
+        assert 0.75 < est[0].model_seconds * 1e3 / ms < 1.25, (p, est[0].model_seconds)
