@@ -169,7 +169,12 @@ typedef enum {
                                  /* 2: same, forward without the merged N = 2 NP product (A/B)           */
                                  /* 3: same, forward tiles of whole output rows, 3 row buffers (A/B:     */
                                  /*    bitwise equal, 10 % slower on conv1: 16 % more 128-row tiles)     */
-    CCT_TUNE_COUNT = 14
+    CCT_TUNE_FUSED_T23 = 14,     /* 1: Types 2 / 3 run fused when the layer has the implicit (TMA        */
+                                 /* im2col) form: one im2col box per filter tap, the per-tap products    */
+                                 /* accumulated in TMEM (tap-shifted accumulation), so Rhat is never     */
+                                 /* materialised -- the implicit Type 1 kernel.  0 (default): the        */
+                                 /* materialised paper forms, kept as the measured baselines             */
+    CCT_TUNE_COUNT = 15
 } cct_tuning;
 CCT_API cct_status cct_set_tuning(cct_tuning key, int value);
 CCT_API int cct_get_tuning(cct_tuning key); /* -1 for an unknown key */

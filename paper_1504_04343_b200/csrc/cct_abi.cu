@@ -96,13 +96,25 @@ struct Ws {
 
 cudaStream_t as_stream(void* s) { return static_cast<cudaStream_t>(s); }
 
-int resolve(const cct_conv_desc* d, cct_lowering l, cct_pass pass) {
+bool implicit_enabled();
+int resolve_type(const cct_conv_desc* d, cct_lowering l, cct_pass pass) {
     if (l == CCT_LOWER_T1 || l == CCT_LOWER_T2 || l == CCT_LOWER_T3) return int(l);
     cct_calibration cal;
     cct_calibration_default(&cal);
     cct_lowering out = CCT_LOWER_T1;
     if (cct_select_lowering(d, &cal, int(pass), &out, nullptr) != CCT_OK) return 1;
     return int(out);
+}
+// Types 2 / 3 fused (CCT_TUNE_FUSED_T23): with the implicit form available (TMA im2col of x,
+// d % 16 == 0) a fused Type 3 -- the GEMM on the input with the k^2 shifted products summed
+// in the accumulator instead of through a materialised Rhat and a lift -- is exactly the
+// implicit Type 1 kernel (one im2col box per filter tap, tap-shifted accumulation in TMEM),
+// and a fused Type 2 the same with the vertical taps accumulated.
+int resolve(const cct_conv_desc* d, cct_lowering l, cct_pass pass) {
+    const int t = resolve_type(d, l, pass);
+    if ((t == 2 || t == 3) && tuning(CCT_TUNE_FUSED_T23) && implicit_enabled() && im2col_ok(d->d, true))
+        return 1;
+    return t;
 }
 
 // Lowered-matrix geometry of one type.

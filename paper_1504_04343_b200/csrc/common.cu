@@ -36,12 +36,12 @@ constexpr int kTuneDefaults[CCT_TUNE_COUNT] = {
     /* SPLIT_PRODUCER */ 0, /* A_TMEM */ 1,     /* A_TMEM_WIDE */ 1, /* CTA_PAIRS */ 0,
     /* BN384 */ 0,          /* STREAMK */ 1,    /* CHAIN2 */ 1,      /* S2D */ 1,
     /* IMPLICIT_BWD */ 1,   /* WGRAD_SWAP */ 1, /* DGRAD_SWAP */ 0,  /* FWD_SWAP */ 0,
-    /* TRACE_PHASES */ 0,   /* GATHER */ 1};
-constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 3, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1, 3};
+    /* TRACE_PHASES */ 0,   /* GATHER */ 1,     /* FUSED_T23 */ 0};
+constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 3, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1, 3, 1};
 std::atomic<int> g_tune[CCT_TUNE_COUNT] = {
     {kTuneDefaults[0]}, {kTuneDefaults[1]}, {kTuneDefaults[2]},  {kTuneDefaults[3]},  {kTuneDefaults[4]},
     {kTuneDefaults[5]}, {kTuneDefaults[6]}, {kTuneDefaults[7]},  {kTuneDefaults[8]},  {kTuneDefaults[9]},
-    {kTuneDefaults[10]}, {kTuneDefaults[11]}, {kTuneDefaults[12]}, {kTuneDefaults[13]}};
+    {kTuneDefaults[10]}, {kTuneDefaults[11]}, {kTuneDefaults[12]}, {kTuneDefaults[13]}, {kTuneDefaults[14]}};
 }  // namespace
 
 int tuning(int key) { return (key >= 0 && key < CCT_TUNE_COUNT) ? g_tune[key].load(std::memory_order_relaxed) : 0; }

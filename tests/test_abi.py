@@ -175,6 +175,8 @@ def test_tuning_switches_are_explicit():
     cct.reset_tuning()
     defaults = {k: cct.get_tuning(k) for k in cct.TUNE}
     assert defaults["split_producer"] == 0 and defaults["fwd_swap"] == 0 and defaults["s2d"] == 1
+    assert defaults["fused_t23"] == 0 and defaults["gather"] == 1
+    assert L.cct_set_tuning(cct.TUNE["fused_t23"], 2) == 1
     with cct.tuning(s2d=2, split_producer=1):
         assert cct.get_tuning("s2d") == 2 and cct.get_tuning("split_producer") == 1
     assert {k: cct.get_tuning(k) for k in cct.TUNE} == defaults
@@ -192,3 +194,20 @@ def test_library_reads_no_environment():
     assert srcs
     offenders = [p for p in srcs if "getenv" in open(p).read()]
     assert not offenders, offenders
+
+
+def test_fused_t23_resolves_to_implicit_type1():
+    """CPU: with CCT_TUNE_FUSED_T23 a Type 2 / 3 request on a layer with the implicit form
+    (conv2, d = 96) sizes exactly like implicit Type 1 (no Rhat workspace, no lowered cache);
+    conv1 (d = 3) keeps its materialised Type 2 / 3 sizes."""
+    import paper_1504_04343_b200 as cct
+    conv2 = cct.ConvDesc(27, 5, 96, 256, 32, 1, 2)
+    conv1 = cct.ConvDesc(227, 11, 3, 96, 8, 4, 0)
+    ws = lambda d, t: [cct.workspace_size(d, t, p) for p in range(3)]
+    base2, base1 = {t: ws(conv2, t) for t in (1, 2, 3)}, {t: ws(conv1, t) for t in (1, 2, 3)}
+    assert base2[3][0] > base2[1][0] and cct.lowered_cache_size(conv2, 3) > 0
+    with cct.tuning(fused_t23=1):
+        for t in (2, 3):
+            assert ws(conv2, t) == base2[1] and cct.lowered_cache_size(conv2, t) == 0
+            assert ws(conv1, t) == base1[t]
+    assert ws(conv2, 3) == base2[3]

@@ -506,6 +506,48 @@ def test_space_to_depth(cct, dev, orc, layer):
         assert torch.equal(y, ym) and torch.equal(dx, dxm)
 
 
+@pytest.mark.parametrize("t", [2, 3])
+@pytest.mark.parametrize("layer", [CAFFENET[1], CAFFENET[2], ("d3", 11, 4, 3, 16, 1, 1)], ids=lambda l: l[0])
+def test_fused_types_2_3(cct, dev, orc, layer, t):
+    """CCT_TUNE_FUSED_T23: a Type 2 / 3 request on a layer with the implicit form (d % 16 == 0)
+    runs fused -- the k^2 (Type 3) or k (Type 2) shifted products accumulated in TMEM, one
+    im2col box per tap, no Rhat and no lift pass: bit for bit the implicit Type 1 result, and
+    within the oracle tolerance.  Without the implicit form (d = 3) the request stays the
+    materialised Type 2 / 3 path (lift phase recorded)."""
+    import ctypes as C
+    from paper_1504_04343_b200 import conv
+    L = cct.lib()
+    _, n, k, d, o, s, p = layer
+    b = 4
+    desc = cct.ConvDesc(n, k, d, o, b, s, p)
+    m = desc.m
+    x_np, w_np = orc.random_problem(91, b, n, d, k, o)
+    dy_np = orc.uniform(92, b * o * m * m)
+    x, w, dy = T(x_np, dev, b, n, n, d), T(w_np, dev, o, k, k, d), T(dy_np, dev, b, o, m, m)
+    P = C.c_double * 7
+    ms, fl, by = P(), P(), P()
+    cnt = (C.c_uint64 * 7)()
+    with cct.tuning(fused_t23=1):
+        L.cct_profile_read(None, None, None, None, 1)
+        L.cct_profile_enable(1)
+        yf = conv.conv_fwd(x, w, desc, t)
+        dxf = conv.conv_bwd_data(dy, w, desc, t)
+        dwf = conv.conv_bwd_weight(x, dy, desc, t)
+        torch.cuda.synchronize()
+        L.cct_profile_enable(0)
+        L.cct_profile_read(ms, fl, by, cnt, 1)
+    fused = d % 16 == 0
+    assert (cnt[2] == 0) == fused  # lift phase only on the materialised Type 2 / 3 path
+    y1, dx1, dw1 = (conv.conv_fwd(x, w, desc, 1), conv.conv_bwd_data(dy, w, desc, 1),
+                    conv.conv_bwd_weight(x, dy, desc, 1))
+    if fused:
+        assert torch.equal(yf, y1) and torch.equal(dxf, dx1) and torch.equal(dwf, dw1)
+    refs = (orc.conv_fwd(x_np, w_np, b, n, d, k, o, s, p), orc.conv_bwd_data(dy_np, w_np, b, n, d, k, o, s, p),
+            orc.conv_bwd_weight(x_np, dy_np, b, n, d, k, o, s, p))
+    for got, ref in zip((yf, dxf, dwf), refs):
+        assert rel_l2(got.cpu().numpy().ravel(), ref) <= TOL
+
+
 SWAP_SCRIPT = r"""
 import os, sys, json
 import numpy as np, torch
