@@ -174,7 +174,11 @@ typedef enum {
                                  /* accumulated in TMEM (tap-shifted accumulation), so Rhat is never     */
                                  /* materialised -- the implicit Type 1 kernel.  0 (default): the        */
                                  /* materialised paper forms, kept as the measured baselines             */
-    CCT_TUNE_COUNT = 15
+    CCT_TUNE_OVERLAP = 15,       /* 1 (default): inside one cct_conv_bwd call, the backward-weight of a  */
+                                 /* fused small-channel layer runs on a library-owned high-priority     */
+                                 /* side stream beside the backward-data's vertical fold (event fork /  */
+                                 /* join; the call's stream still orders everything).  0: one stream    */
+    CCT_TUNE_COUNT = 16
 } cct_tuning;
 CCT_API cct_status cct_set_tuning(cct_tuning key, int value);
 CCT_API int cct_get_tuning(cct_tuning key); /* -1 for an unknown key */

@@ -34,7 +34,7 @@ OK, ERR_CONFIG, ERR_RESOURCE, ERR_CUDA, ERR_UNSUPPORTED = 0, 1, 2, 3, 4
 # cct_tuning keys (include/cct.h): explicit process-wide switches between measured variants
 TUNE = {"split_producer": 0, "a_tmem": 1, "a_tmem_wide": 2, "cta_pairs": 3, "bn384": 4, "streamk": 5,
         "chain2": 6, "s2d": 7, "implicit_bwd": 8, "wgrad_swap": 9, "dgrad_swap": 10, "fwd_swap": 11,
-        "trace_phases": 12, "gather": 13, "fused_t23": 14}
+        "trace_phases": 12, "gather": 13, "fused_t23": 14, "overlap": 15}
 
 
 class CctError(RuntimeError):

@@ -610,6 +610,21 @@ cct_status run_bwd_one(const Geo& g, int type, const float* x, const float* cach
     if (dx && t1_hfold_dgrad(g, type) && aligned16(or_plan(dy, ws))) {  // (dx: plain stores)
         const size_t mark = ws.off;
         float* w2 = ws.take(hfold_dgrad_ws_floats(g));
+        const Fork* fk = dw && tuning(CCT_TUNE_OVERLAP) ? fork_resources() : nullptr;
+        if (fk) {
+            // the backward-weight (x, dy -> dW; scratch above H) on the side stream from the end of
+            // the backward-data GEMM, beside the vertical fold; joined back into st
+            if (ws.base) {
+                CCT_TRY(hfold_dgrad(g, dy, w, dx, w2, st, fk->fork), "fused backward-data");
+                CCT_TRY(cudaStreamWaitEvent(fk->side, fk->fork, 0), "fork");
+            }
+            cct_status s = run_bwd_one(g, type, x, cache, dy, w, nullptr, dw, ws, ws.base ? fk->side : st);
+            if (ws.base) {  // joined on every path, so st never runs ahead of the side stream's work
+                CCT_TRY(cudaEventRecord(fk->join, fk->side), "join");
+                CCT_TRY(cudaStreamWaitEvent(st, fk->join, 0), "join");
+            }
+            return s;
+        }
         if (ws.base) CCT_TRY(hfold_dgrad(g, dy, w, dx, w2, st), "fused backward-data");
         if (!dw) return CCT_OK;
         const size_t hi = ws.off;

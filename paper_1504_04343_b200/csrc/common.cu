@@ -36,12 +36,13 @@ constexpr int kTuneDefaults[CCT_TUNE_COUNT] = {
     /* SPLIT_PRODUCER */ 0, /* A_TMEM */ 1,     /* A_TMEM_WIDE */ 1, /* CTA_PAIRS */ 0,
     /* BN384 */ 0,          /* STREAMK */ 1,    /* CHAIN2 */ 1,      /* S2D */ 1,
     /* IMPLICIT_BWD */ 1,   /* WGRAD_SWAP */ 1, /* DGRAD_SWAP */ 0,  /* FWD_SWAP */ 0,
-    /* TRACE_PHASES */ 0,   /* GATHER */ 1,     /* FUSED_T23 */ 0};
-constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 3, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1, 3, 1};
+    /* TRACE_PHASES */ 0,   /* GATHER */ 1,     /* FUSED_T23 */ 0,   /* OVERLAP */ 1};
+constexpr int kTuneMax[CCT_TUNE_COUNT] = {1, 3, 1, 2, 1, 1, 1, 2, 2, 1, 2, 1, 1, 3, 1, 1};
 std::atomic<int> g_tune[CCT_TUNE_COUNT] = {
     {kTuneDefaults[0]}, {kTuneDefaults[1]}, {kTuneDefaults[2]},  {kTuneDefaults[3]},  {kTuneDefaults[4]},
     {kTuneDefaults[5]}, {kTuneDefaults[6]}, {kTuneDefaults[7]},  {kTuneDefaults[8]},  {kTuneDefaults[9]},
-    {kTuneDefaults[10]}, {kTuneDefaults[11]}, {kTuneDefaults[12]}, {kTuneDefaults[13]}, {kTuneDefaults[14]}};
+    {kTuneDefaults[10]}, {kTuneDefaults[11]}, {kTuneDefaults[12]}, {kTuneDefaults[13]}, {kTuneDefaults[14]},
+    {kTuneDefaults[15]}};
 }  // namespace
 
 int tuning(int key) { return (key >= 0 && key < CCT_TUNE_COUNT) ? g_tune[key].load(std::memory_order_relaxed) : 0; }
@@ -64,6 +65,41 @@ uint64_t g_acc_n[kNumPhases];
 }  // namespace
 
 void profile_enable(bool on) { g_prof.store(on); }
+
+namespace {
+struct ForkSet {
+    Fork f[16] = {};
+    bool made[16] = {};
+    ~ForkSet() {
+        for (int i = 0; i < 16; ++i)
+            if (made[i]) {
+                cudaStreamDestroy(f[i].side);
+                cudaEventDestroy(f[i].fork);
+                cudaEventDestroy(f[i].join);
+            }
+    }
+};
+thread_local ForkSet t_fork;
+}  // namespace
+
+const Fork* fork_resources() {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return nullptr;
+    if (!t_fork.made[dev]) {
+        int lo = 0, hi = 0;
+        Fork& f = t_fork.f[dev];
+        if (cudaDeviceGetStreamPriorityRange(&lo, &hi) != cudaSuccess ||
+            cudaStreamCreateWithPriority(&f.side, cudaStreamNonBlocking, hi) != cudaSuccess)
+            return nullptr;
+        if (cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&f.join, cudaEventDisableTiming) != cudaSuccess) {
+            cudaStreamDestroy(f.side);
+            return nullptr;
+        }
+        t_fork.made[dev] = true;
+    }
+    return &t_fork.f[dev];
+}
 
 PhaseScope::PhaseScope(Phase ph, cudaStream_t s, double flops, double bytes) : slot(-1), st(s) {
     if (tuning(CCT_TUNE_TRACE_PHASES)) fprintf(stderr, "cct-phase %d bytes %.0f flops %.0f\n", int(ph), bytes, flops);

@@ -26,6 +26,15 @@ struct PhaseScope {
     cudaStream_t st;
 };
 void profile_enable(bool on);
+
+// In-call fork / join (CCT_TUNE_OVERLAP): per host thread and device, a high-priority side stream
+// and two events, so independent work inside one ABI call (the backward-weight beside the
+// backward-data's fold) runs concurrently.  Null when they cannot be created.
+struct Fork {
+    cudaStream_t side;
+    cudaEvent_t fork, join;
+};
+const Fork* fork_resources();
 // sync + accumulate: ms, flops, bytes, launches per phase (arrays of kNumPhases)
 void profile_read(double* ms, double* flops, double* bytes, uint64_t* launches, bool reset);
 

@@ -1,6 +1,9 @@
 // dgrad.cu -- fused backward-data of small-channel strided Type 1 layers (see dgrad.cuh).
 //
-// GEMM (per tile = TR output rows of one image, <= 128 pixels, lanes = pixels):
+// GEMM (per tile = 4 x (32 - (NF - 1)) consecutive output pixels of the flattened (image, row,
+// column) order; TMEM lane quadrant w holds pixels [P0 + w (32 - (NF - 1)) - (NF - 1), + 32), so
+// its first NF - 1 lanes repeat the previous quadrant's last pixels -- the horizontal fold then
+// needs only warp shuffles -- and do not store):
 //   D (pixels x lowered columns of a filter-row group) = dy tile (pixels x o) * Khat^T group,
 //   3xTF32 on tcgen05 (A_small B_big + A_big B_small + A_big B_big), fp32 accumulate in TMEM.
 // The lowered columns of filter row i sit at [i KDP, i KDP + k d) of its group (KDP = k d
@@ -39,22 +42,22 @@ constexpr uint32_t kABytes = kTileM * kKB * 4;  // one raw dy k-block (128 pixel
 struct Params {
     float* H;                   // [q][r][i][XP]
     int b, m, k, o, XP;
-    int TR, tpi, tiles;         // output rows per tile, tiles per image, total tiles
+    int ov, wpix, npix, tiles;  // repeated lanes per quadrant (NF - 1), new pixels per quadrant, pixels, tiles
     int ngroups, fr, kb;        // filter-row groups, rows per group, k-blocks over o
     int nmax;                   // B rows reserved per (k-block, half) in smem
     int npad[kMaxGroups];       // N of each group (multiple of 32)
     int brow0[kMaxGroups];      // first prepared-bank row of each group ([big | small] rows)
+    int dbg;                    // 0 in the product; tools/hfold_probe.cu drops stages to find the bound
 };
 
 struct Layout {
-    uint32_t b, a, xch, bars, total;
+    uint32_t b, a, bars, total;
 };
-__host__ __device__ inline Layout layout(int nmax, int kb, int kdp) {
+__host__ __device__ inline Layout layout(int nmax, int kb) {
     Layout L;
     L.b = 0;
     L.a = uint32_t(kb) * 2u * uint32_t(nmax) * 64u;
-    L.xch = L.a + kRA * kABytes;
-    L.bars = (L.xch + 2u * 2u * 4u * 2u * uint32_t(kdp) * 4u + 15u) & ~15u;  // [half][parity][warp][2 lanes]
+    L.bars = L.a + kRA * kABytes;
     L.total = L.bars + uint32_t(2 * kRA + 4 + 4 + 4) * 8u + 16u;
     return L;
 }
@@ -70,7 +73,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(NF >= 1 && NF <= 3 && KDP <= 36 && SD % 4 == 0, "fold geometry");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
-    const Layout L = layout(p.nmax, p.kb, KDP);
+    const Layout L = layout(p.nmax, p.kb);
     // afull / aempty: raw dy stage (TMA bytes / the transform has read it); sfull / sempty: TMEM
     // A slot (transform wrote big | small / MMA commit); bbar / bempty: group bank; tfull / tempty
     uint64_t* afull = reinterpret_cast<uint64_t*>(smem + L.bars);
@@ -84,7 +87,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
     const int RS = a_slots(p.nmax);
     const uint32_t A_COL = uint32_t(2 * p.nmax);
-    float* xch = reinterpret_cast<float*>(smem + L.xch);
 
     const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
     if (warp == 0 && lane == 0) {
@@ -131,13 +133,15 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             __syncwarp();
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x) {
-                const int q = T / p.tpi;
-                const int pix = q * mm + (T - q * p.tpi) * p.TR * p.m;
+                const int pix = T * 4 * p.wpix - p.ov;  // may start before pixel 0: TMA zero-fills
                 for (int kb = 0; kb < p.kb; ++kb) {
                     ptx::mbar_wait_sleep(&aempty[as], aph ^ 1);
                     if (ptx::elect_one()) {
                         ptx::mbar_arrive_expect_tx(&afull[as], kABytes);
-                        ptx::tma_load_2d(smem + L.a + uint32_t(as) * kABytes, &tmA, &afull[as], kb * kKB, pix);
+#pragma unroll
+                        for (int w = 0; w < 4; ++w)
+                            ptx::tma_load_2d(smem + L.a + uint32_t(as) * kABytes + uint32_t(w) * (kABytes / 4), &tmA,
+                                             &afull[as], kb * kKB, pix + w * p.wpix);
                     }
                     __syncwarp();
                     if (++as == kRA) { as = 0; aph ^= 1; }
@@ -166,6 +170,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (ptx::elect_one()) {
 #pragma unroll
                         for (int kk = 0; kk < 2; ++kk) {
+                            if (p.dbg & 4) break;
                             const uint64_t bb = ptx::smem_desc(bbig + kk * 32, 16, 512, 4);
                             const uint64_t bs = ptx::smem_desc(bsml + kk * 32, 16, 512, 4);
                             ptx::mma_tf32_ts(d0, asml + kk * 8, bb, idesc, (kb | kk) ? 1u : 0u);  // small products first
@@ -188,26 +193,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ===================== epilogue: horizontal fold into H =====================
         const int qd = warp & 3;
         const int half = warp >= 12 ? 1 : 0;  // filter rows il = half, half + 2, ...
-        const int l = qd * 32 + lane;
-        const int rl = l / p.m, cc = l - rl * p.m;  // this lane's pixel (row within the tile, column)
-        int lt = 0, nb = 0;
+        int lt = 0;
         for (int g = 0; g < p.ngroups; ++g) {
             const int i0 = g * p.fr, nrow = min(p.fr, p.k - i0);
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
                 const int acc = lt & 1;
-                const int q = T / p.tpi;
-                const int r = (T - q * p.tpi) * p.TR + rl;
-                const bool ok = rl < p.TR && r < p.m;
+                const int P = T * 4 * p.wpix + qd * p.wpix + lane - p.ov;  // this lane's pixel
+                const int q = P / mm, rr = P - q * mm, r = rr / p.m, cc = rr - r * p.m;
+                const bool ok = lane >= p.ov && P < p.npix;
                 ptx::mbar_wait_sleep(&tfull[acc], (lt >> 1) & 1);
                 ptx::tc_fence_after();
+                if (p.dbg & 1) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                    continue;
+                }
                 const uint32_t tc0 = tmem + (uint32_t(qd * 32) << 16) + uint32_t(acc * p.nmax);
                 uint32_t u[32], t4[4];
                 if (half < nrow) {
                     ptx::tmem_ld_32x32b_x32(tc0 + uint32_t(half * KDP), u);
                     if constexpr (KDP > 32) ptx::tmem_ld_32x32b_x4(tc0 + uint32_t(half * KDP + 32), t4);
                 }
-                for (int il = half; il < nrow; il += 2, ++nb) {
+                for (int il = half; il < nrow; il += 2) {
                     ptx::tmem_ld_wait();
+                    if (p.dbg & 8) {
+                        if (il + 2 < nrow) {
+                            ptx::tmem_ld_32x32b_x32(tc0 + uint32_t((il + 2) * KDP), u);
+                            if constexpr (KDP > 32) ptx::tmem_ld_32x32b_x4(tc0 + uint32_t((il + 2) * KDP + 32), t4);
+                        }
+                        continue;
+                    }
                     float v[KDP];
 #pragma unroll
                     for (int e = 0; e < KDP; ++e) v[e] = __uint_as_float(e < 32 ? u[e] : t4[e - 32]);
@@ -215,15 +230,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         ptx::tmem_ld_32x32b_x32(tc0 + uint32_t((il + 2) * KDP), u);
                         if constexpr (KDP > 32) ptx::tmem_ld_32x32b_x4(tc0 + uint32_t((il + 2) * KDP + 32), t4);
                     }
-                    // the last NF - 1 lanes' runs, for lane 0.. of the next warp (double-buffered)
-                    float* xh = xch + (half * 2 + (nb & 1)) * 4 * 2 * KDP;
-                    float* xw = xh + qd * 2 * KDP;
-                    if (lane >= 32 - (NF - 1)) {
-#pragma unroll
-                        for (int e = 0; e < KDP; ++e) xw[(lane - (32 - (NF - 1))) * KDP + e] = v[e];
-                    }
-                    ptx::named_bar_sync(1 + half, 128);
-                    const float* xp = xh + (qd > 0 ? qd - 1 : 0) * 2 * KDP;
                     float out[KD];
 #pragma unroll
                     for (int e = 0; e < KD; ++e) out[e] = v[e];
@@ -231,12 +237,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int f = 1; f < NF; ++f) {
 #pragma unroll
                         for (int e = 0; e + f * SD < KD; ++e) {
-                            float pv = __shfl_up_sync(0xffffffffu, v[e + f * SD], f);
-                            if (lane < f) pv = qd > 0 ? xp[(lane + (NF - 1) - f) * KDP + e + f * SD] : 0.f;
+                            // lanes < f read garbage: they are repeated lanes (lane < ov), not stored
+                            const float pv = __shfl_up_sync(0xffffffffu, v[e + f * SD], f);
                             out[e] += cc >= f ? pv : 0.f;
                         }
                     }
-                    if (ok) {
+                    if (ok && !(p.dbg & 16)) {
                         float* hrow = p.H + (int64_t(q * p.m + r) * p.k + (i0 + il)) * p.XP + SD * cc;
 #pragma unroll
                         for (int e = 0; e < SD; e += 4)
@@ -262,6 +268,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x)
                 for (int kb = 0; kb < p.kb; ++kb) {
                     ptx::mbar_wait_sleep(&afull[as], aph);
+                    if (p.dbg & 2) {
+                        ptx::mbar_wait(&sempty[ss], sph ^ 1);
+                        __syncwarp();
+                        if (lane == 0) {
+                            ptx::mbar_arrive(&sfull[ss]);
+                            ptx::mbar_arrive(&aempty[as]);
+                        }
+                        if (++as == kRA) { as = 0; aph ^= 1; }
+                        if (++ss == RS) { ss = 0; sph ^= 1; }
+                        continue;
+                    }
                     const uint32_t raw = a_u + uint32_t(as) * kABytes;
                     // row r of the K-major SWIZZLE_64B tile: 16-byte chunk c at (c ^ (r / 2 % 4))
                     float4 x[4];
@@ -304,31 +321,33 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 // dx[q][y][x] = sum_{r: 0 <= y + p - s r < k, 0 <= r < m} H[q][r][y + p - s r][x + p d]  (r ascending)
-// (H columns >= XW, the padded input columns no filter window reaches, are zero).  Grid-stride
-// over (dx row, 4 columns): float4 loads of the <= ceil(k / s) H rows (p d % 4 == 0), 4 stores.
-__global__ void vfold_kernel(const float* __restrict__ H, float* __restrict__ dx, int rows, int n, int d, int k, int s,
-                             int p, int m, int XP, int XW) {
-    const int nd = n * d, nx4 = (nd + 3) / 4;
-    const int64_t items = int64_t(rows) * nx4;
-    for (int64_t it = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; it < items; it += int64_t(gridDim.x) * blockDim.x) {
-        const int row = int(it / nx4), x = int(it - int64_t(row) * nx4) * 4;  // row = q n + y
-        const int q = row / n, y = row - q * n;
-        const int yp = y + p, xp = x + p * d;
-        const int rlo = max(0, (yp - k + s) / s), rhi = min(m - 1, yp / s);
-        float4 a = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (xp < XW)
-            for (int r = rlo; r <= rhi; ++r) {
+// (H columns >= XW, the padded input columns no filter window reaches, are zero).  One block per
+// dx row (blockIdx.x = q n + y: no per-element divisions), a thread per 4 columns: the <= NF
+// (= ceil(k / s) <= 3) H rows' float4 loads issued together, then the sum in r order.
+__global__ void vfold_kernel(const float* __restrict__ H, float* __restrict__ dx, int n, int d, int k, int s, int p,
+                             int m, int XP, int XW) {
+    const int row = blockIdx.x, q = row / n, y = row - q * n;
+    const int nd = n * d, yp = y + p;
+    const int rlo = max(0, (yp - k + s) / s), rhi = min(m - 1, yp / s);
+    for (int x = int(threadIdx.x) * 4; x < nd; x += int(blockDim.x) * 4) {
+        const int xp = x + p * d;
+        float4 h[3];
+    #pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            h[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+            const int r = rlo + j;
+            if (r <= rhi && xp < XW) {
                 const float* hp = H + (int64_t(q * m + r) * k + (yp - s * r)) * XP + xp;
-                float4 h;
                 if (((p * d) & 3) == 0) {
-                    h = __ldg(reinterpret_cast<const float4*>(hp));
+                    h[j] = __ldg(reinterpret_cast<const float4*>(hp));
                 } else {  // unaligned padded column offset (row pitch XP >= XW + 3 keeps hp[3] in bounds)
-                    h = make_float4(__ldg(hp), __ldg(hp + 1), __ldg(hp + 2), __ldg(hp + 3));
+                    h[j] = make_float4(__ldg(hp), __ldg(hp + 1), __ldg(hp + 2), __ldg(hp + 3));
                 }
-                a.x += h.x; a.y += h.y; a.z += h.z; a.w += h.w;
             }
+        }
+        const float av[4] = {(h[0].x + h[1].x) + h[2].x, (h[0].y + h[1].y) + h[2].y, (h[0].z + h[1].z) + h[2].z,
+                             (h[0].w + h[1].w) + h[2].w};
         float* o = dx + int64_t(row) * nd + x;
-        const float av[4] = {a.x, a.y, a.z, a.w};
 #pragma unroll
         for (int u = 0; u < 4; ++u)
             if (x + u < nd) o[u] = xp + u < XW ? av[u] : 0.f;
@@ -390,20 +409,23 @@ struct Plan {
     bool ok = false;
 };
 
+int g_probe_dbg = 0;  // Params::dbg of every launch (set only by tools/hfold_probe.cu)
+
 Plan plan(const Geo& g) {
     Plan P;
     const int64_t kd = g.k * g.d, sd = g.s * g.d;
     // instantiated fold geometries (k d, s d): CaffeNet / AlexNet conv1 (33, 12), test shapes
     const bool geo_ok = (kd == 33 && sd == 12) || (kd == 20 && sd == 8) || (kd == 28 && sd == 16);
-    if (!geo_ok || g.m < 2 || g.m > kTileM || g.o < 1 || g.o > 96 || g.o % 4 != 0 || g.k > 32) return P;
+    if (!geo_ok || g.m < 2 || g.o < 1 || g.o > 96 || g.o % 4 != 0 || g.k > 32) return P;
     if (g.b * g.m * g.m >= (int64_t(1) << 31) - kTileM || g.b * g.n * g.n * g.d >= (int64_t(1) << 40)) return P;
     P.kdp = int((kd + 3) & ~int64_t(3));
     Params& p = P.p;
     p.b = int(g.b); p.m = int(g.m); p.k = int(g.k); p.o = int(g.o);
     p.XP = int((sd * (g.m - 1) + kd + 3 + 3) & ~int64_t(3));  // >= XW + 3: vfold's 4-float reads
-    p.TR = int(kTileM / g.m);
-    p.tpi = (p.m + p.TR - 1) / p.TR;
-    p.tiles = p.b * p.tpi;
+    p.ov = int((kd + sd - 1) / sd) - 1;
+    p.wpix = 32 - p.ov;
+    p.npix = int(g.b * g.m * g.m);
+    p.tiles = (p.npix + 4 * p.wpix - 1) / (4 * p.wpix);
     p.kb = (p.o + kKB - 1) / kKB;
     P.kp = p.kb * kKB;
     // filter-row groups: N = rows x KDP <= 256 (multiple of 32), balanced
@@ -422,7 +444,7 @@ Plan plan(const Geo& g) {
     }
     if (a_slots(p.nmax) < 2) return P;
     P.rows = row;
-    const Layout L = layout(p.nmax, p.kb, P.kdp);
+    const Layout L = layout(p.nmax, p.kb);
     if (L.total + 1024 > uint32_t(kSmemMax)) return P;
     P.smem = L.total + 1024;
     P.grid = std::min(num_sms(), p.tiles);
@@ -444,10 +466,12 @@ int64_t hfold_dgrad_ws_floats(const Geo& g) {
     return h + int64_t(P.rows) * P.kp + nhwc;
 }
 
-cudaError_t hfold_dgrad(const Geo& g, const float* dy, const float* w, float* dx, float* ws, cudaStream_t st) {
+cudaError_t hfold_dgrad(const Geo& g, const float* dy, const float* w, float* dx, float* ws, cudaStream_t st,
+                        cudaEvent_t gemm_done) {
     Plan P = hf::plan(g);
     if (!P.ok) return cudaErrorInvalidValue;
     Params& p = P.p;
+    p.dbg = g_probe_dbg;
     const int64_t mm = g.m * g.m;
     float* H = ws;
     float* bp = H + int64_t(p.b) * p.m * p.k * p.XP;
@@ -468,7 +492,7 @@ cudaError_t hfold_dgrad(const Geo& g, const float* dy, const float* w, float* dx
         if (e != cudaSuccess) return e;
     }
     CUtensorMap ta, tb;
-    if (!kmajor_map(&ta, dyn, g.b * mm, g.o, g.o, kTileM) || !kmajor_map(&tb, bp, P.rows, P.kp, P.kp, 32))
+    if (!kmajor_map(&ta, dyn, g.b * mm, g.o, g.o, 32) || !kmajor_map(&tb, bp, P.rows, P.kp, P.kp, 32))
         return cudaErrorInvalidValue;
     {
         PhaseScope ps(kPhaseGemm, st, 2.0 * double(g.b) * double(mm) * double(g.k * g.k * g.d) * double(g.o), 0);
@@ -487,13 +511,20 @@ cudaError_t hfold_dgrad(const Geo& g, const float* dy, const float* w, float* dx
         else go(conv_dgrad_hfold_kernel<28, 16>);
         if (e != cudaSuccess) return e;
     }
+    if (gemm_done) {
+        cudaError_t e = cudaEventRecord(gemm_done, st);
+        if (e != cudaSuccess) return e;
+    }
     {
         PhaseScope ps(kPhaseCol2im, st, 0, 4.0 * (double(p.b) * p.m * p.k * p.XP + double(g.b) * g.n * g.n * g.d));
         const int rows = int(g.b * g.n);
-        const int64_t items = int64_t(rows) * ((g.n * g.d + 3) / 4);
         const int xw = int(g.s * g.d * (g.m - 1) + g.k * g.d);
-        vfold_kernel<<<grid_for(items, 256, 16), 256, 0, st>>>(H, dx, rows, int(g.n), int(g.d), int(g.k), int(g.s),
-                                                              int(g.p), p.m, p.XP, xw);
+        // the fold may run beside a persistent max-shared-memory kernel: keep the SM's carve-out there
+        static const cudaError_t carve =
+            cudaFuncSetAttribute(vfold_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+        (void)carve;
+        const int threads = int(std::min<int64_t>(1024, (g.n * g.d + 127) / 128 * 32));
+        vfold_kernel<<<rows, threads, 0, st>>>(H, dx, int(g.n), int(g.d), int(g.k), int(g.s), int(g.p), p.m, p.XP, xw);
         note_launch();
     }
     return cudaGetLastError();

@@ -22,7 +22,10 @@ namespace cct {
 
 bool hfold_dgrad_ok(const Geo& g);
 int64_t hfold_dgrad_ws_floats(const Geo& g);
-// dx (NHWC) = backward-data of dy (layout g.yl) through the kernel bank w (o, k, k, d)
-cudaError_t hfold_dgrad(const Geo& g, const float* dy, const float* w, float* dx, float* ws, cudaStream_t st);
+// dx (NHWC) = backward-data of dy (layout g.yl) through the kernel bank w (o, k, k, d), on st:
+// the GEMM + horizontal fold, then the vertical fold (vfold_kernel, reading H from ws).  When
+// gemm_done is not null it is recorded on st between the two (the caller may fork there).
+cudaError_t hfold_dgrad(const Geo& g, const float* dy, const float* w, float* dx, float* ws, cudaStream_t st,
+                        cudaEvent_t gemm_done = nullptr);
 
 }  // namespace cct

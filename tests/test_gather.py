@@ -176,6 +176,8 @@ DGEOMS = [
     (63, 11, 3, 96, 1, 4, 5),    # pad > k / 2, m = 16
     (31, 5, 4, 32, 2, 2, 1),     # k d = 20, s d = 8, ragged right edge
     (40, 7, 4, 48, 3, 4, 3),     # k d = 28, s d = 16
+    (531, 11, 3, 16, 1, 4, 0),   # m = 131 > 128: an output row spans tiles
+    (15, 11, 3, 8, 5, 4, 2),     # m = 2: tiles span many images
 ]
 
 
@@ -226,8 +228,20 @@ def test_hfold_dgrad_full_batch(cct, dev):
         den += float((ref ** 2).sum())
     err = (num / den) ** 0.5
     assert err <= TOL, f"rel-L2 {err:.3e}"
-    dx2, _ = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x)
+    dx2, dw2 = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x)
     assert torch.equal(dx2, dx)
+    # CCT_TUNE_OVERLAP: the backward-weight on the side stream beside the vertical fold, joined
+    # back into the call's stream -- same bits as one stream, and ordered for the caller
+    with cct.tuning(overlap=0):
+        dx3, dw3 = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x)
+    assert torch.equal(dx3, dx) and torch.equal(dw3, dw2)
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        dx4, dw4 = conv.conv_bwd(dy, w, desc, cct.LOWER_T1, x=x, stream=s)
+        dw5 = dw4.clone()  # consumer on the caller's stream right after the call
+    s.synchronize()
+    assert torch.equal(dx4, dx) and torch.equal(dw5, dw2)
 
 
 def test_fused_conv1_under_workspace_limit(cct, dev):
