@@ -57,6 +57,9 @@ struct FwdParams {
     int stages;                // kernel-bank ring depth (smem)
     int aslots;                // A slot ring depth (TMEM)
     int relu;
+    int dbg;                   // 0 in the product; tools/gather_probe.cu drops stages to find the bound
+    unsigned long long* trace; // null in the product; tools/gather_probe.cu: CTA 0 event clocks
+    int pace_ns;               // epilogue pause between 32-column TMEM chunks
 };
 
 // MERGE (NP <= 96): the two products that share A_big run as ONE N = 2 NP MMA over the
@@ -146,6 +149,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = __shfl_sync(0xffffffffu, int(threadIdx.x >> 5), 0), lane = threadIdx.x & 31;
+    const bool spin = (p.dbg & 64) != 0;
+    // probe trace: [role][tile][event] clock64 of CTA 0 (role 0 MMA, 1 gather group 0, 2 epilogue,
+    // 3 row producer, 4 bank producer)
+    unsigned long long* const trc = (p.trace && blockIdx.x == 0) ? p.trace : nullptr;
+#define FTR(role, lt, ev) \
+    do { if (trc && lane == 0 && (lt) < 64) trc[(size_t(role) * 64 + (lt)) * 32 + (ev)] = clock64(); } while (0)
+    auto fwait = [spin](uint64_t* bar, uint32_t par) {
+        if (spin) ptx::mbar_wait(bar, par);
+        else ptx::mbar_wait_sleep(bar, par);
+    };
     // zero the stage buffers (their margins are never written by the row copies) and the
     // zero row; build the k-block tables: group g of k-block kb -> (filter row, offset)
     {
@@ -205,17 +218,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ===================== kernel-bank producer (warp-uniform loop, elected issue) =====================
         {
-            int st = 0;
+            int st = 0, lbt = 0;
             uint32_t ph = 0;
-            for (int T = blockIdx.x; T < p.tiles; T += gridDim.x) {
+            for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lbt) {
                 const int row0 = variant_of(p, T / p.tpi) * 2 * p.o;  // this image's bank variant
                 for (int kb = 0; kb < p.kb_tile; ++kb) {
-                    ptx::mbar_wait_sleep(&bempty[st], ph ^ 1);
+                    fwait(&bempty[st], ph ^ 1);
+                    FTR(4, lbt, 1 + kb);
                     if (ptx::elect_one()) {
+                        if (p.dbg & 16) {
+                            ptx::mbar_arrive(&bfull[st]);
+                        } else {
                         ptx::mbar_arrive_expect_tx(&bfull[st], 2 * C_::B_BYTES);
                         uint8_t* dst = smem + L.ring + uint32_t(st) * 2 * C_::B_BYTES;
                         ptx::tma_load_2d(dst, &tmB, &bfull[st], kb * kKB, row0);                      // small
                         ptx::tma_load_2d(dst + C_::B_BYTES, &tmB, &bfull[st], kb * kKB, row0 + p.o);  // big
+                        }
                     }
                     __syncwarp();
                     if (++st == RB) { st = 0; ph ^= 1; }
@@ -235,18 +253,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
                 const int acc = lt & 1;
                 ptx::mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
+                FTR(0, lt, 0);
                 ptx::tc_fence_after();
                 const uint32_t d0 = tmem + uint32_t(acc * C_::ACC_COLS);
                 for (int kb = 0; kb < p.kb_tile; ++kb) {
                     ptx::mbar_wait(&bfull[bs], bph);
+                    FTR(5, lt, 1 + kb);
                     ptx::mbar_wait(&afull[as], aph);
+                    FTR(0, lt, 1 + kb);
                     ptx::tc_fence_after();
                     const uint32_t bsml = ring_u + uint32_t(bs) * 2 * C_::B_BYTES;  // [small | big] rows
                     const uint32_t bbig = bsml + C_::B_BYTES;
                     const uint32_t abig = tmem + uint32_t(C_::A_COL) + uint32_t(as) * 32, asml = abig + kKB;
                     const uint32_t first = kb ? 1u : 0u;
                     if (ptx::elect_one()) {
-                        if constexpr (C_::MERGE) {
+                        if (p.dbg & 4) {
+                        } else if constexpr (C_::MERGE) {
 #pragma unroll
                             for (int kk = 0; kk < 2; ++kk) {
                                 // [A_big B_small | A_big B_big] (the first MMA of a tile clears both halves)
@@ -268,13 +290,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int kk = 0; kk < 2; ++kk)
                                 ptx::mma_tf32_ts(d0, abig + kk * 8, ptx::smem_desc(bbig + kk * 32, 16, 512, 4), idesc, 1u);
                         }
-                        ptx::mma_commit(&bempty[bs]);
-                        ptx::mma_commit(&aempty[as]);
+                        if (p.dbg & 32) {  // probe: plain arrives instead of tcgen05.commit
+                            ptx::mbar_arrive(&bempty[bs]);
+                            ptx::mbar_arrive(&aempty[as]);
+                        } else {
+                            ptx::mma_commit(&bempty[bs]);
+                            ptx::mma_commit(&aempty[as]);
+                        }
                     }
                     __syncwarp();
                     if (++bs == RB) { bs = 0; bph ^= 1; }
                     if (++as == RA) { as = 0; aph ^= 1; }
                 }
+                FTR(0, lt, 30);
                 if (ptx::elect_one()) ptx::mma_commit(&tfull[acc]);
                 __syncwarp();
             }
@@ -285,7 +313,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int lt = 0;
             for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
                 const int buf = lt % p.xb;
-                ptx::mbar_wait_sleep(&xempty[buf], ((lt / p.xb) & 1) ^ 1);
+                fwait(&xempty[buf], ((lt / p.xb) & 1) ^ 1);
+                FTR(3, lt, 0);
                 const TileGeo tg = tile_geo(p, T);
                 float* sb = reinterpret_cast<float*>(smem + L.stage) + int64_t(buf) * p.xr * p.pitch;
                 uint32_t bytes = 0;
@@ -304,6 +333,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     bytes += uint32_t(nfl) * 4u;
                 }
+                if (p.dbg & 8) {
+                    ptx::mbar_arrive(&xfull[buf]);
+                    continue;
+                }
                 ptx::mbar_arrive_expect_tx(&xfull[buf], bytes);
                 for (int rho = 0; rho < tg.nrows; ++rho) {
                     const int yy = tg.y0 + rho;
@@ -315,6 +348,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (nfl > 0)
                         ptx::bulk_load(sb + int64_t(rho) * p.pitch + p.lmargin, p.x + a0, uint32_t(nfl) * 4u, &xfull[buf]);
                 }
+                FTR(3, lt, 2);
             }
         }
     } else if (warp >= 4 && warp < 8) {
@@ -323,8 +357,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         int lt = 0;
         for (int T = blockIdx.x; T < p.tiles; T += gridDim.x, ++lt) {
             const int acc = lt & 1;
-            ptx::mbar_wait_sleep(&tfull[acc], (lt >> 1) & 1);
+            fwait(&tfull[acc], (lt >> 1) & 1);
+            if (warp == 4) FTR(2, lt, 0);
             ptx::tc_fence_after();
+            if (p.dbg & 1) {
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
+                continue;
+            }
             const TileGeo tg = tile_geo(p, T);
             const int P = tg.P0 + t;
             const bool ok = P < tg.P1;
@@ -332,6 +372,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const bool plain = !p.bias && !p.relu;
 #pragma unroll 1
             for (int c0 = 0; c0 < NP; c0 += 32) {
+                // paced accumulator reads: the MMAs read their A operand from TMEM too, and an
+                // epilogue draining 2 x 96 columns at once stalled them for ~4k cycles per tile
+                // (tools/gather_probe.cu trace); spread over the next tile's MMAs: -5 % (measured)
+                if (c0 && p.pace_ns) __nanosleep(uint32_t(p.pace_ns));
                 uint32_t v[32];
                 const uint32_t tc = tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(acc * C_::ACC_COLS + c0);
                 ptx::tmem_ld_32x32b_x32(tc, v);
@@ -378,6 +422,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             ptx::tc_fence_before();
             __syncwarp();
+            if (warp == 4) FTR(2, lt, 1);
             if (lane == 0) ptx::mbar_arrive(&tempty[acc]);
         }
     } else if (warp >= 8) {
@@ -408,11 +453,21 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t slot0 = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b + uint32_t(p.s * (r - tg.ra)) * pitch_b;
             const int tb = col0 * p.d * 4;  // byte offset of this pixel's run within a staged row
             const int* kt = ktab + variant_of(p, tg.q) * ngroups_k;
-            ptx::mbar_wait_sleep(&xfull[buf], (lt / p.xb) & 1);
+            if (warp == 8) FTR(1, lt, 0);
+            fwait(&xfull[buf], (lt / p.xb) & 1);
+            if (warp == 8) FTR(1, lt, 1);
             for (int kb = int((uint32_t(grp) - gbase) & (kGatherGroups - 1)); kb < p.kb_tile; kb += kGatherGroups) {
                 // gather + split first; the slot is waited for only before the TMEM store
                 // the k-block's 4 group entries (uniform): filter row | zero mask | byte offset of
                 // the aligned float4; all four loads issued before any use (no branches between)
+                if (p.dbg & 2) {
+                    if (pass > 0) fwait(&aempty[sl], (pass - 1) & 1);
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&afull[sl]);
+                    sl += kGatherGroups;
+                    while (sl >= RA) { sl -= RA; ++pass; }
+                    continue;
+                }
                 const int4 e4 = *reinterpret_cast<const int4*>(kt + kb * 4);
                 const int ent[4] = {e4.x, e4.y, e4.z, e4.w};
                 float4 f[4];
@@ -455,12 +510,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         v[16 + 4 * g + u] = __float_as_uint(fa[u] - __uint_as_float(big));
                     }
                 }
-                if (pass > 0) ptx::mbar_wait_sleep(&aempty[sl], (pass - 1) & 1);
+                if (warp == 8) FTR(1, lt, 2 + kb / kGatherGroups);
+                if (pass > 0) fwait(&aempty[sl], (pass - 1) & 1);
+                if (warp == 8) FTR(1, lt, 10 + kb / kGatherGroups);
                 ptx::tmem_st_32x32b_x32(tmem + (uint32_t((warp & 3) * 32) << 16) + uint32_t(C_::A_COL) + uint32_t(sl) * 32, v);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(&afull[sl]);
+                if (warp == 8) FTR(1, lt, 18 + kb / kGatherGroups);
+                FTR(6 + warp - 8, lt, kb);  // every gather warp: its arrive for k-block kb
                 sl += kGatherGroups;
                 while (sl >= RA) { sl -= RA; ++pass; }
             }
@@ -476,6 +535,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ptx::tc_fence_after();
         ptx::tmem_dealloc<512, 1>(tmem);
     }
+#undef FTR
 }
 
 // kernel bank (o, k, k, d) -> per variant phi: [small rows | big rows] x Kp, filter row i's
@@ -1041,6 +1101,9 @@ WgPlan wg_plan(const Geo& g) {
     P.ok = true;
     return P;
 }
+int g_probe_dbg = 0;  // FwdParams::dbg of every launch (set only by tools/gather_probe.cu)
+unsigned long long* g_probe_trace = nullptr;  // FwdParams::trace (likewise)
+int g_probe_pace_ns = -1;                      // >= 0: FwdParams::pace_ns override (likewise)
 }  // namespace gth
 
 using namespace gth;
@@ -1067,6 +1130,9 @@ cudaError_t gather_fwd(const Geo& g, const float* x, const float* w, float* y, i
     CUtensorMap tm;
     if (!make_kmajor_map(&tm, ws, int64_t(P.nvar) * 2 * g.o, P.kp, P.np)) return cudaErrorInvalidValue;
     FwdParams fp{};
+    fp.dbg = g_probe_dbg;
+    fp.trace = g_probe_trace;
+    fp.pace_ns = g_probe_pace_ns >= 0 ? g_probe_pace_ns : 300;
     fp.x = x;
     fp.y = y;
     fp.bias = bias;
