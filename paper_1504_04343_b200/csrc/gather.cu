@@ -31,6 +31,11 @@
 #include "ptx.cuh"
 #include "reduce.cuh"
 
+// A/B builds (tools/build_variant.sh) override this default; the product is built with the measured best
+#ifndef CCT_FWD_PACE_NS
+#define CCT_FWD_PACE_NS 300
+#endif
+
 namespace cct {
 namespace gth {
 
@@ -1132,7 +1137,7 @@ cudaError_t gather_fwd(const Geo& g, const float* x, const float* w, float* y, i
     FwdParams fp{};
     fp.dbg = g_probe_dbg;
     fp.trace = g_probe_trace;
-    fp.pace_ns = g_probe_pace_ns >= 0 ? g_probe_pace_ns : 300;
+    fp.pace_ns = g_probe_pace_ns >= 0 ? g_probe_pace_ns : CCT_FWD_PACE_NS;
     fp.x = x;
     fp.y = y;
     fp.bias = bias;
