@@ -258,8 +258,9 @@ void one_pass(const G& g, int type, int pass, const cct_calibration* c, double* 
     };
     double t = 0, by = 0, launches = 0;
     // measured class rates (configs[1] sweep on the round-2 build, profiles/r02): the staged
-    // lift streams at ~0.88 and the plane expand at ~0.77 of the lower / col2im copy rate
-    const double lift_bw = c->hbm_bytes_per_s * 0.88, expand_bw = c->hbm_bytes_per_s * 0.77;
+    // relative to the lower / col2im copy rate: the bulk-copy lift streams at ~1.25 (5.3 TB/s) and
+    // the shift-copy expand at ~0.98 (4.1 TB/s) -- configs[1] sweep, profiles/r02/sweep_lowering_types_b256_r2final
+    const double lift_bw = c->hbm_bytes_per_s * 1.25, expand_bw = c->hbm_bytes_per_s * 0.98;
     auto hbm = [&](double b) { by += b; t += b / c->hbm_bytes_per_s; launches += 1; };
     auto hbm_at = [&](double b, double bw) { by += b; t += b / bw; launches += 1; };
     const double a_in = t1_implicit ? xin : dhat;         // bytes of the A operand stream

@@ -26,6 +26,7 @@
 
 #include "common.cuh"
 #include "lowering.cuh"
+#include "ptx.cuh"
 
 namespace cct {
 
@@ -165,6 +166,95 @@ __global__ void __launch_bounds__(kThreads) lift_staged_kernel(const float* __re
     }
 }
 
+// Bulk-staged variant: the block's contiguous run of tap planes arrives by one 1D bulk copy
+// (TMA engine, cp.async.bulk) into one of two shared-memory buffers while the block sums the
+// previous run out of the other -- HBM streams continuously, no load instructions.  The copy
+// starts at the 16-byte boundary below the run (off0 = 0..3 floats) and ends at the one above it,
+// except at the end of Rhat (`total` floats), whose last <= 3 floats are plain loads.  Same
+// summation order as lift_kernel (bit-identical).
+template <int TYPE, bool NHWC>
+__global__ void __launch_bounds__(kThreads) lift_bulk_kernel(const float* __restrict__ rh, float* __restrict__ y,
+                                                             Geo g, int gmax, int64_t total) {
+    extern __shared__ __align__(16) float smb[];  // 2 x (gmax x taps x rpi + 8) staged runs [+ NHWC outputs]
+    __shared__ __align__(8) uint64_t bar[2];
+    const int m = int(g.m), mm = m * m, o = int(g.o), k = int(g.k), s = int(g.s), R = int(g.R);
+    const int taps = TYPE == 2 ? k : k * k;
+    const int rpi = TYPE == 2 ? R * m : R * R;
+    const int blk_floats = taps * rpi;
+    const int buf_floats = (gmax * blk_floats + 8 + 3) & ~3;  // 16-byte aligned buffers
+    const int ngroups = (o + gmax - 1) / gmax;
+    const int64_t nblk = g.b * ngroups;
+    const float inv_mm = 1.f / float(mm), inv_m = 1.f / float(m);
+    float* acc_s = smb + 2 * buf_floats;
+    // run [a0, a1) floats of block blk, copied to 16-byte aligned [c0, c1) (c1 <= total rounded down)
+    auto span = [&](int64_t blk, int64_t& a0, int64_t& a1, int64_t& c0, int64_t& c1) {
+        const int64_t q = blk / ngroups;
+        const int oj0 = int(blk - q * ngroups) * gmax;
+        a0 = (q * o + oj0) * int64_t(blk_floats);
+        a1 = a0 + int64_t(min(gmax, o - oj0)) * blk_floats;
+        c0 = a0 & ~int64_t(3);
+        c1 = min((a1 + 3) & ~int64_t(3), total & ~int64_t(3));
+    };
+    auto issue = [&](int64_t blk, int b) {
+        int64_t a0, a1, c0, c1;
+        span(blk, a0, a1, c0, c1);
+        const uint32_t bytes = c1 > c0 ? uint32_t(c1 - c0) * 4u : 0u;
+        ptx::mbar_arrive_expect_tx(&bar[b], bytes);
+        if (bytes) ptx::bulk_load(smb + b * buf_floats, rh + c0, bytes, &bar[b]);
+    };
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(&bar[0], 1);
+        ptx::mbar_init(&bar[1], 1);
+        ptx::fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && blockIdx.x < nblk) issue(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+        const int b = it & 1;
+        if (threadIdx.x == 0 && blk + gridDim.x < nblk) issue(blk + gridDim.x, b ^ 1);
+        int64_t a0, a1, c0, c1;
+        span(blk, a0, a1, c0, c1);
+        const float* sm = smb + b * buf_floats + (a0 - c0);  // the run's first float
+        ptx::mbar_wait(&bar[b], uint32_t(it >> 1) & 1u);
+        if (c1 < a1) {  // end of Rhat: the last floats by plain loads
+            if (threadIdx.x == 0)
+                for (int64_t e = max(c1, a0); e < a1; ++e) smb[b * buf_floats + (e - c0)] = __ldg(rh + e);
+            __syncthreads();
+        }
+        const int64_t q = blk / ngroups;
+        const int oj0 = int(blk - q * ngroups) * gmax;
+        const int G = min(gmax, o - oj0);
+        for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+            const int gl = fdiv(e, mm, inv_mm), pix = e - gl * mm;
+            const int r = fdiv(pix, m, inv_m), c = pix - r * m;
+            const float* pl = sm + gl * blk_floats;
+            float a = 0.f;
+            if constexpr (TYPE == 2) {
+                const float* p0 = pl + s * r * m + c;
+                for (int i = 0; i < k; ++i) a += p0[i * (rpi + m)];
+            } else {
+                const float* p0 = pl + s * r * R + s * c;
+                for (int i = 0; i < k; ++i) {
+                    const float* pi = p0 + i * (k * rpi + R);
+                    for (int j = 0; j < k; ++j) a += pi[j * (rpi + 1)];
+                }
+            }
+            if constexpr (NHWC) acc_s[gl * mm + pix] = a;
+            else y[(q * o + oj0) * mm + e] = a;
+        }
+        if constexpr (NHWC) {
+            __syncthreads();
+            const float inv_g = 1.f / float(G);
+            for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+                const int pix = fdiv(e, G, inv_g), gl = e - pix * G;
+                y[(q * mm + pix) * o + oj0 + gl] = acc_s[gl * mm + pix];
+            }
+        }
+        __syncthreads();  // buffer b is refilled by the issue of iteration it + 1
+    }
+}
+
 // One block per (image, kG channels): the dy planes are staged in shared memory once; a thread
 // owns lowered rows (idx, idx + kThreads, ...) of an image's run, splits idx once, and writes
 // that row of every (channel, tap) column -- kG k^a independent stores per row, each warp a
@@ -221,6 +311,108 @@ __global__ void __launch_bounds__(kThreads) expand_planes_kernel(const float* __
         }
         __syncthreads();
     }
+}
+
+// Shift form of expand (T3 any stride, T2): column (channel gl, tap t) of an image's dRhat^T run is
+// the channel's *dilated padded plane* Z (dy[r][c] at (s r, s c) of an R x rw grid, zero
+// elsewhere, preceded by a zero guard of the largest tap shift) read at a constant shift:
+//   T3: out[Y R + X] = Z[guard + Y R + X - (i R + j)]     T2: out[Y m + c] = Z[guard + Y m + c - i m]
+// (X < j lands in the previous row's last k - 1 columns, which are zero: s (m - 1) = R - k).  A
+// block builds Z of its channels in shared memory once -- in four copies offset by 0..3 floats, so
+// that for every column one copy has the column's shift at the same 16-byte phase as the image's
+// run in global memory -- and every column is then a copy of aligned float4s (ld.shared.v4 /
+// st.global.v4, a scalar head and tail), no per-element index arithmetic.
+template <int TYPE, bool NHWC>
+__global__ void __launch_bounds__(kThreads) expand_shift_kernel(const float* __restrict__ dy, float* __restrict__ drt,
+                                                                Geo g, int64_t ldr, int gz) {
+    // [gz][4 phases][zl4]: copy f holds Z[p] at p + f; then 2 x gz x m^2: the dy planes of this
+    // block and (in flight, cp.async) of the block after it
+    extern __shared__ __align__(16) float zc[];
+    const int m = int(g.m), mm = m * m, o = int(g.o), k = int(g.k), s = int(g.s), R = int(g.R);
+    const int taps = TYPE == 2 ? k : k * k;
+    const int rw = TYPE == 2 ? m : R;
+    const int rpi = R * rw;
+    const int guard = TYPE == 2 ? (k - 1) * rw : (k - 1) * R + (k - 1);
+    const int zl4 = (guard + rpi + 3 + 3) & ~3;
+    const int ngroups = (o + gz - 1) / gz;
+    const int64_t nblk = g.b * ngroups;
+    float* sdy = zc + gz * 4 * zl4;
+    int* ctab = reinterpret_cast<int*>(sdy + 2 * gz * mm);  // gz x taps column offsets
+    const float inv_mm = 1.f / float(mm), inv_m = 1.f / float(m);
+    // consecutive blocks = consecutive images of one channel group
+    auto fetch = [&](int64_t blk, int buf) {  // the block's dy planes -> sdy[buf] (channel-major)
+        if (blk < nblk) {
+            const int64_t grp = blk / g.b, q = blk - grp * g.b;
+            const int oj0 = int(grp) * gz, G = min(gz, o - oj0);
+            const uint32_t dst = uint32_t(__cvta_generic_to_shared(sdy + buf * gz * mm));
+            if constexpr (NHWC) {
+                const float inv_g = 1.f / float(G);
+                for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+                    const int pix = fdiv(e, G, inv_g), gl = e - pix * G;
+                    ptx::cp_async4(dst + uint32_t(gl * mm + pix) * 4u, dy + (q * mm + pix) * o + oj0 + gl);
+                }
+            } else {
+                const float* src = dy + (q * o + oj0) * mm;
+                for (int e = threadIdx.x; e < G * mm; e += kThreads) ptx::cp_async4(dst + uint32_t(e) * 4u, src + e);
+            }
+        }
+        ptx::cp_async_commit();
+    };
+    fetch(blockIdx.x, 0);
+    int it = 0;
+    for (int64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x, ++it) {
+        const int64_t grp = blk / g.b, q = blk - grp * g.b;
+        const int oj0 = int(grp) * gz;
+        const int G = min(gz, o - oj0);
+        fetch(blk + gridDim.x, (it + 1) & 1);
+        {
+            float4* z4 = reinterpret_cast<float4*>(zc);
+            for (int e = threadIdx.x; e < G * zl4; e += kThreads) z4[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        ptx::cp_async_wait<1>();  // this block's planes (issued one iteration ago) landed
+        __syncthreads();
+        const float* sd = sdy + (it & 1) * gz * mm;
+        for (int e = threadIdx.x; e < G * mm; e += kThreads) {
+            const int gl = fdiv(e, mm, inv_mm), pix = e - gl * mm;
+            const int r = fdiv(pix, m, inv_m), c = pix - r * m;
+            const int pz = guard + (TYPE == 2 ? s * r * rw + c : s * r * R + s * c);
+            float* zg = zc + gl * 4 * zl4 + pz;
+            const float v = sd[e];
+#pragma unroll
+            for (int f = 0; f < 4; ++f) zg[f * zl4 + f] = v;
+        }
+        __syncthreads();
+        const int ga = int((q * rpi) & 3);          // 16-byte phase of the image's run (ldr % 4 == 0)
+        const int h = min((4 - ga) & 3, rpi);       // scalar head up to the boundary
+        const int nv = (rpi - h) >> 2, t0 = h + 4 * nv;
+        float* out0 = drt + int64_t(oj0) * taps * ldr + q * rpi;
+        const int ncol = G * taps;
+        // per column: offset of zs (zs[idx] = Z[guard - shift + idx] in the phase-matched copy)
+        for (int col = threadIdx.x; col < ncol; col += kThreads) {
+            const int gl = col / taps, t = col - gl * taps;
+            const int shift = TYPE == 2 ? t * rw : (t / k) * R + (t - (t / k) * k);
+            const int f = (ga - guard + shift) & 3;
+            ctab[col] = (gl * 4 + f) * zl4 + guard - shift + f;
+        }
+        __syncthreads();
+        // all (column, float4) pairs of the block over all threads: a warp stores 512 contiguous
+        // bytes of one column (or the seam of two), ld.shared.v4 conflict-free
+        const float inv_nv = 1.f / float(max(nv, 1));
+        for (int e = threadIdx.x; e < ncol * nv; e += kThreads) {
+            const int col = fdiv(e, nv, inv_nv), v = e - col * nv;
+            const int ix = h + 4 * v;
+            *reinterpret_cast<float4*>(out0 + int64_t(col) * ldr + ix) =
+                *reinterpret_cast<const float4*>(zc + ctab[col] + ix);
+        }
+        const int ht = h + (rpi - t0);  // scalar floats per column: head, then tail
+        for (int e = threadIdx.x; e < ncol * ht; e += kThreads) {
+            const int col = e / ht, u = e - col * ht;
+            const int ix = u < h ? u : t0 + (u - h);
+            out0[int64_t(col) * ldr + ix] = zc[ctab[col] + ix];
+        }
+        __syncthreads();
+    }
+    ptx::cp_async_wait<0>();
 }
 
 // Type 2 / 3 lowering (internal order, depth % 4 == 0): block per padded input row
@@ -289,6 +481,21 @@ cudaError_t lift_planes(const Geo& g, int type, const float* rhat, float* y, cud
     // per SM keep the load phase of one overlapping the sums of another)
     const int64_t blk_bytes = int64_t(taps) * rpi * 4;
     const int gmax = int(std::min<int64_t>(kG, (24 * 1024) / std::max<int64_t>(1, blk_bytes)));
+    if (gmax >= 1 && (reinterpret_cast<uintptr_t>(rhat) & 15) == 0 && g.b * g.o * int64_t(taps) * rpi < (int64_t(1) << 40)) {
+        // double-buffered bulk copies (buffer = the kernel's buf_floats)
+        const size_t buf = ((size_t(gmax) * size_t(taps * rpi) + 8 + 3) & ~size_t(3)) * 4;
+        const size_t smem = 2 * buf + (g.yl ? size_t(gmax) * size_t(g.m * g.m) * 4 : 0);
+        const int grid = blocks_for(g.b * ((g.o + gmax - 1) / gmax), 4);
+        const int64_t total = g.b * g.o * int64_t(taps) * rpi;
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            kern<<<grid, kThreads, smem, st>>>(rhat, y, g, gmax, total);
+        };
+        if (type == 2) g.yl ? go(lift_bulk_kernel<2, true>) : go(lift_bulk_kernel<2, false>);
+        else g.yl ? go(lift_bulk_kernel<3, true>) : go(lift_bulk_kernel<3, false>);
+        note_launch();
+        return cudaGetLastError();
+    }
     if (gmax >= 1) {
         const size_t smem = size_t(gmax) * size_t(blk_bytes) + (g.yl ? size_t(gmax) * size_t(g.m * g.m) * 4 : 0);
         if (smem <= 96 * 1024) {
@@ -320,14 +527,30 @@ cudaError_t expand_planes(const Geo& g, int type, const float* dy, float* drt, i
     const int taps = type == 2 ? int(g.k) : int(g.k * g.k);
     const int64_t rpi = type == 2 ? g.R * g.m : g.R * g.R;
     PhaseScope ps(kPhaseExpand, st, 0, 4.0 * double(g.b * g.o) * double(taps * rpi + g.m * g.m));
-    const size_t smem = size_t(kG) * size_t(g.m * g.m) * 4;
-    const int grid = blocks_for(g.b * ((g.o + kG - 1) / kG), 8);
-    auto go = [&](auto kern) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        kern<<<grid, kThreads, smem, st>>>(dy, drt, g, ldr);
-    };
-    if (type == 2) g.yl ? go(expand_planes_kernel<2, true>) : go(expand_planes_kernel<2, false>);
-    else g.yl ? go(expand_planes_kernel<3, true>) : go(expand_planes_kernel<3, false>);
+    // shift form when kG (or at least 2) channels' dy + dilated planes fit in 48 KB
+    const int64_t zl4 = ((type == 2 ? (g.k - 1) * g.m : (g.k - 1) * g.R + (g.k - 1)) + rpi + 6) & ~int64_t(3);
+    const int64_t per_ch = (4 * zl4 + 2 * g.m * g.m + (type == 2 ? g.k : g.k * g.k)) * 4;  // 4 Z copies, 2 dy planes, column table
+    const int gz = int(std::min<int64_t>(kG, (48 * 1024) / per_ch));
+    if (gz >= 2 && rpi < (1 << 22) && g.m * g.m < (1 << 20) && ldr % 4 == 0 &&
+        (reinterpret_cast<uintptr_t>(drt) & 15) == 0) {
+        const size_t smem = size_t(gz) * size_t(per_ch);
+        const int grid = blocks_for(g.b * ((g.o + gz - 1) / gz), 8);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            kern<<<grid, kThreads, smem, st>>>(dy, drt, g, ldr, gz);
+        };
+        if (type == 2) g.yl ? go(expand_shift_kernel<2, true>) : go(expand_shift_kernel<2, false>);
+        else g.yl ? go(expand_shift_kernel<3, true>) : go(expand_shift_kernel<3, false>);
+    } else {
+        const size_t smem = size_t(kG) * size_t(g.m * g.m) * 4;
+        const int grid = blocks_for(g.b * ((g.o + kG - 1) / kG), 8);
+        auto go = [&](auto kern) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+            kern<<<grid, kThreads, smem, st>>>(dy, drt, g, ldr);
+        };
+        if (type == 2) g.yl ? go(expand_planes_kernel<2, true>) : go(expand_planes_kernel<2, false>);
+        else g.yl ? go(expand_planes_kernel<3, true>) : go(expand_planes_kernel<3, false>);
+    }
     note_launch();
     // ldr padding rows (rows b*rpi .. ldr) of every column: zero (never read by a valid tile row,
     // but the GEMM's K / N tails read them)

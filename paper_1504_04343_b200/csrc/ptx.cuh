@@ -304,6 +304,14 @@ __device__ __forceinline__ void tmem_ld_wait() {
 
 // ---- 1D bulk copies (TMA engine, no tensor map) -----------------------------------
 // global -> shared, completion counted on an mbarrier (bytes, addresses 16-byte multiples)
+// 4-byte asynchronous global -> shared copy (LDGSTS) and its group fences
+__device__ __forceinline__ void cp_async4(uint32_t smem_addr, const void* gsrc) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_addr), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(

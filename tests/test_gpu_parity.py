@@ -180,6 +180,40 @@ def test_edge_shapes(cct, dev, orc, geom):
         assert rel_l2(dw, orc.conv_bwd_weight(x, dy, b, n, d, k, o, s, p)) <= TOL
 
 
+T23_GEOMS = [(13, 3, 8, 12, 3, 1, 1), (11, 5, 4, 20, 2, 2, 2), (15, 3, 4, 5, 3, 3, 0), (12, 4, 8, 9, 2, 4, 1),
+             (9, 1, 4, 7, 3, 2, 0), (27, 5, 4, 10, 1, 1, 2)]
+
+
+@pytest.mark.parametrize("layout", [0, 1], ids=["nchw", "nhwc"])
+@pytest.mark.parametrize("geom", T23_GEOMS, ids=[f"n{g[0]}k{g[1]}s{g[5]}p{g[6]}o{g[3]}" for g in T23_GEOMS])
+def test_t23_streaming_kernels(cct, dev, orc, geom, layout):
+    """The Type 2 / 3 streaming kernels -- lift from bulk-copied (double-buffered, 16-byte aligned
+    down / up) tap-plane runs, expand as shifted copies of the dilated padded dy plane -- over
+    strides 1-4, k = 1..5, partial channel groups (o not a multiple of the 8-channel block) and
+    runs that start at every float phase (odd plane sizes): fwd, bwd-data, bwd-weight against the
+    oracle, repeatable bit for bit."""
+    from paper_1504_04343_b200 import conv
+    n, k, d, o, b, s, p = geom
+    desc = cct.ConvDesc(n, k, d, o, b, s, p, layout)
+    m = desc.m
+    x_np, w_np = orc.random_problem(61 + n, b, n, d, k, o)
+    dy_np = orc.uniform(62 + n, b * o * m * m)
+    x, w = T(x_np, dev, b, n, n, d), T(w_np, dev, o, k, k, d)
+    dy = T(dy_np, dev, b, o, m, m)
+    if layout:
+        dy = dy.permute(0, 2, 3, 1).contiguous()
+    refs = (orc.conv_fwd(x_np, w_np, b, n, d, k, o, s, p), orc.conv_bwd_data(dy_np, w_np, b, n, d, k, o, s, p),
+            orc.conv_bwd_weight(x_np, dy_np, b, n, d, k, o, s, p))
+    for t in (2, 3):
+        y = conv.conv_fwd(x, w, desc, t)
+        dx = conv.conv_bwd_data(dy, w, desc, t)
+        dw = conv.conv_bwd_weight(x, dy, desc, t)
+        yc = y.permute(0, 3, 1, 2) if layout else y
+        for got, ref in zip((yc, dx, dw), refs):
+            assert rel_l2(got.contiguous().cpu().numpy().ravel(), ref) <= TOL, (t, geom)
+        assert torch.equal(conv.conv_fwd(x, w, desc, t), y) and torch.equal(conv.conv_bwd_data(dy, w, desc, t), dx)
+
+
 def test_auto_lowering_matches_oracle(cct, dev, orc):
     n, k, d, o, b, s, p = 13, 3, 64, 32, 2, 1, 1
     x, w = orc.random_problem(3, b, n, d, k, o)
