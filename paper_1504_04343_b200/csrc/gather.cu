@@ -1008,7 +1008,10 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
 #pragma unroll
                     for (int jj = 0; jj < kKB; ++jj) {
                         const bool second = jj >= split;
-                        float f = ptx::lds32((second ? rb1 : rb0) + uint32_t(jj) * sd4);
+                        // pixels past the tile's end (jj >= nval, warp-uniform) are not read: their
+                        // addresses can run past this row buffer into the one being refilled
+                        const float f0 = jj < nval ? ptx::lds32((second ? rb1 : rb0) + uint32_t(jj) * sd4) : 0.f;
+                        float f = f0;
                         bool ok = cok && jj < nval;
                         if constexpr (PAD) {
                             const int cc = second ? jj - split : c0 + jj;

@@ -50,9 +50,13 @@ def conv_case(name, n, k, d, o, b, s, p, types=(1, 2, 3), **tune):
             y = conv.conv_fwd(x, w, desc, t)
             dx = conv.conv_bwd_data(dy, w, desc, t)
             dw = conv.conv_bwd_weight(x, dy, desc, t)
+            # the combined backward (one call: shared expand; fused small-channel layers fork the
+            # backward-weight onto the side stream, CCT_TUNE_OVERLAP)
+            dx2, dw2 = conv.conv_bwd(dy, w, desc, t, x=x)
             torch.cuda.synchronize()
-            e = (rel(y, ry), rel(dx, rdx), rel(dw, rdw))
-            print(f"{name} T{t} {tune}: fwd {e[0]:.1e} dgrad {e[1]:.1e} wgrad {e[2]:.1e}", flush=True)
+            e = (rel(y, ry), rel(dx, rdx), rel(dw, rdw), rel(dx2, rdx), rel(dw2, rdw))
+            print(f"{name} T{t} {tune}: fwd {e[0]:.1e} dgrad {e[1]:.1e} wgrad {e[2]:.1e} "
+                  f"combined {e[3]:.1e} / {e[4]:.1e}", flush=True)
             assert max(e) <= TOL, (name, t, e)
 
 
@@ -107,6 +111,12 @@ def main():
     conv_case("gather_conv1", 227, 11, 3, 96, 8, 4, 0, types=(1,)); n += 1
     conv_case("gather_6mma", 227, 11, 3, 96, 8, 4, 0, types=(1,), gather=2); n += 1
     conv_case("gather_pad", 71, 11, 3, 64, 3, 4, 2, types=(1,)); n += 1
+    conv_case("gather_no_overlap", 71, 11, 3, 64, 3, 4, 2, types=(1,), overlap=0); n += 1
+    # Types 2 / 3 streaming kernels (bulk-copy lift, shift-copy expand): strides 2 and 3, odd plane
+    # sizes (runs at every 16-byte phase), partial channel groups
+    conv_case("t23_s2", 11, 5, 4, 20, 3, 2, 2, types=(2, 3)); n += 2
+    conv_case("t23_s3", 15, 3, 4, 13, 3, 3, 0, types=(2, 3)); n += 2
+    conv_case("t23_k1", 9, 1, 4, 7, 3, 2, 0, types=(2, 3)); n += 2
     print(f"SANITIZE_CASES_OK {n}", flush=True)
 
 
