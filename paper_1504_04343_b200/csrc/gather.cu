@@ -682,6 +682,8 @@ struct WgParams {
     int mt_tiles;            // M-tiles (ceil(kkd / 128))
     int tpi, tpx, tiles, chains;  // tiles per image, pixels per tile (whole output rows when m <= 128), total tiles, chains
     int pitch, lmargin, xr;  // staged rows (as the forward)
+    int xstride;             // floats per row buffer: xr rows + a guard band (the last k-block's reads
+                             // past the tile's end stay in it, not in the buffer being refilled)
     int xb;                  // row-stage buffers (2 or 3)
     int bstages, aslots;
 };
@@ -699,11 +701,11 @@ __host__ __device__ inline uint32_t wg_bstage_bytes(int np) { return uint32_t(np
 struct WgLayout {
     uint32_t ring, stage, bars, total;
 };
-__host__ __device__ inline WgLayout wg_layout(int np, int bstages, int aslots, int xr, int pitch, int xb) {
+__host__ __device__ inline WgLayout wg_layout(int np, int bstages, int aslots, int xstride, int xb) {
     WgLayout L;
     L.ring = 0;
     L.stage = uint32_t(bstages) * 2u * wg_bstage_bytes(np);
-    L.bars = (L.stage + uint32_t(xb) * uint32_t(xr) * uint32_t(pitch) * 4u + 15u) & ~15u;
+    L.bars = (L.stage + uint32_t(xb) * uint32_t(xstride) * 4u + 15u) & ~15u;
     L.total = L.bars + uint32_t(3 * bstages + 2 * aslots + 2 * xb + 4) * 8u + 16u;
     return L;
 }
@@ -732,7 +734,7 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
     uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
     constexpr uint32_t HB = NP * kKB * 4;  // one half (raw or small) of a dy stage
     const int RB = p.bstages, RA = p.aslots;
-    const WgLayout L = wg_layout(NP, RB, RA, p.xr, p.pitch, p.xb);
+    const WgLayout L = wg_layout(NP, RB, RA, p.xstride, p.xb);
     uint64_t* bfull = reinterpret_cast<uint64_t*>(smem + L.bars);
     uint64_t* btdone = bfull + RB;
     uint64_t* bempty = btdone + RB;
@@ -871,7 +873,7 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
                     wg_tile(p, T, q, P0, P1);
                     const int ra = P0 / p.m, rb = (P1 - 1) / p.m;
                     const int y0 = p.s * ra - p.p, nrows = p.s * (rb - ra) + p.k;
-                    float* sb = reinterpret_cast<float*>(smem + L.stage) + int64_t(buf) * p.xr * p.pitch;
+                    float* sb = reinterpret_cast<float*>(smem + L.stage) + int64_t(buf) * p.xstride;
                     uint32_t bytes = 0;
                     for (int rho = 0; rho < nrows; ++rho) {
                         const int yy = y0 + rho;
@@ -981,7 +983,7 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
                 wg_tile(p, T, q, P0, P1);
                 const int ra = P0 / p.m;
                 const int nkb = (P1 - P0 + kKB - 1) / kKB;
-                const uint32_t sbase = stage_u + uint32_t(buf) * uint32_t(p.xr) * pitch_b;
+                const uint32_t sbase = stage_u + uint32_t(buf) * uint32_t(p.xstride) * 4u;
                 ptx::mbar_wait_sleep(&xfull[buf], (lt / p.xb) & 1);
                 int r0 = P0 / p.m, c0 = P0 - r0 * p.m;  // first pixel of k-block kb
                 for (int kb = 0; kb < nkb; ++kb) {
@@ -1008,10 +1010,8 @@ __global__ void __launch_bounds__(wg_threads<MT>(), 1)
 #pragma unroll
                     for (int jj = 0; jj < kKB; ++jj) {
                         const bool second = jj >= split;
-                        // pixels past the tile's end (jj >= nval, warp-uniform) are not read: their
-                        // addresses can run past this row buffer into the one being refilled
-                        const float f0 = jj < nval ? ptx::lds32((second ? rb1 : rb0) + uint32_t(jj) * sd4) : 0.f;
-                        float f = f0;
+                        // (pixels past the tile's end read the buffer's guard band; discarded below)
+                        float f = ptx::lds32((second ? rb1 : rb0) + uint32_t(jj) * sd4);
                         bool ok = cok && jj < nval;
                         if constexpr (PAD) {
                             const int cc = second ? jj - split : c0 + jj;
@@ -1062,7 +1062,7 @@ bool make_mnmajor_map(CUtensorMap* map, const float* base, int64_t pixels, int64
 }
 
 struct WgPlan {
-    int np = 0, mt = 0, bstages = 0, aslots = 0, xr = 0, xb = 0, pitch = 0, lmargin = 0, tpi = 0, tpx = 0, tiles = 0,
+    int np = 0, mt = 0, bstages = 0, aslots = 0, xr = 0, xstride = 0, xb = 0, pitch = 0, lmargin = 0, tpi = 0, tpx = 0, tiles = 0,
         chains = 0, grid = 0;
     uint32_t smem = 0;
     bool ok = false;
@@ -1087,11 +1087,12 @@ WgPlan wg_plan(const Geo& g) {
     P.xr = int(g.s * (rows_span - 1) + g.k);
     P.lmargin = int((g.p * g.d + 4 + 3) & ~int64_t(3));
     P.pitch = int((P.lmargin + (g.n + g.p) * g.d + 8 + 3) & ~int64_t(3));
-    if (int64_t(P.xr) * P.pitch * 4 * 3 >= (int64_t(1) << 31)) return P;
+    P.xstride = int(int64_t(P.xr) * P.pitch + ((16 * g.s * g.d + 64 + 3) & ~int64_t(3)));
+    if (int64_t(P.xstride) * 4 * 3 >= (int64_t(1) << 31)) return P;
     // three row-stage buffers when they fit next to >= 6 dy stages, else two
     for (int xb = 3; xb >= 2 && !P.bstages; --xb)
         for (int st = 8; st >= (xb == 3 ? 6 : 2); --st) {
-            const WgLayout L = wg_layout(P.np, st, P.aslots, P.xr, P.pitch, xb);
+            const WgLayout L = wg_layout(P.np, st, P.aslots, P.xstride, xb);
             if (L.total + 1024 <= uint32_t(kSmemMax)) {
                 P.bstages = st;
                 P.xb = xb;
@@ -1222,6 +1223,7 @@ cudaError_t gather_wgrad(const Geo& g, const float* x, const float* dy, float* d
     wp.pitch = P.pitch;
     wp.lmargin = P.lmargin;
     wp.xr = P.xr;
+    wp.xstride = P.xstride;
     wp.bstages = P.bstages;
     wp.aslots = P.aslots;
     {
