@@ -200,11 +200,25 @@ def ref_types(a):
     return [int(a.lowering)] * len(CAFFENET_GEOM)
 
 
+def workload_config(a, world, per_gpu, global_images, types):
+    """The `config` both arms print for the same command line (same workload, so the driver's
+    same-config check holds); the reference arm's bounded sample is in its cpu_baseline."""
+    return {"workload": WORKLOAD,
+            "images_per_gpu": per_gpu, "global_batch": global_images,
+            "lowering": {g[0]: t for g, t in zip(CAFFENET_GEOM, types)},
+            "parallelism": f"dp{world} (batch split, NCCL all-reduce of dW)" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2 (step working set > 2 GB)",
+            "layout": a.layout,
+            **({"tune": a.tune} if a.tune else {})}
+
+
 def run_reference(a):
     world, rank, _ = dist_env()
     if rank != 0:
         return
     types = ref_types(a)
+    # the GPU arm's per-rank batch for the same flags (equal split of --global-batch, rank 0's share)
+    per_gpu = -(-a.global_batch // world) if a.global_batch else a.batch
     threads = min(os.cpu_count() or 1, 256)
     sample = a.cpu_sample or CPU_STACK_SAMPLE
     for _ in range(a.warmup):
@@ -220,10 +234,10 @@ def run_reference(a):
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": 1e3 * tot / a.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32 (fp64 accumulate)", "data": "synthetic U(-1,1), CaffeNet conv1-5 shapes",
-        "config": {"workload": WORKLOAD, "images_per_step": sample,
-                   "lowering": {g[0]: t for g, t in zip(CAFFENET_GEOM, types)}},
+        "config": workload_config(a, world, per_gpu, per_gpu * world if not a.global_batch else a.global_batch,
+                                  types),
         "cpu_baseline": {"value": v, "unit": UNIT, "cores": thr, "kind": kind, "cpu_model": cpu_model(),
-                         "sample": f"{sample} images of the conv1-5 stack per step (BASELINE.md section 3), "
+                         "sample": f"{sample} of the workload's images of the conv1-5 stack per step (BASELINE.md section 3), "
                                    f"fwd+bwd_data+bwd_weight, the reference's multiply (gemm.cpp:93) with {thr} "
                                    f"threads around the restated lowering; median step {1e3 * statistics.median(times):.0f} ms"},
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -487,13 +501,7 @@ def run_ours(a):
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f32 (3xTF32 tensor-core GEMMs, fp32 accumulate)",
             "data": "synthetic U(-1,1), CaffeNet conv1-5 shapes",
-            "config": {"workload": WORKLOAD,
-                       "images_per_gpu": st.batch, "global_batch": images,
-                       "lowering": {l.name: t for l, t in zip(st.layers, st.types)},
-                       "parallelism": f"dp{world} (batch split, NCCL all-reduce of dW)" if world > 1 else "single GPU",
-                       "l2": "inputs larger than L2 (step working set > 2 GB)",
-                       "layout": a.layout,
-                       **({"tune": a.tune} if a.tune else {})},
+            "config": workload_config(a, world, st.batch, images, list(st.types)),
             "tflops": tflops, "tflops_per_gpu": tflops / world,
             "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "cpu_baseline": cpu,
             "clocks": clk, "phases": phase, "configs": cfg,
