@@ -33,7 +33,7 @@
 
 // A/B builds (tools/build_variant.sh) override this default; the product is built with the measured best
 #ifndef CCT_FWD_PACE_NS
-#define CCT_FWD_PACE_NS 300
+#define CCT_FWD_PACE_NS 600
 #endif
 
 namespace cct {
