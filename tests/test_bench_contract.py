@@ -46,3 +46,10 @@ def test_reference_arm_never_loads_the_product():
     assert bench_line["cpu_baseline"]["kind"] in ("reference", "port")
     assert bench_line["config"]["workload"].startswith("caffenet conv1-5")
     assert probe == {"pkg": False, "libcct": False, "torch": False}
+    # the same config the B200 arm prints for the same flags (the driver's same-config check);
+    # the bounded CPU sample is described in cpu_baseline, not in config
+    import argparse
+    import bench
+    a = argparse.Namespace(layout="nhwc", tune="")
+    assert bench_line["config"] == json.loads(json.dumps(bench.workload_config(a, 1, 256, 256, list(bench.REF_TYPES))))
+    assert "1 of the workload's images" in bench_line["cpu_baseline"]["sample"]
