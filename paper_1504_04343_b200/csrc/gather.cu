@@ -35,6 +35,9 @@
 #ifndef CCT_FWD_PACE_NS
 #define CCT_FWD_PACE_NS 600
 #endif
+#ifndef CCT_FWD_MAX_STAGES  // kernel-bank ring depth cap of the forward (A/B diagnostics)
+#define CCT_FWD_MAX_STAGES 12
+#endif
 
 namespace cct {
 namespace gth {
@@ -626,7 +629,7 @@ FwdPlan fwd_plan(const Geo& g) {
     P.merge = tuning(CCT_TUNE_GATHER) != 2;  // 2: the 6-MMA form (A/B)
     P.aslots = max_aslots(P.np, P.merge);
     if (P.aslots < kGatherGroups) return P;
-    for (int st = 12; st >= 3; --st) {
+    for (int st = CCT_FWD_MAX_STAGES; st >= 3; --st) {
         const FwdLayout L = fwd_layout(P.np, st, P.aslots, P.xr, P.pitch, P.kb * 4, P.xb);
         if (L.total + 1024 <= uint32_t(kSmemMax)) {
             P.stages = st;
