@@ -381,6 +381,7 @@ __global__ void __launch_bounds__(kThreads) expand_shift_kernel(const float* __r
 #pragma unroll
             for (int f = 0; f < 4; ++f) zg[f * zl4 + f] = v;
         }
+        ptx::fence_proxy_async_smem();  // Z (generic-proxy writes) -> the bulk copies below read it
         __syncthreads();
         const int ga = int((q * rpi) & 3);          // 16-byte phase of the image's run (ldr % 4 == 0)
         const int h = min((4 - ga) & 3, rpi);       // scalar head up to the boundary
@@ -395,14 +396,13 @@ __global__ void __launch_bounds__(kThreads) expand_shift_kernel(const float* __r
             ctab[col] = (gl * 4 + f) * zl4 + guard - shift + f;
         }
         __syncthreads();
-        // all (column, float4) pairs of the block over all threads: a warp stores 512 contiguous
-        // bytes of one column (or the seam of two), ld.shared.v4 conflict-free
-        const float inv_nv = 1.f / float(max(nv, 1));
-        for (int e = threadIdx.x; e < ncol * nv; e += kThreads) {
-            const int col = fdiv(e, nv, inv_nv), v = e - col * nv;
-            const int ix = h + 4 * v;
-            *reinterpret_cast<float4*>(out0 + int64_t(col) * ldr + ix) =
-                *reinterpret_cast<const float4*>(zc + ctab[col] + ix);
+        // the aligned body of every column: one 1D bulk copy (TMA engine) shared -> global per
+        // column, 16-byte aligned at both ends (the phase-matched copy of Z), so the stores stream
+        // without per-thread store instructions while the threads write the scalar head / tail
+        if (nv > 0) {
+            for (int col = threadIdx.x; col < ncol; col += kThreads)
+                ptx::bulk_store(out0 + int64_t(col) * ldr + h, zc + ctab[col] + h, uint32_t(nv) * 16u);
+            ptx::bulk_commit();
         }
         const int ht = h + (rpi - t0);  // scalar floats per column: head, then tail
         for (int e = threadIdx.x; e < ncol * ht; e += kThreads) {
@@ -410,9 +410,11 @@ __global__ void __launch_bounds__(kThreads) expand_shift_kernel(const float* __r
             const int ix = u < h ? u : t0 + (u - h);
             out0[int64_t(col) * ldr + ix] = zc[ctab[col] + ix];
         }
+        ptx::bulk_wait_read();  // this thread's bulk copies have read Z before it is rebuilt
         __syncthreads();
     }
     ptx::cp_async_wait<0>();
+    ptx::bulk_wait_all();
 }
 
 // Type 2 / 3 lowering (internal order, depth % 4 == 0): block per padded input row
